@@ -1,0 +1,238 @@
+"""Generate the golden fixtures from the REFERENCE (run in the build container).
+
+    python tests/golden/make_golden.py
+
+Outputs (committed):
+  tests/golden/graphs/<motif>.sdfg.json   reference canonical JSON (serialization.to_json)
+  tests/golden/cases/<motif>__<case>.npz  inputs, symbols, interpreter outputs
+                                          (or the reference's error class name)
+
+Every output comes from ``sdfg.interpreter.run`` (interpreter.py:767-832), the
+reference's ground-truth executor; the reference's KATs
+(test_interpreter.py:45-82, test_acceptance.py:87-96) are reproduced as named
+cases.  Nothing here is imported by the product.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+import motifs_ref as M  # noqa: E402
+from sdfg.interpreter import run  # noqa: E402
+from sdfg.serialization import to_json  # noqa: E402
+
+GRAPHS = os.path.join(HERE, "graphs")
+CASES = os.path.join(HERE, "cases")
+
+F32 = np.float32
+
+
+def f32(a):
+    """fp32-representable float64 data (BASELINE inputs are fp32)."""
+    return np.asarray(a, dtype=F32).astype(np.float64)
+
+
+def save_graph(name, g):
+    os.makedirs(GRAPHS, exist_ok=True)
+    with open(os.path.join(GRAPHS, f"{name}.sdfg.json"), "w") as f:
+        json.dump(to_json(g), f, sort_keys=True, indent=1)
+
+
+def save_case(motif, case, g, arrays, symbols):
+    os.makedirs(CASES, exist_ok=True)
+    payload = {f"in__{k}": np.asarray(v) for k, v in arrays.items()}
+    payload["symbols"] = np.array(json.dumps({k: int(v) for k, v in symbols.items()}))
+    try:
+        rep = run(g, arrays, symbols)
+        for k, v in rep.outputs.items():
+            payload[f"out__{k}"] = v
+        payload["error"] = np.array("")
+    except Exception as exc:  # the reference's error class is part of the contract
+        payload["error"] = np.array(type(exc).__name__)
+        payload["error_msg"] = np.array(str(exc))
+    np.savez_compressed(os.path.join(CASES, f"{motif}__{case}.npz"), **payload)
+    print(f"{motif}__{case}: error={payload['error']}")
+
+
+def histogram_cases():
+    g = M.histogram()
+    save_graph("histogram", g)
+    rng = np.random.default_rng(0)
+    for case, (H, W) in {"16x16": (16, 16), "64x64": (64, 64), "1x1": (1, 1),
+                         "3x37": (3, 37)}.items():
+        img = f32(rng.random((H, W), dtype=F32))
+        save_case("histogram", case, g, {"img": img, "hist": np.zeros(256, np.int64)},
+                  {"H": H, "W": W})
+    # accumulate into existing contents (gallery.py:374-377 semantics)
+    img = f32(rng.random((8, 8), dtype=F32))
+    save_case("histogram", "accumulate", g,
+              {"img": img, "hist": rng.integers(0, 1000, 256).astype(np.int64)},
+              {"H": 8, "W": 8})
+    # exact bin boundaries k/256 and the largest fp32 below 1
+    edges = np.concatenate([np.arange(256) / 256.0,
+                            [np.nextafter(F32(1), F32(0))], [0.0]]).astype(F32)
+    save_case("histogram", "boundaries", g,
+              {"img": f32(edges.reshape(1, -1)), "hist": np.zeros(256, np.int64)},
+              {"H": 1, "W": edges.size})
+    # out-of-range bin -> reference raises OutOfBoundsError (interpreter.py:265-268)
+    bad = f32(np.array([[0.5, 1.0]], dtype=F32))
+    save_case("histogram", "oob_high", g, {"img": bad, "hist": np.zeros(256, np.int64)},
+              {"H": 1, "W": 2})
+    bad = f32(np.array([[-0.25, 0.5]], dtype=F32))
+    save_case("histogram", "oob_low", g, {"img": bad, "hist": np.zeros(256, np.int64)},
+              {"H": 1, "W": 2})
+
+    gi = M.histogram_int()
+    save_graph("histogram_int", gi)
+    from sdfg.gallery import fixture
+    fx = fixture("histogram")
+    for seed in range(3):
+        arrays, symbols = fx.make_inputs(np.random.default_rng(seed))
+        save_case("histogram_int", f"seed{seed}", gi, arrays, symbols)
+
+
+def query_cases():
+    g = M.query("<")
+    save_graph("query", g)
+    rng = np.random.default_rng(1)
+    for case, N in {"n4096": 4096, "n1": 1, "n1000": 1000, "n33": 33}.items():
+        col = f32(rng.random(N, dtype=F32))
+        save_case("query", case, g,
+                  {"col": col, "thr": np.array([0.5]), "out_vals": np.zeros(N),
+                   "count": np.zeros(1, np.int64)}, {"N": N})
+    N = 64
+    col = f32(rng.random(N, dtype=F32))
+    col[::7] = 0.5  # ties with the threshold are rejected by '<'
+    save_case("query", "ties_accumulate", g,
+              {"col": col, "thr": np.array([0.5]),
+               "out_vals": f32(rng.random(N, dtype=F32)),  # tail must stay untouched
+               "count": np.array([7], np.int64)}, {"N": N})
+    save_case("query", "none_pass", g,
+              {"col": np.ones(40), "thr": np.array([0.5]), "out_vals": np.full(40, 3.0),
+               "count": np.zeros(1, np.int64)}, {"N": 40})
+    save_case("query", "all_pass", g,
+              {"col": np.zeros(40), "thr": np.array([0.5]), "out_vals": np.zeros(40),
+               "count": np.zeros(1, np.int64)}, {"N": 40})
+    save_case("query", "n0", g,
+              {"col": np.zeros(0), "thr": np.array([0.5]), "out_vals": np.zeros(0),
+               "count": np.zeros(1, np.int64)}, {"N": 0})
+
+    gq = M.query_gallery()
+    save_graph("query_gallery", gq)
+    # KAT test_interpreter.py:76-82
+    save_case("query_gallery", "kat", gq,
+              {"col": np.array([1.0, 6.0, 3.0, 8.0]), "thr": np.array([5.0]),
+               "out_vals": np.zeros(4), "count": np.zeros(1, np.int64)}, {"N": 4})
+    from sdfg.gallery import fixture
+    fx = fixture("query")
+    for seed in range(3):
+        arrays, symbols = fx.make_inputs(np.random.default_rng(seed))
+        save_case("query_gallery", f"seed{seed}", gq, arrays, symbols)
+
+
+def spmv_inputs(rng, H, W, nnz_row, y_in=False):
+    cols = np.sort(rng.integers(0, W, size=(H, nnz_row)), axis=1).reshape(-1)
+    return ({"A_row": (np.arange(H + 1) * nnz_row).astype(np.int64),
+             "A_col": cols.astype(np.int64),
+             "A_val": f32(rng.random(H * nnz_row, dtype=F32)),
+             "x": f32(rng.random(W, dtype=F32)),
+             "b": f32(rng.random(H, dtype=F32)) if y_in else np.zeros(H)},
+            {"H": H, "W": W, "nnz": H * nnz_row})
+
+
+def spmv_cases():
+    g = M.spmv()
+    save_graph("spmv", g)
+    # KAT test_interpreter.py:56-67
+    save_case("spmv", "kat", g,
+              {"A_row": np.array([0, 1, 3], np.int64), "A_col": np.array([1, 0, 2], np.int64),
+               "A_val": np.array([2.0, 3.0, 4.0]), "x": np.array([1.0, 2.0, 3.0]),
+               "b": np.zeros(2)}, {"H": 2, "W": 3, "nnz": 3})
+    rng = np.random.default_rng(3)
+    a, s = spmv_inputs(rng, 128, 128, 16)
+    save_case("spmv", "h128_nnz16", g, a, s)
+    a, s = spmv_inputs(rng, 64, 200, 64, y_in=True)
+    save_case("spmv", "h64_nnz64_accumulate", g, a, s)
+    # ragged rows incl. empty rows
+    lens = np.array([0, 3, 0, 1, 7, 33, 0, 2])
+    rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(rowptr[-1])
+    save_case("spmv", "ragged", g,
+              {"A_row": rowptr, "A_col": rng.integers(0, 50, nnz).astype(np.int64),
+               "A_val": f32(rng.random(nnz, dtype=F32)), "x": f32(rng.random(50, dtype=F32)),
+               "b": np.zeros(8)}, {"H": 8, "W": 50, "nnz": nnz})
+    from sdfg.gallery import fixture
+    fx = fixture("spmv")
+    for seed in range(3):
+        arrays, symbols = fx.make_inputs(np.random.default_rng(seed))
+        save_case("spmv", f"gallery_seed{seed}", g, arrays, symbols)
+
+
+def jacobi_inputs(rng, N, border=False, distinct=False):
+    A = np.zeros((2, N, N), dtype=F32)
+    A[0, 1:N - 1, 1:N - 1] = rng.random((N - 2, N - 2), dtype=F32) if N > 2 else 0
+    if border:
+        A[0, 0, :] = rng.random(N, dtype=F32)
+        A[0, :, -1] = rng.random(N, dtype=F32)
+    A[1] = A[0]
+    if distinct:
+        A[1] = rng.random((N, N), dtype=F32)
+    return f32(A)
+
+
+def jacobi_cases():
+    g = M.jacobi2d()
+    save_graph("jacobi2d", g)
+    rng = np.random.default_rng(2)
+    for case, (N, T, kw) in {"n16_t3": (16, 3, {}), "n5_t1": (5, 1, {}),
+                             "n3_t2": (3, 2, {}), "n12_t0": (12, 0, {}),
+                             "n13_t4_border": (13, 4, {"border": True}),
+                             "n9_t3_distinct": (9, 3, {"distinct": True}),
+                             "n24_t6": (24, 6, {})}.items():
+        save_case("jacobi2d", case, g, {"A": jacobi_inputs(rng, N, **kw)}, {"N": N, "T": T})
+
+    gl = M.laplace1d()
+    save_graph("laplace1d", gl)
+    # KAT test_interpreter.py:45-49
+    save_case("laplace1d", "ramp", gl,
+              {"A": np.array([[0, 1, 2, 3, 4], [0, 0, 0, 0, 0]], dtype=float)}, {"N": 5, "T": 1})
+
+
+def matmul_cases():
+    for name, b in (("matmul", M.matmul), ("matmul_raw", M.matmul_raw),
+                    ("matmul_tiled", M.BUILDERS["matmul_tiled"]),
+                    ("matmul_chain", M.BUILDERS["matmul_chain"])):
+        g = b()
+        save_graph(name, g)
+    g = M.matmul()
+    rng = np.random.default_rng(4)
+    for case, (m, n, k) in {"16x16x16": (16, 16, 16), "5x7x3": (5, 7, 3),
+                            "1x1x1": (1, 1, 1), "24x8x40": (24, 8, 40)}.items():
+        save_case("matmul", case, g,
+                  {"A": f32(rng.random((m, k), dtype=F32)), "B": f32(rng.random((k, n), dtype=F32)),
+                   "C": f32(rng.random((m, n), dtype=F32))}, {"M": m, "N": n, "K": k})
+    # KAT test_interpreter.py:69-74 (identity operand)
+    save_case("matmul", "identity", g,
+              {"A": np.eye(2), "B": np.array([[1.0, 2.0], [3.0, 4.0]]), "C": np.zeros((2, 2))},
+              {"M": 2, "N": 2, "K": 2})
+    for name in ("matmul_raw", "matmul_tiled", "matmul_chain"):
+        gg = {"matmul_raw": M.matmul_raw, "matmul_tiled": M.BUILDERS["matmul_tiled"],
+              "matmul_chain": M.BUILDERS["matmul_chain"]}[name]()
+        save_case(name, "6x9x5", gg,
+                  {"A": f32(rng.random((6, 5), dtype=F32)), "B": f32(rng.random((5, 9), dtype=F32)),
+                   "C": np.zeros((6, 9))}, {"M": 6, "N": 9, "K": 5})
+
+
+if __name__ == "__main__":
+    histogram_cases()
+    query_cases()
+    spmv_cases()
+    jacobi_cases()
+    matmul_cases()
