@@ -1,0 +1,552 @@
+#!/usr/bin/env python3
+"""bench.py -- B200 throughput of the SDFG Map/WCR/stream motifs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--motif M|all] [--impl ours|reference]
+
+One JSON line on rank 0.  The headline workload is BASELINE.json configs[1]
+(Query: filter x < 0.5 over 2^26 fp32 via stream push); every other config
+is measured too and reported under "motifs".  A step = one execution of the
+motif's SDFG on one batch of synthetic input resident in HBM; the Jacobi step
+is the whole T=1000 time loop.  "e2e" repeats the headline through the
+reference-facing C ABI host entry (reference types, host pinned buffers,
+H2D + kernels + D2H inside the timed region).
+
+--impl reference times the reference's own CPU path: the C its code
+generator emits for the same SDFG, compiled with its own toolchain flags
+(oracle/_ref, built by oracle/make_ref.py), run on all host cores by
+partitioning the map's outer range across threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "per-motif GB/s (hist/query/SpMV/Jacobi), MM TFLOP/s vs roofline, 1/2/4/8 GPU"
+HEADLINE = "query"
+ALL = ["histogram", "query", "spmv", "jacobi2d", "gemm4096", "gemm16384"]
+
+
+def peaks():
+    try:
+        p = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+        return {"hbm": p["hbm_gbs"], "bf16": p["bf16_tflops"], "bf16_sus": p["bf16_tflops_sustained"],
+                "src": "measured"}
+    except Exception:
+        return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
+
+
+def traffic_table():
+    try:
+        return json.load(open(os.path.join(REPO, "profiles", "ncu_traffic.json")))
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for ln in open(self.path):
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except Exception:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except Exception:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- dist
+
+class Dist:
+    def __init__(self, gpus):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if gpus != self.world:
+            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={self.world}; launch with torchrun for N>1")
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v):
+        if not self.pg:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------- timing
+
+def time_steps(step, steps, warmup, dist, stream=None):
+    """W untimed steps, then K steps between CUDA events on the launching
+    stream, barrier + synchronize on both sides; max over ranks."""
+    import torch
+    s = stream or torch.cuda.current_stream()
+    for k in range(warmup):
+        step(k)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for k in range(steps):
+        step(warmup + k)
+    b.record(s)
+    b.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    return dist.max(a.elapsed_time(b) / steps)
+
+
+def time_host(step, steps, warmup, dist):
+    """Wall time of synchronous host-entry steps (e2e), max over ranks."""
+    for k in range(warmup):
+        step(k)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        step(warmup + k)
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    dist.barrier()
+    return dist.max(ms)
+
+
+def pinned(shape, dtype):
+    import torch
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+# ---------------------------------------------------------------- motifs
+# Algorithmic bytes = compulsory footprint of the propagated memlet subsets
+# x element size.
+
+def bench_histogram(args, dist, P):
+    import torch
+    from paper_1902_10345_b200 import device, _lib
+    H = W = 4096
+    nbuf = 4  # 4 x 67 MB > 126 MB L2: every step streams from HBM
+    g = torch.Generator(device="cuda").manual_seed(0 + dist.rank)
+    imgs = [torch.rand(H, W, device="cuda", generator=g) for _ in range(nbuf)]
+    hist = torch.zeros(256, dtype=torch.int64, device="cuda")
+    oob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    reduce_ = dist.pg is not None
+
+    def step(k):
+        device.hist(imgs[k % nbuf], hist, oob)
+        if reduce_:  # per-GPU partial bins -> allreduce (NCCL)
+            dist.pg.all_reduce(hist)
+
+    ms = time_steps(step, args.steps, args.warmup, dist)
+    assert oob.item() == 0
+    by = 4 * H * W + 2 * 256 * 8
+    out = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms,
+           "bytes_per_unit": by, "launches_per_step": 1,
+           "roofline": roof("hbm", by / ms / 1e6, P, "hist_smem_kernel"),
+           "l2": f"{nbuf} rotating 64 MiB inputs (> 126 MB L2)",
+           "config": {"workload": "Histogram 4096x4096 fp32, 256 bins (configs[0])", "H": H, "W": W,
+                      "bins": 256}}
+    if args.e2e:
+        himg = pinned((H, W), torch.float64)
+        himg.copy_(imgs[0].double().cpu())
+        hh = pinned(256, torch.int64)
+        hh.zero_()
+        L = _lib.load()
+
+        def hstep(k):
+            _lib.check(L.sdfgb_host_histogram(ctypes.c_void_p(himg.data_ptr()), ctypes.c_void_p(hh.data_ptr()),
+                                              H, W, 256, 256.0, 1.0, _lib.PREC_FP32))
+        ems = time_host(hstep, max(2, args.steps // 2), 1, dist)
+        out["e2e"] = {"value": dist.world * by / ems / 1e6, "unit": "GB/s", "ms_per_step": ems,
+                      "h2d_bytes_per_step": himg.numel() * 8 + 256 * 8, "d2h_bytes_per_step": 256 * 8 + 8}
+    return out
+
+
+def bench_query(args, dist, P):
+    import torch
+    from paper_1902_10345_b200 import device, _lib
+    n = 1 << 26
+    g = torch.Generator(device="cuda").manual_seed(1 + dist.rank)
+    col = torch.rand(n, device="cuda", generator=g)
+    out = torch.empty(n, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = device.query_workspace(n, 4)
+    offsets = dist.pg is not None
+
+    def step(k):
+        device.query(col, 0.5, out, cnt, ws, "<")
+        if offsets:  # per-shard compaction; global offsets from an all-gather of counts
+            allc = torch.empty(dist.world, dtype=torch.int64, device="cuda")
+            dist.pg.all_gather_into_tensor(allc, cnt)
+
+    ms = time_steps(step, args.steps, args.warmup, dist)
+    nsel = int(cnt.item()) // (args.steps + args.warmup)
+    by = 4 * n + 4 * nsel + 8
+    res = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms, "bytes_per_unit": by,
+           "launches_per_step": 1, "roofline": roof("hbm", by / ms / 1e6, P, "query_kernel"),
+           "l2": "input 256 MiB > L2",
+           "config": {"workload": "Query x < 0.5 over 2^26 fp32 (configs[1])", "N": n, "selected": nsel}}
+    if args.e2e:
+        hcol = pinned(n, torch.float64)
+        hcol.copy_(col.double().cpu())
+        hout = pinned(n, torch.float64)
+        hthr = pinned(1, torch.float64)
+        hthr.fill_(0.5)
+        hcnt = pinned(1, torch.int64)
+        L = _lib.load()
+
+        def hstep(k):
+            hcnt.zero_()
+            _lib.check(L.sdfgb_host_query(ctypes.c_void_p(hcol.data_ptr()), ctypes.c_void_p(hthr.data_ptr()),
+                                          ctypes.c_void_p(hout.data_ptr()), ctypes.c_void_p(hcnt.data_ptr()),
+                                          n, 0, _lib.PREC_FP32))
+        ems = time_host(hstep, max(2, args.steps // 2), 1, dist)
+        res["e2e"] = {"value": dist.world * by / ems / 1e6, "unit": "GB/s", "ms_per_step": ems,
+                      "h2d_bytes_per_step": n * 8 + 16, "d2h_bytes_per_step": int(hcnt.item()) * 8 + 8}
+    return res
+
+
+def bench_spmv(args, dist, P):
+    import torch
+    from paper_1902_10345_b200 import device, _lib
+    H = W = 1 << 22
+    nz = 64
+    g = torch.Generator(device="cuda").manual_seed(3 + dist.rank)
+    col = torch.sort(torch.randint(0, W, (H, nz), device="cuda", generator=g, dtype=torch.int32), dim=1)[0]
+    col = col.reshape(-1).contiguous()
+    val = torch.rand(H * nz, device="cuda", generator=g)
+    x = torch.rand(W, device="cuda", generator=g)
+    rowptr = (torch.arange(H + 1, device="cuda", dtype=torch.int64) * nz).to(torch.int32)
+    b = torch.zeros(H, device="cuda")
+
+    def step(k):
+        device.spmv(rowptr, col, val, x, b)
+
+    ms = time_steps(step, args.steps, args.warmup, dist)
+    nnz = H * nz
+    by = nnz * 8 + 4 * (H + 1) + 4 * W + 8 * H
+    res = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms, "bytes_per_unit": by,
+           "launches_per_step": 1, "roofline": roof("hbm", by / ms / 1e6, P, "spmv_warp_row_kernel"),
+           "l2": "matrix 2 GiB > L2 (x, 16 MiB, is L2-resident by design)",
+           "config": {"workload": "CSR SpMV 2^22 x 2^22, 64 nnz/row fp32/int32", "H": H, "nnz": nnz}}
+    if args.e2e:
+        L = _lib.load()
+        hrow = pinned(H + 1, torch.int64)
+        hrow.copy_(rowptr.long().cpu())
+        hcol = pinned(nnz, torch.int64)
+        hcol.copy_(col.long().cpu())
+        hval = pinned(nnz, torch.float64)
+        hval.copy_(val.double().cpu())
+        hx = pinned(W, torch.float64)
+        hx.copy_(x.double().cpu())
+        hb = pinned(H, torch.float64)
+        hb.zero_()
+
+        def hstep(k):
+            _lib.check(L.sdfgb_host_spmv(*(ctypes.c_void_p(t.data_ptr()) for t in (hrow, hcol, hval, hx, hb)),
+                                         H, W, nnz, _lib.PREC_FP32))
+        ems = time_host(hstep, 2, 1, dist)
+        res["e2e"] = {"value": dist.world * by / ems / 1e6, "unit": "GB/s", "ms_per_step": ems,
+                      "h2d_bytes_per_step": (H + 1) * 8 + nnz * 16 + W * 8 + H * 8, "d2h_bytes_per_step": H * 8}
+        del hrow, hcol, hval, hx, hb
+    return res
+
+
+def bench_jacobi(args, dist, P):
+    import torch
+    from paper_1902_10345_b200 import device, _lib
+    N, T = 8192, 1000
+    g = torch.Generator(device="cuda").manual_seed(2 + dist.rank)
+    A = torch.zeros(2, N, N, device="cuda")
+    A[0, 1:-1, 1:-1] = torch.rand(N - 2, N - 2, device="cuda", generator=g)
+    A[1] = A[0]
+
+    def step(k):
+        device.jacobi2d(A, T)
+
+    steps = max(1, min(args.steps, 3))
+    ms = time_steps(step, steps, 1, dist)
+    per = 4 * N * N + 4 * (N - 2) * (N - 2)
+    by = per * T
+    res = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms, "bytes_per_unit": by,
+           "launches_per_step": T, "roofline": roof("hbm", per / (ms / T) / 1e6, P, "jacobi_step_kernel"),
+           "l2": "2 x 256 MiB planes > L2",
+           "config": {"workload": "Jacobi-2D 8192^2 fp32, T=1000 (whole time loop per step)", "N": N, "T": T},
+           "steps": steps, "warmup": 1}
+    if args.e2e:
+        L = _lib.load()
+        hA = pinned((2, N, N), torch.float64)
+        hA.copy_(A.double().cpu())
+        from paper_1902_10345_b200.device import JACOBI5, _terms
+        di, dj = _terms(JACOBI5)
+
+        def hstep(k):
+            _lib.check(L.sdfgb_host_jacobi2d(ctypes.c_void_p(hA.data_ptr()), N, T, 0.2, di, dj, 5, _lib.PREC_FP32))
+        ems = time_host(hstep, 1, 0, dist)
+        res["e2e"] = {"value": dist.world * by / ems / 1e6, "unit": "GB/s", "ms_per_step": ems,
+                      "h2d_bytes_per_step": 2 * N * N * 8, "d2h_bytes_per_step": 2 * N * N * 8}
+    return res
+
+
+def bench_gemm(n, args, dist, P):
+    import torch
+    from paper_1902_10345_b200 import device, _lib
+    g = torch.Generator(device="cuda").manual_seed(4 + dist.rank)
+    A = torch.rand(n, n, device="cuda", generator=g)
+    B = torch.rand(n, n, device="cuda", generator=g)
+    C = torch.empty(n, n, device="cuda")
+    ws = device.gemm_workspace(n, n, n)
+
+    def step(k):
+        device.gemm(A, B, C, ws)
+
+    steps = max(2, min(args.steps, 10 if n <= 4096 else 4))
+    ms = time_steps(step, steps, args.warmup, dist)
+    fl = 2.0 * n ** 3
+    tf = fl / ms / 1e9
+    sustained = n > 8192
+    pk = (P["bf16_sus"] if sustained else P["bf16"]) / 2 / 3
+    res = {"value": dist.world * tf, "unit": "TFLOP/s", "ms_per_step": ms, "flops_per_unit": fl,
+           "launches_per_step": 3,
+           "roofline": {"bound": "tensor", "achieved": tf, "peak": pk, "unit": "TFLOP/s", "frac": tf / pk,
+                        "peak_note": f"3xTF32 = {'sustained' if sustained else 'burst'} bf16 / 2 / 3 ({P['src']})",
+                        "achieved_note": "includes the hi/lo split pre-pass",
+                        "traffic": traffic_table().get("gemm_3xtf32_kernel")},
+           "l2": "operands + split workspace > L2" if n >= 4096 else "",
+           "config": {"workload": f"MM fp32 {n}^3 via tcgen05 3xTF32", "M": n, "N": n, "K": n},
+           "steps": steps}
+    if args.e2e and n <= 4096:
+        L = _lib.load()
+        hA = pinned((n, n), torch.float64)
+        hA.copy_(A.double().cpu())
+        hB = pinned((n, n), torch.float64)
+        hB.copy_(B.double().cpu())
+        hC = pinned((n, n), torch.float64)
+
+        def hstep(k):
+            _lib.check(L.sdfgb_host_matmul(ctypes.c_void_p(hA.data_ptr()), ctypes.c_void_p(hB.data_ptr()),
+                                           ctypes.c_void_p(hC.data_ptr()), n, n, n))
+        ems = time_host(hstep, 2, 1, dist)
+        res["e2e"] = {"value": dist.world * fl / ems / 1e9, "unit": "TFLOP/s", "ms_per_step": ems,
+                      "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * n * 8}
+    return res
+
+
+def roof(bound, achieved, P, kernel):
+    pk = P["hbm"]
+    return {"bound": bound, "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
+            "peak_note": f"{P['src']} HBM copy bandwidth (MEASURED_PEAKS.json)",
+            "frac_of_8TBs_spec": achieved / 8000.0,
+            "traffic": traffic_table().get(kernel)}
+
+
+# ---------------------------------------------------------------- CPU arm
+
+def ref_lib(key):
+    man_p = os.path.join(REPO, "oracle", "_ref", "manifest.json")
+    if not os.path.exists(man_p):
+        return None
+    m = json.load(open(man_p))[key]
+    L = ctypes.CDLL(os.path.join(REPO, "oracle", "_ref", m["lib"]))
+    fn = getattr(L, m["entry"])
+    fn.restype = None
+    return fn
+
+
+def _threads():
+    return max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 1)
+
+
+def _par(fn, parts):
+    th = [threading.Thread(target=fn, args=p) for p in parts]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+
+
+def cpu_query(reps=2):
+    """The reference's generated query C (oracle/_ref) on all host cores:
+    the map's range is split into contiguous chunks, one C call per chunk
+    (the stream drain keeps per-chunk order, chunks are concatenated)."""
+    n = 1 << 26
+    fn = ref_lib("query")
+    kind = "reference"
+    if fn is None:
+        kind = "port"
+    col = np.random.default_rng(1).random(n, dtype=np.float32).astype(np.float64)
+    out = np.empty(n)
+    thr = np.array([0.5])
+    T = _threads()
+    bounds = np.linspace(0, n, T + 1).astype(np.int64)
+    counts = np.zeros((T, 1), np.int64)
+    if fn is None:
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import oracle
+
+    def work(i):
+        a, b = int(bounds[i]), int(bounds[i + 1])
+        if fn is not None:
+            fn(ctypes.c_void_p(col.ctypes.data + 8 * a), ctypes.c_void_p(thr.ctypes.data),
+               ctypes.c_void_p(out.ctypes.data + 8 * a), ctypes.c_void_p(counts[i].ctypes.data),
+               ctypes.c_int64(b - a))
+        else:
+            oracle.lib().orc_query_f64(col.ctypes.data + 8 * a, b - a, 0, 0.5, out.ctypes.data + 8 * a,
+                                       counts[i].ctypes.data)
+    best = 1e30
+    for _ in range(reps):
+        counts[:] = 0
+        t0 = time.perf_counter()
+        _par(work, [(i,) for i in range(T)])
+        best = min(best, time.perf_counter() - t0)
+    nsel = int(counts.sum())
+    by = 4 * n + 4 * nsel + 8
+    return {"value": by / best / 1e9, "unit": "GB/s", "cores": T, "kind": kind,
+            "sample": f"full 2^26 query, {T} threads x contiguous chunks of the map range, best of {reps}",
+            "seconds": best}
+
+
+# ---------------------------------------------------------------- main
+
+def run_reference(args):
+    dist_rank = int(os.environ.get("RANK", "0"))
+    if dist_rank != 0:
+        return 0
+    r = cpu_query(reps=max(1, min(args.steps, 3)))
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "Query x < 0.5 over 2^26 (configs[1]), reference-generated C on host cores"},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--motif", default="all")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    dist = Dist(args.gpus)
+    torch.cuda.set_device(dist.local)
+    P = peaks()
+    motifs = ALL if args.motif == "all" else args.motif.split(",")
+    if HEADLINE not in motifs:
+        motifs = [HEADLINE] + motifs
+    results = {}
+    with ClockSampler(dist.local) as clk:
+        for m in motifs:
+            if m == "histogram":
+                results[m] = bench_histogram(args, dist, P)
+            elif m == "query":
+                results[m] = bench_query(args, dist, P)
+            elif m == "spmv":
+                results[m] = bench_spmv(args, dist, P)
+            elif m == "jacobi2d":
+                results[m] = bench_jacobi(args, dist, P)
+            elif m.startswith("gemm"):
+                results[m] = bench_gemm(int(m[4:]), args, dist, P)
+            torch.cuda.empty_cache()
+    clocks = clk.summary()
+    h = results[HEADLINE]
+    line = {
+        "metric": METRIC, "value": h["value"], "unit": h["unit"], "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded torch.rand on device)",
+        "config": dict(h["config"], l2=h["l2"], parallelism=f"shards{dist.world}"),
+        "roofline": h["roofline"], "e2e": h.get("e2e"), "gpu_launches": h["launches_per_step"] * args.steps,
+        "clocks": clocks,
+        "motifs": {k: {kk: vv for kk, vv in v.items()} for k, v in results.items()},
+    }
+    if dist.rank == 0 and args.cpu:
+        line["cpu_baseline"] = {k: v for k, v in cpu_query(reps=1).items() if k != "seconds"}
+    if dist.rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,166 @@
+/*
+ * sdfgb200.h -- C ABI of libsdfgb200.so, the B200 (sm_100a) execution backend
+ * for SDFG Map scopes with write-conflict resolution (WCR) and stream memlets.
+ *
+ * The reference (arXiv 1902.10345 SDFG toolkit, /root/reference/pkg) has no
+ * native library: its CPU dispatcher EMITS one C function per graph,
+ *     void <sdfg.name>(T* container..., int64_t symbol...)      codegen.py:839-846
+ * with containers = non-transient arrays in Sdfg.data order and symbols in
+ * Sdfg.symbols order (codegen.py:620-627), compiles it with cc -shared
+ * (codegen.py:890-913) and binds it through ctypes in CompiledSdfg.run
+ * (codegen.py:866-887).  This library is what that ctypes binding calls
+ * instead when an SDFG state was matched by GPUTransformMap:
+ *
+ *   1. host entries  (sdfgb_host_*): the drop-in for CompiledSdfg._fn --
+ *      host pointers in the reference's own types (double*, int64_t*),
+ *      synchronous, containers in the reference's argument order.
+ *   2. device entries (sdfgb_*): device pointers, asynchronous on a CUDA
+ *      stream passed as void* -- the timed path and the multi-GPU building
+ *      block (one process per GPU; collectives live above this ABI).
+ *
+ * Conventions
+ *   - Every entry returns SDFGB_OK (0) or an error code; the message is in
+ *     sdfgb_last_error() (thread-local).  The reference's entry returns void
+ *     and reports failures as Python exceptions (CodegenError, ToolchainError,
+ *     interpreter OutOfBoundsError, interpreter.py:56-57,265-268); the Python
+ *     layer maps these codes onto exceptions with the same names.
+ *   - WCR targets ACCUMULATE into existing contents, exactly like the
+ *     reference (hist_out = hist_in + counts, gallery.py:374-377;
+ *     count += n; b += A x).  Nothing is zeroed implicitly.
+ *   - Precision: *_f32 entries compute in fp32 (BASELINE.json configs);
+ *     *_f64 / *_i64 entries compute in the reference's own basetypes
+ *     (ir.py:33-35).
+ *   - No entry falls back to the CPU.  Without a usable CUDA device every
+ *     entry fails with SDFGB_ERR_CUDA.
+ */
+#ifndef SDFGB200_H
+#define SDFGB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDFGB_ABI_VERSION 1
+
+#define SDFGB_OK 0
+#define SDFGB_ERR_INVALID 1     /* bad argument / unsupported shape        */
+#define SDFGB_ERR_CUDA 2        /* CUDA runtime / launch failure            */
+#define SDFGB_ERR_OOB 3         /* out-of-bounds WCR index (OutOfBoundsError) */
+#define SDFGB_ERR_WORKSPACE 4   /* workspace too small                       */
+
+/* comparison operators of a stream-push predicate (tasklets.py _CMPOPS) */
+#define SDFGB_CMP_LT 0
+#define SDFGB_CMP_LE 1
+#define SDFGB_CMP_GT 2
+#define SDFGB_CMP_GE 3
+#define SDFGB_CMP_EQ 4
+#define SDFGB_CMP_NE 5
+
+/* ---------------------------------------------------------------- misc */
+int sdfgb_abi_version(void);
+const char* sdfgb_last_error(void);
+int sdfgb_device_count(int* count);
+/* Pinned host memory for zero-staging H2D/D2H in the host entries. */
+int sdfgb_host_alloc(void** ptr, size_t bytes);
+int sdfgb_host_free(void* ptr);
+
+/* ------------------------------------------------------ device entries */
+
+/* Histogram, WCR sum with a dynamic subscript (tasklets.py:297-300 ->
+ * interpreter.py:262-278; codegen.py:733-747).  For each element v:
+ *     k = floor((double)v * scale / div)          (f32/f64;  bi = v*S//D)
+ *     k = v                                       (i64;      h[v] = 1)
+ *     hist[k] += 1         for 0 <= k < bins, else *oob += 1 (not counted)
+ * hist is int64 device memory (the reference container type). */
+int sdfgb_hist_f32(const float* img, int64_t n, double scale, double div,
+                   int64_t* hist, int64_t bins, uint64_t* oob, void* stream);
+int sdfgb_hist_f64(const double* img, int64_t n, double scale, double div,
+                   int64_t* hist, int64_t bins, uint64_t* oob, void* stream);
+int sdfgb_hist_i64(const int64_t* img, int64_t n,
+                   int64_t* hist, int64_t bins, uint64_t* oob, void* stream);
+
+/* Query = predicated stream push + drain (codegen.py:462-471, :363-376;
+ * interpreter.py:346-365, :447-481).  out_vals[0:k) = {v : v OP thr} in
+ * INPUT ORDER (order-preserving compaction, matching the CPU FIFO);
+ * out_vals[k:] untouched; count[0] += k.  thr is read on the host side.
+ * ws must hold sdfgb_query_workspace_bytes(n) bytes, zeroed ONCE before
+ * its first use (it resets itself afterwards). */
+size_t sdfgb_query_workspace_bytes(int64_t n, int elem_bytes);
+int sdfgb_query_f32(const float* col, int64_t n, int op, double thr,
+                    float* out_vals, int64_t* count,
+                    void* ws, size_t ws_bytes, void* stream);
+int sdfgb_query_f64(const double* col, int64_t n, int op, double thr,
+                    double* out_vals, int64_t* count,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* CSR SpMV: data-dependent inner map over [rowptr[i], rowptr[i+1]) with the
+ * indirection x[col[j]] and WCR sum into b[i] (gallery.py:152-213):
+ *     b[i] += sum_j val[j] * x[col[j]]               i in [0, H) */
+int sdfgb_spmv_csr_f32(const int32_t* rowptr, const int32_t* col, const float* val,
+                       const float* x, float* b, int64_t H, void* stream);
+int sdfgb_spmv_csr_f64(const int64_t* rowptr, const int64_t* col, const double* val,
+                       const double* x, double* b, int64_t H, void* stream);
+
+/* 2-D Jacobi time loop (loops.py:31-61 guard loop around a stencil map):
+ *     for t in [0, T): A[(t+1)%2, i, j] = coef * (((A[t%2, i+di0, j+dj0]
+ *                         + A[t%2, i+di1, j+dj1]) + ...)      i, j in [1, N-2]
+ * A is [2, N, N] row-major; borders are never written.  The nterms offsets
+ * (|di|,|dj| <= 1, nterms <= 9) fix the summation order of the tasklet. */
+int sdfgb_jacobi2d_f32(float* A, int64_t N, int64_t T, double coef,
+                       const int32_t* di, const int32_t* dj, int nterms, void* stream);
+int sdfgb_jacobi2d_f64(double* A, int64_t N, int64_t T, double coef,
+                       const int32_t* di, const int32_t* dj, int nterms, void* stream);
+/* One row-block of one step (multi-GPU building block): rows [r0, r1) of the
+ * destination plane, reading src and writing dst (both [rows, N] planes whose
+ * row 0 is global row g0). */
+int sdfgb_jacobi2d_step_f32(const float* src, float* dst, int64_t N, int64_t rows,
+                            int64_t g0, int64_t r0, int64_t r1, double coef,
+                            const int32_t* di, const int32_t* dj, int nterms, void* stream);
+
+/* GEMM after MapReduceFusion (library.py:461-554): C = A(MxK) * B(KxN),
+ * row-major fp32, fp32-accurate through 3xTF32 on tcgen05 tensor cores.
+ * ws must hold sdfgb_gemm_workspace_bytes(M, N, K) bytes. */
+size_t sdfgb_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+int sdfgb_gemm_f32(const float* A, const float* B, float* C,
+                   int64_t M, int64_t N, int64_t K,
+                   void* ws, size_t ws_bytes, void* stream);
+/* SIMT fp32 FFMA GEMM (k-sequential per element) used as the on-device
+ * cross-check of the tensor-core path in tests. */
+int sdfgb_gemm_f32_simt(const float* A, const float* B, float* C,
+                        int64_t M, int64_t N, int64_t K, void* stream);
+
+/* -------------------------------------------------------- host entries
+ * Drop-in for CompiledSdfg._fn(*ptrs, *syms) (codegen.py:886): host
+ * buffers in the reference's types; H2D, kernel(s), D2H, synchronous.
+ * precision: 0 = fp32 on device (BASELINE), 1 = native (f64 / i64).      */
+#define SDFGB_PREC_FP32 0
+#define SDFGB_PREC_NATIVE 1
+
+/* void histogram(double* img, int64_t* hist, int64_t H, int64_t W) */
+int sdfgb_host_histogram(const double* img, int64_t* hist, int64_t H, int64_t W,
+                         int64_t bins, double scale, double div, int precision);
+/* void histogram(int64_t* img, int64_t* hist, int64_t H, int64_t W, int64_t B)  gallery.py:354 */
+int sdfgb_host_histogram_i64(const int64_t* img, int64_t* hist, int64_t H, int64_t W,
+                             int64_t bins);
+/* void query(double* col, double* thr, double* out_vals, int64_t* count, int64_t N) */
+int sdfgb_host_query(const double* col, const double* thr, double* out_vals,
+                     int64_t* count, int64_t N, int op, int precision);
+/* void spmv(int64_t* A_row, int64_t* A_col, double* A_val, double* x, double* b,
+ *           int64_t H, int64_t W, int64_t nnz) */
+int sdfgb_host_spmv(const int64_t* A_row, const int64_t* A_col, const double* A_val,
+                    const double* x, double* b, int64_t H, int64_t W, int64_t nnz,
+                    int precision);
+/* void jacobi2d(double* A, int64_t N, int64_t T) */
+int sdfgb_host_jacobi2d(double* A, int64_t N, int64_t T, double coef,
+                        const int32_t* di, const int32_t* dj, int nterms, int precision);
+/* void matmul(double* A, double* B, double* C, int64_t M, int64_t N, int64_t K) */
+int sdfgb_host_matmul(const double* A, const double* B, double* C,
+                      int64_t M, int64_t N, int64_t K);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDFGB200_H */

@@ -1,0 +1,393 @@
+// gemm.cu -- K5: the MapReduceFusion'd matmul map on tcgen05 tensor cores.
+//
+// Reference: gallery.matmul (gallery.py:107-144) after MapReduceFusion
+// (library.py:461-554): an init state writes C = 0, then the 3-D map
+// (i, j, k) accumulates C[i, j] += A[i, k] * B[k, j] through a WCR-sum memlet.
+// Only this motif is a dense contraction, so only it goes to the tensor pipe.
+//
+// fp32 accuracy from TF32 tensor cores via the 3xTF32 split:
+//     A = Ahi + Alo, Ahi = rna_tf32(A), Alo = A - Ahi (exact in fp32)
+//     C ~= Ahi*Bhi + Ahi*Blo + Alo*Bhi        (Alo*Blo ~ 2^-22 dropped)
+// 1xTF32 would miss the 1e-4 tolerance (6.8e-4 at K=4096).
+//
+// v1 structure (one 128x128 C tile per CTA, 256 threads):
+//   * split pre-pass writes Ahi/Alo (M x K) and Bt_hi/Bt_lo (N x K), all
+//     K-major so every operand is a TMA SWIZZLE_128B K-major tile;
+//   * warp 0: TMA producer over a 3-stage smem ring (64 KB/stage), mbarrier
+//     full/empty pipeline;
+//   * warp 1: single-thread tcgen05.mma.kind::tf32 issuer, M=128 N=128 K=8,
+//     3 MMAs per K=8 step into one TMEM accumulator (128 lanes x 128 cols),
+//     tcgen05.commit frees smem stages and finally signals the epilogue;
+//   * warp 2: TMEM allocator; warps 4-7: tcgen05.ld -> registers -> C.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace sdfgb {
+namespace {
+
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+        " [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B (cute::UMMA::SmemDescriptor):
+// start>>4 [0,14) | LBO=1 [16,30) | SBO=1024>>4 [32,46) | version=1 [46,48) | layout=2 [61,64)
+__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+// instruction descriptor kind::tf32, fp32 accumulate, A/B K-major
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------ split pre-pass
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__global__ void split_rows_kernel(const float* __restrict__ A, float* __restrict__ hi,
+                                  float* __restrict__ lo, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float a = A[i];
+        float h = tf32_rna(a);
+        hi[i] = h;
+        lo[i] = a - h;
+    }
+}
+
+// B (K x N, row-major) -> Bt_hi / Bt_lo (N x K, row-major) via 32x32 smem tiles
+__global__ void split_transpose_kernel(const float* __restrict__ B, float* __restrict__ hi,
+                                       float* __restrict__ lo, int64_t K, int64_t N) {
+    __shared__ float t[32][33];
+    const int64_t k0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t k = k0 + r, n = n0 + threadIdx.x;
+        t[r][threadIdx.x] = (k < K && n < N) ? B[k * N + n] : 0.f;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t n = n0 + r, k = k0 + threadIdx.x;
+        if (n < N && k < K) {
+            float a = t[threadIdx.x][r];
+            float h = tf32_rna(a);
+            hi[n * K + k] = h;
+            lo[n * K + k] = a - h;
+        }
+    }
+}
+
+// ------------------------------------------------------------ tcgen05 GEMM
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
+constexpr int TILE_BYTES = BM * BK * 4;              // 16 KB (BM == BN)
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo
+constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
+                   float* __restrict__ C, int M, int N, int K) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int KB = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAhi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAlo)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBhi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBlo)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_d = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                mbar_expect_tx(&full[s], STAGE_BYTES);
+                tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kb * BK, m0);
+                tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kb * BK, m0);
+                tma_load_2d(st + 2 * TILE_BYTES, &mBhi, &full[s], kb * BK, n0);
+                tma_load_2d(st + 3 * TILE_BYTES, &mBlo, &full[s], kb * BK, n0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(BM, BN);
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k) {
+                    const uint32_t off = k * 32;  // 8 tf32 = 32 B along K inside the 128 B atom
+                    const uint64_t ahi = sw128_kmajor_desc(base + 0 * TILE_BYTES + off);
+                    const uint64_t alo = sw128_kmajor_desc(base + 1 * TILE_BYTES + off);
+                    const uint64_t bhi = sw128_kmajor_desc(base + 2 * TILE_BYTES + off);
+                    const uint64_t blo = sw128_kmajor_desc(base + 3 * TILE_BYTES + off);
+                    tc_mma_tf32(tmem_d, alo, bhi, idesc, (kb | k) != 0);
+                    tc_mma_tf32(tmem_d, ahi, blo, idesc, 1u);
+                    tc_mma_tf32(tmem_d, ahi, bhi, idesc, 1u);
+                }
+                tc_commit(&empty[s]);
+            }
+            tc_commit(tmem_full);
+        }
+    } else if (warp >= 4) {
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        const int rw = (warp & 3) * 32;
+        const int row = m0 + rw + lane;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+            uint32_t r[16];
+            tmem_ld16(tmem_d + ((uint32_t)rw << 16) + c, r);
+            if (row < M) {
+                float* dst = C + (int64_t)row * N + n0 + c;
+                if (n0 + c + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        reinterpret_cast<float4*>(dst)[q] =
+                            make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        if (n0 + c + q < N) dst[q] = __uint_as_float(r[q]);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN));
+    }
+}
+
+// ------------------------------------------------------------ SIMT cross-check
+// 64x64 tile, 256 threads, 4x4 per thread, k-sequential FFMA per element.
+__global__ void __launch_bounds__(256)
+gemm_simt_kernel(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
+                 int64_t M, int64_t N, int64_t K) {
+    __shared__ float As[16][64 + 4];
+    __shared__ float Bs[16][64 + 4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
+    float acc[4][4] = {};
+    for (int64_t k0 = 0; k0 < K; k0 += 16) {
+        for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+            const int kk = e % 16, mm = e / 16;
+            As[kk][mm] = (m0 + mm < M && k0 + kk < K) ? A[(m0 + mm) * K + k0 + kk] : 0.f;
+            const int nn = e % 64, kb = e / 64;
+            Bs[kb][nn] = (n0 + nn < N && k0 + kb < K) ? B[(k0 + kb) * N + n0 + nn] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(As[kk][ty * 4 + i], Bs[kk][tx * 4 + j], acc[i][j]);
+        __syncthreads();
+    }
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            const int64_t m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+            if (m < M && n < N) C[m * N + n] = acc[i][j];
+        }
+}
+
+// ------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+int make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t K) {
+    auto fn = encode_fn();
+    if (!fn) return set_error(SDFGB_ERR_CUDA, "gemm: cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 4};
+    cuuint32_t box[2] = {BK, BM};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(SDFGB_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SDFGB_OK;
+}
+
+}  // namespace
+}  // namespace sdfgb
+
+extern "C" size_t sdfgb_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+    // Ahi, Alo (M x K) and Bt_hi, Bt_lo (N x K), each 256-byte aligned
+    auto r = [](size_t b) { return (b + 255) / 256 * 256; };
+    return 2 * r((size_t)M * K * 4) + 2 * r((size_t)N * K * 4);
+}
+
+extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
+                              void* ws, size_t ws_bytes, void* stream) {
+    using namespace sdfgb;
+    if (M < 0 || N < 0 || K < 0 || (M * N > 0 && !C))
+        return set_error(SDFGB_ERR_INVALID, "gemm: bad arguments");
+    if (M == 0 || N == 0) return SDFGB_OK;
+    cudaStream_t s = as_stream(stream);
+    if (K == 0) {  // init_C state only: C = 0 (library.py:541-554)
+        SDFGB_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
+        return SDFGB_OK;
+    }
+    if (K % 4 != 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+        return set_error(SDFGB_ERR_INVALID, "gemm: K must be a multiple of 4 (TMA row stride)");
+    if (!A || !B || !ws || ws_bytes < sdfgb_gemm_workspace_bytes(M, N, K))
+        return set_error(SDFGB_ERR_WORKSPACE, "gemm: workspace too small");
+    auto r = [](size_t b) { return (b + 255) / 256 * 256; };
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    float* Ahi = reinterpret_cast<float*>(w);
+    float* Alo = reinterpret_cast<float*>(w + r((size_t)M * K * 4));
+    float* Bhi = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4));
+    float* Blo = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4) + r((size_t)N * K * 4));
+
+    split_rows_kernel<<<num_sms() * 8, 256, 0, s>>>(A, Ahi, Alo, M * K);
+    SDFGB_LAUNCHED("split_rows_kernel");
+    dim3 tg((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32));
+    split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bhi, Blo, K, N);
+    SDFGB_LAUNCHED("split_transpose_kernel");
+
+    CUtensorMap mAhi, mAlo, mBhi, mBlo;
+    SDFGB_TRY(make_kmajor_map(&mAhi, Ahi, M, K));
+    SDFGB_TRY(make_kmajor_map(&mAlo, Alo, M, K));
+    SDFGB_TRY(make_kmajor_map(&mBhi, Bhi, N, K));
+    SDFGB_TRY(make_kmajor_map(&mBlo, Blo, N, K));
+    static std::once_flag attr;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr, [] {
+        attr_err = cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    });
+    SDFGB_CUDA(attr_err);
+    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+    gemm_3xtf32_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, s>>>(mAhi, mAlo, mBhi, mBlo, C, (int)M, (int)N, (int)K);
+    SDFGB_LAUNCHED("gemm_3xtf32_kernel");
+    return SDFGB_OK;
+}
+
+extern "C" int sdfgb_gemm_f32_simt(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
+                                   void* stream) {
+    using namespace sdfgb;
+    if (M < 0 || N < 0 || K < 0 || (M * N > 0 && (!A || !B || !C)))
+        return set_error(SDFGB_ERR_INVALID, "gemm_simt: bad arguments");
+    if (M == 0 || N == 0) return SDFGB_OK;
+    dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64));
+    gemm_simt_kernel<<<grid, 256, 0, as_stream(stream)>>>(A, B, C, M, N, K);
+    SDFGB_LAUNCHED("gemm_simt_kernel");
+    return SDFGB_OK;
+}

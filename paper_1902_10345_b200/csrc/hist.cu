@@ -1,0 +1,244 @@
+// hist.cu -- K1: WCR-sum histogram with a dynamic subscript.
+//
+// Replaces the reference's per-instance subscript write ``h[k] = 1`` under a
+// WCR-sum memlet (tasklets.py:297-300 -> interpreter.py:262-278 ->
+// codegen.py:733-747 ``hist[k] += 1``) executed once per point of the map
+// [0:H-1, 0:W-1].  Binning ``bi = v * S // D`` follows the C emission
+// ``(int64_t)floor((double)(v*S) / (double)D)`` (tasklets.py:432-433, :480-481),
+// computed here in double so it is bit-identical to the reference for every
+// input (fp32 data widens exactly).
+//
+// B200 design (HBM-bound: 4 B/px read, 256 x 8 B written):
+//   * streaming 128-bit loads (ld.global.nc.L1::no_allocate), 4 vectors in
+//     flight per thread;
+//   * shared-memory-privatised counters, R replicas (warp % R) so skewed
+//     images do not serialise one address; a warp whose lanes all hit one
+//     bin issues a single add of 32;
+//   * 8-CTA thread-block clusters fold their smem histograms through DSMEM
+//     into the leader CTA, which alone merges into global memory -> only
+//     grid/8 x bins global atomics (the 2 KB hist lives in 4 L2 slices, so
+//     per-CTA global merges would serialise there).
+#include <algorithm>
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sdfgb {
+namespace {
+
+constexpr int kHistBlock = 512;
+constexpr int kHistUnroll = 4;
+constexpr int kHistCluster = 8;
+constexpr int kMaxSmemBins = 12288;  // 48 KB of uint32 counters per replica set
+
+enum BinMode { kScaled = 0, kIdentity = 1 };
+
+template <typename T, int MODE>
+__device__ __forceinline__ bool bin_of(T v, double scale, double div, bool has_div,
+                                       int64_t bins, int& bin) {
+    if constexpr (MODE == kIdentity) {
+        int64_t k = (int64_t)v;
+        bin = (int)k;
+        return k >= 0 && k < bins;
+    } else {
+        double q = (double)v * scale;
+        if (has_div) q = q / div;
+        q = floor(q);
+        bin = (int)q;
+        return q >= 0.0 && q < (double)bins;  // NaN -> false
+    }
+}
+
+template <typename T, int MODE>
+__device__ __forceinline__ void bump(uint32_t* h, T v, double scale, double div, bool has_div,
+                                     int64_t bins, uint32_t& bad) {
+    int b;
+    bool ok = bin_of<T, MODE>(v, scale, div, has_div, bins, b);
+    unsigned okm = __ballot_sync(0xffffffffu, ok);
+    bad += 32 - __popc(okm);
+    int b0 = __shfl_sync(0xffffffffu, b, 0);
+    if (okm == 0xffffffffu && __all_sync(0xffffffffu, b == b0)) {
+        if ((threadIdx.x & 31) == 0) atomicAdd(&h[b0], 32u);
+    } else if (ok) {
+        atomicAdd(&h[b], 1u);
+    }
+}
+
+template <typename T, int MODE>
+__global__ void __cluster_dims__(kHistCluster, 1, 1) __launch_bounds__(kHistBlock)
+hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale, double div,
+                 int64_t bins, int reps, unsigned long long* __restrict__ hist,
+                 unsigned long long* __restrict__ oob) {
+    extern __shared__ uint32_t sh[];
+    using V = typename Vec16<T>::type;
+    constexpr int VN = Vec16<T>::n;
+    const bool has_div = div != 1.0;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+
+    for (int64_t k = tid; k < (int64_t)reps * bins; k += blockDim.x) sh[k] = 0u;
+    __syncthreads();
+
+    uint32_t* h = sh + (warp % reps) * bins;
+    uint32_t bad = 0;
+
+    // misaligned head (< VN elements) and the ragged tail: whole warps, lane-masked
+    const int64_t nvec = (n - head) / VN;
+    const int64_t tail0 = head + nvec * VN;
+    if (blockIdx.x == 0 && warp == 0) {
+        const int lane = tid & 31;
+        for (int64_t base = 0; base < head; base += 32) {
+            int64_t p = base + lane;
+            // out-of-range lanes feed a sentinel the ballot discounts below
+            bool live = p < head;
+            T v = live ? in[p] : T(0);
+            int b;
+            bool ok = live && bin_of<T, MODE>(v, scale, div, has_div, bins, b);
+            unsigned okm = __ballot_sync(0xffffffffu, ok);
+            unsigned livem = __ballot_sync(0xffffffffu, live);
+            bad += __popc(livem) - __popc(okm);
+            if (ok) atomicAdd(&h[b], 1u);
+        }
+        for (int64_t base = tail0; base < n; base += 32) {
+            int64_t p = base + lane;
+            bool live = p < n;
+            T v = live ? in[p] : T(0);
+            int b;
+            bool ok = live && bin_of<T, MODE>(v, scale, div, has_div, bins, b);
+            unsigned okm = __ballot_sync(0xffffffffu, ok);
+            unsigned livem = __ballot_sync(0xffffffffu, live);
+            bad += __popc(livem) - __popc(okm);
+            if (ok) atomicAdd(&h[b], 1u);
+        }
+    }
+
+    const V* vin = reinterpret_cast<const V*>(in + head);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
+    // main body: kHistUnroll vectors in flight per thread
+    const int lane = tid & 31;
+    // loop bounds are taken on the warp's first lane so whole warps stay
+    // converged for the votes in bump()
+    for (; (i - lane) + 31 + (kHistUnroll - 1) * stride < nvec; i += kHistUnroll * stride) {
+        V v[kHistUnroll];
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) v[u] = ldg_stream(vin + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u)
+#pragma unroll
+            for (int c = 0; c < VN; ++c)
+                bump<T, MODE>(h, vget<V, T>(v[u], c), scale, div, has_div, bins, bad);
+    }
+    // remainder vectors: keep whole warps converged for the warp votes
+    for (; i - lane < nvec; i += stride) {
+        bool live = i < nvec;
+        V v = live ? ldg_stream(vin + i) : V{};
+#pragma unroll
+        for (int c = 0; c < VN; ++c) {
+            T x = vget<V, T>(v, c);
+            int b;
+            bool ok = live && bin_of<T, MODE>(x, scale, div, has_div, bins, b);
+            unsigned okm = __ballot_sync(0xffffffffu, ok);
+            unsigned livem = __ballot_sync(0xffffffffu, live);
+            bad += __popc(livem) - __popc(okm);
+            if (ok) atomicAdd(&h[b], 1u);
+        }
+    }
+
+    // out-of-range count (lane 0 of each warp holds the warp's ballot totals)
+    if ((tid & 31) == 0 && bad) atomicAdd(oob, (unsigned long long)bad);
+
+    __syncthreads();
+    // fold replicas into replica 0
+    for (int64_t k = tid; k < bins; k += blockDim.x) {
+        uint32_t s = 0;
+        for (int r = 1; r < reps; ++r) s += sh[r * bins + k];
+        sh[k] += s;
+    }
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (cluster.block_rank() != 0) {
+        uint32_t* lead = cluster.map_shared_rank(sh, 0);
+        for (int64_t k = tid; k < bins; k += blockDim.x) {
+            uint32_t c = sh[k];
+            if (c) atomicAdd(&lead[k], c);
+        }
+    }
+    cluster.sync();
+    if (cluster.block_rank() == 0) {
+        for (int64_t k = tid; k < bins; k += blockDim.x) {
+            uint32_t c = sh[k];
+            if (c) atomicAdd(&hist[k], (unsigned long long)c);
+        }
+    }
+}
+
+// Bins beyond the shared-memory budget: direct global WCR (still on device).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256)
+hist_global_kernel(const T* __restrict__ in, int64_t n, double scale, double div, int64_t bins,
+                   unsigned long long* __restrict__ hist, unsigned long long* __restrict__ oob) {
+    const bool has_div = div != 1.0;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int b;
+        if (bin_of<T, MODE>(in[p], scale, div, has_div, bins, b))
+            atomicAdd(&hist[b], 1ull);
+        else
+            atomicAdd(oob, 1ull);
+    }
+}
+
+template <typename T, int MODE>
+int launch_hist(const T* img, int64_t n, double scale, double div, int64_t* hist, int64_t bins,
+                uint64_t* oob, void* stream) {
+    if (n < 0 || bins <= 0 || (n > 0 && !img) || !hist || !oob)
+        return set_error(SDFGB_ERR_INVALID, "hist: bad arguments (n=%lld bins=%lld)",
+                         (long long)n, (long long)bins);
+    if (n == 0) return SDFGB_OK;
+    cudaStream_t s = as_stream(stream);
+    auto* H = reinterpret_cast<unsigned long long*>(hist);
+    auto* O = reinterpret_cast<unsigned long long*>(oob);
+    if (bins > kMaxSmemBins) {
+        int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+        hist_global_kernel<T, MODE><<<blocks, 256, 0, s>>>(img, n, scale, div, bins, H, O);
+        SDFGB_LAUNCHED("hist_global_kernel");
+        return SDFGB_OK;
+    }
+    constexpr int VN = Vec16<T>::n;
+    int reps = (int)std::max<int64_t>(1, std::min<int64_t>(8, kMaxSmemBins / bins));
+    size_t smem = (size_t)reps * bins * sizeof(uint32_t);
+    auto kern = hist_smem_kernel<T, MODE>;
+    if (smem > 48 * 1024)
+        SDFGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    uintptr_t addr = reinterpret_cast<uintptr_t>(img);
+    int64_t head = (int64_t)(((16 - (addr & 15)) & 15) / sizeof(T));
+    if (head > n) head = n;
+    int64_t nvec = (n - head) / VN;
+    int64_t want = (nvec + (int64_t)kHistBlock * kHistUnroll - 1) / ((int64_t)kHistBlock * kHistUnroll);
+    int64_t cap = (int64_t)num_sms() * (2048 / kHistBlock);
+    int64_t blocks = std::max<int64_t>(1, std::min(want, cap));
+    blocks = (blocks + kHistCluster - 1) / kHistCluster * kHistCluster;
+    kern<<<(unsigned)blocks, kHistBlock, smem, s>>>(img, n, head, scale, div, bins, reps, H, O);
+    SDFGB_LAUNCHED("hist_smem_kernel");
+    return SDFGB_OK;
+}
+
+}  // namespace
+}  // namespace sdfgb
+
+extern "C" int sdfgb_hist_f32(const float* img, int64_t n, double scale, double div,
+                              int64_t* hist, int64_t bins, uint64_t* oob, void* stream) {
+    return sdfgb::launch_hist<float, sdfgb::kScaled>(img, n, scale, div, hist, bins, oob, stream);
+}
+extern "C" int sdfgb_hist_f64(const double* img, int64_t n, double scale, double div,
+                              int64_t* hist, int64_t bins, uint64_t* oob, void* stream) {
+    return sdfgb::launch_hist<double, sdfgb::kScaled>(img, n, scale, div, hist, bins, oob, stream);
+}
+extern "C" int sdfgb_hist_i64(const int64_t* img, int64_t n, int64_t* hist, int64_t bins,
+                              uint64_t* oob, void* stream) {
+    return sdfgb::launch_hist<int64_t, sdfgb::kIdentity>(img, n, 1.0, 1.0, hist, bins, oob, stream);
+}

@@ -1,0 +1,250 @@
+// query.cu -- K2: predicated stream push + drain as one order-preserving
+// stream compaction.
+//
+// Reference semantics (query motif, gallery.py:300-347):
+//   map i in [0:N-1]:  if col[i] OP limit: push col[i] to stream S; count += 1
+//   then S is drained FIFO into out_vals[0:n)           (codegen.py:363-376)
+// The CPU stream is a realloc-doubling queue with one memcpy per push
+// (codegen.py:123-143, :462-471); the FIFO order is the map's iteration order.
+//
+// B200 design: single pass, HBM-bound (read 4N, write 4n).  Each CTA owns a
+// tile of 16 elements x 256 threads; predicate bits -> per-thread counts ->
+// one 64-bit packed block scan (4 chunk counters in 16-bit lanes) -> tile
+// aggregate -> decoupled look-back over per-tile status words for the tile's
+// global offset -> survivors are written at their input-order rank.  The
+// output is therefore IDENTICAL to the CPU FIFO order, not just the same set.
+//
+// Tile ids come from an atomic ticket (a CTA only obtains a tile once running,
+// so every predecessor it waits on is resident -> forward progress).  Status
+// words carry a 20-bit launch epoch, so the workspace never needs clearing;
+// the last CTA to finish resets the ticket/done counters for the next launch.
+#include <algorithm>
+#include <atomic>
+
+#include "common.cuh"
+
+namespace sdfgb {
+namespace {
+
+constexpr int kQBlock = 256;
+constexpr int kQVecPerThread = 4;
+
+constexpr uint64_t kFlagAgg = 1ull;
+constexpr uint64_t kFlagPrefix = 2ull;
+constexpr int kValueBits = 42;
+constexpr uint64_t kValueMask = (1ull << kValueBits) - 1;
+
+struct QueryWs {
+    unsigned long long ticket;
+    unsigned long long done;
+    unsigned long long pad[14];
+    unsigned long long status[1];  // num_tiles words
+};
+
+__device__ __forceinline__ uint64_t ld_relaxed(const unsigned long long* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, uint64_t value) {
+    return ((uint64_t)epoch << 44) | (flag << kValueBits) | (value & kValueMask);
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kQBlock)
+query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __restrict__ out,
+             unsigned long long* __restrict__ count, QueryWs* __restrict__ ws,
+             int64_t num_tiles, uint32_t epoch) {
+    using V = typename Vec16<T>::type;
+    constexpr int VN = Vec16<T>::n;
+    constexpr int K = kQVecPerThread;
+    constexpr int TILE = kQBlock * K * VN;
+
+    __shared__ int64_t s_tile;
+    __shared__ uint64_t s_warp[kQBlock / 32];
+    __shared__ int64_t s_excl;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = (int64_t)atomicAdd(&ws->ticket, 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * TILE;
+
+    // ---- load + predicate (element e = base + k*kQBlock*VN + tid*VN + c)
+    T v[K][VN];
+    uint32_t bits = 0;  // bit k*VN+c
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
+        if (VEC && e0 + VN <= n) {
+            V x = ldg_stream(reinterpret_cast<const V*>(col + e0));
+#pragma unroll
+            for (int c = 0; c < VN; ++c) v[k][c] = vget<V, T>(x, c);
+#pragma unroll
+            for (int c = 0; c < VN; ++c)
+                bits |= (uint32_t)cmp_apply((double)v[k][c], op, thr) << (k * VN + c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < VN; ++c) {
+                const bool live = e0 + c < n;
+                v[k][c] = live ? col[e0 + c] : T(0);
+                bits |= (uint32_t)(live && cmp_apply((double)v[k][c], op, thr)) << (k * VN + c);
+            }
+        }
+    }
+
+    // ---- packed block scan: 16-bit field k = this thread's count in chunk k
+    uint64_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        mine |= (uint64_t)__popc((bits >> (k * VN)) & ((1u << VN) - 1)) << (16 * k);
+    uint64_t incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += o;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint64_t wpre = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kQBlock / 32; ++w) {
+        uint64_t t = s_warp[w];
+        if (w < warp) wpre += t;
+        total += t;
+    }
+    const uint64_t excl = wpre + incl - mine;
+    uint32_t chunk_base[K];
+    uint32_t agg = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        chunk_base[k] = agg;
+        agg += (uint32_t)((total >> (16 * k)) & 0xffff);
+    }
+
+    // ---- decoupled look-back for the tile's global offset
+    if (warp == 0) {
+        int64_t prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) st_relaxed(&ws->status[0], pack_status(epoch, kFlagPrefix, agg));
+        } else {
+            if (lane == 0) st_relaxed(&ws->status[tile], pack_status(epoch, kFlagAgg, agg));
+            int64_t pred = tile - 1;
+            while (true) {
+                const int64_t idx = pred - lane;
+                uint64_t w;
+                bool valid;
+                do {
+                    if (idx >= 0) {
+                        w = ld_relaxed(&ws->status[idx]);
+                        valid = (uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull);
+                    } else {
+                        w = pack_status(epoch, kFlagPrefix, 0);  // before tile 0
+                        valid = true;
+                    }
+                } while (!__all_sync(0xffffffffu, valid));
+                const bool is_prefix = ((w >> kValueBits) & 3ull) == kFlagPrefix;
+                const unsigned pm = __ballot_sync(0xffffffffu, is_prefix);
+                const int stop = pm ? __ffs(pm) - 1 : 31;  // lanes 0..stop contribute
+                uint64_t val = lane <= stop ? (w & kValueMask) : 0;
+#pragma unroll
+                for (int d = 16; d; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
+                prefix += (int64_t)val;
+                if (pm) break;
+                pred -= 32;
+            }
+            if (lane == 0)
+                st_relaxed(&ws->status[tile], pack_status(epoch, kFlagPrefix, prefix + agg));
+        }
+        if (lane == 0) {
+            s_excl = prefix;
+            if (tile == num_tiles - 1) atomicAdd(count, (unsigned long long)(prefix + agg));
+        }
+    }
+    __syncthreads();
+
+    // ---- scatter survivors at their input-order rank
+    const int64_t obase = s_excl;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        uint32_t r = chunk_base[k] + (uint32_t)((excl >> (16 * k)) & 0xffff);
+#pragma unroll
+        for (int c = 0; c < VN; ++c) {
+            if (bits & (1u << (k * VN + c))) out[obase + r++] = v[k][c];
+        }
+    }
+
+    // ---- last CTA out resets the counters for the next launch
+    if (tid == 0) {
+        __threadfence();
+        unsigned long long d = atomicAdd(&ws->done, 1ull);
+        if (d == (unsigned long long)num_tiles - 1) {
+            ws->ticket = 0;
+            ws->done = 0;
+            __threadfence();
+        }
+    }
+}
+
+std::atomic<uint32_t> g_epoch{0};
+
+uint32_t next_epoch() {
+    uint32_t e;
+    do {
+        e = (g_epoch.fetch_add(1) + 1) & 0xFFFFF;
+    } while (e == 0);
+    return e;
+}
+
+template <typename T>
+int64_t tiles_for(int64_t n) {
+    const int64_t tile = (int64_t)kQBlock * kQVecPerThread * Vec16<T>::n;
+    return (n + tile - 1) / tile;
+}
+
+template <typename T>
+int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* count, void* ws,
+                 size_t ws_bytes, void* stream) {
+    if (n < 0 || op < 0 || op > 5 || !count || (n > 0 && (!col || !out || !ws)))
+        return set_error(SDFGB_ERR_INVALID, "query: bad arguments");
+    if (n == 0) return SDFGB_OK;
+    if ((uint64_t)n > kValueMask) return set_error(SDFGB_ERR_INVALID, "query: n too large");
+    const int64_t tiles = tiles_for<T>(n);
+    if (ws_bytes < sdfgb_query_workspace_bytes(n, sizeof(T)))
+        return set_error(SDFGB_ERR_WORKSPACE, "query: workspace %zu < %zu bytes", ws_bytes,
+                         sdfgb_query_workspace_bytes(n, sizeof(T)));
+    if ((reinterpret_cast<uintptr_t>(ws) & 7) != 0)
+        return set_error(SDFGB_ERR_INVALID, "query: workspace must be 8-byte aligned");
+    const bool vec = (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+    auto* W = reinterpret_cast<QueryWs*>(ws);
+    auto* C = reinterpret_cast<unsigned long long*>(count);
+    const uint32_t epoch = next_epoch();
+    cudaStream_t s = as_stream(stream);
+    if (vec)
+        query_kernel<T, true><<<(unsigned)tiles, kQBlock, 0, s>>>(col, n, op, thr, out, C, W,
+                                                                   tiles, epoch);
+    else
+        query_kernel<T, false><<<(unsigned)tiles, kQBlock, 0, s>>>(col, n, op, thr, out, C, W,
+                                                                    tiles, epoch);
+    SDFGB_LAUNCHED("query_kernel");
+    return SDFGB_OK;
+}
+
+}  // namespace
+}  // namespace sdfgb
+
+extern "C" size_t sdfgb_query_workspace_bytes(int64_t n, int elem_bytes) {
+    int64_t tiles = elem_bytes == 8 ? sdfgb::tiles_for<double>(n) : sdfgb::tiles_for<float>(n);
+    return offsetof(sdfgb::QueryWs, status) + (size_t)std::max<int64_t>(tiles, 1) * 8;
+}
+extern "C" int sdfgb_query_f32(const float* col, int64_t n, int op, double thr, float* out_vals,
+                               int64_t* count, void* ws, size_t ws_bytes, void* stream) {
+    return sdfgb::launch_query<float>(col, n, op, thr, out_vals, count, ws, ws_bytes, stream);
+}
+extern "C" int sdfgb_query_f64(const double* col, int64_t n, int op, double thr, double* out_vals,
+                               int64_t* count, void* ws, size_t ws_bytes, void* stream) {
+    return sdfgb::launch_query<double>(col, n, op, thr, out_vals, count, ws, ws_bytes, stream);
+}

@@ -1,0 +1,86 @@
+// spmv.cu -- K3: CSR SpMV, the spmv motif (gallery.py:152-213):
+//   map i in [0:H-1]:
+//     map j in [row_b:row_e-1]   (data-dependent range, A_row[i], A_row[i+1])
+//       x_val = x[A_col[j]]       (indirection tasklet, ir.py:608-639)
+//       b[i] (+)= A_val[j] * x_val   (WCR sum, accumulates onto b_in)
+//
+// B200 design: warp per row.  Lanes stream the row's col/val coalesced
+// (the matrix is 8 B/nnz of HBM traffic, read once), gather x through
+// L1/L2 (x is 16 MB at the BASELINE shape -> L2-resident), reduce with
+// shuffles, lane 0 commits b[i] += sum.  Two rows per warp iteration keep
+// more independent gathers in flight.  The per-row summation is a lane
+// tree rather than the reference's left-to-right j order, so results agree
+// to rounding (1e-5 rel for fp32).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sdfgb {
+namespace {
+
+constexpr int kSpmvBlock = 256;
+
+template <typename I, typename T>
+__global__ void __launch_bounds__(kSpmvBlock)
+spmv_warp_row_kernel(const I* __restrict__ rowptr, const I* __restrict__ col,
+                     const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ b,
+                     int64_t H) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kSpmvBlock + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kSpmvBlock) >> 5;
+    for (int64_t r0 = warp * 2; r0 < H; r0 += nwarps * 2) {
+        const int64_t r1 = r0 + 1;
+        const int64_t b0 = rowptr[r0], e0 = rowptr[r0 + 1];
+        const int64_t b1 = r1 < H ? (int64_t)rowptr[r1] : 0;
+        const int64_t e1 = r1 < H ? (int64_t)rowptr[r1 + 1] : 0;
+        T s0 = T(0), s1 = T(0);
+        const int64_t l0 = e0 - b0, l1 = e1 - b1;
+        const int64_t lmax = l0 > l1 ? l0 : l1;
+        for (int64_t o = lane; o < lmax; o += 32) {
+            if (o < l0) {
+                const int64_t j = b0 + o;
+                s0 += __ldg(val + j) * __ldg(x + __ldg(col + j));
+            }
+            if (o < l1) {
+                const int64_t j = b1 + o;
+                s1 += __ldg(val + j) * __ldg(x + __ldg(col + j));
+            }
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, d);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, d);
+        }
+        if (lane == 0) {
+            b[r0] += s0;
+            if (r1 < H) b[r1] += s1;
+        }
+    }
+}
+
+template <typename I, typename T>
+int launch_spmv(const I* rowptr, const I* col, const T* val, const T* x, T* b, int64_t H,
+                void* stream) {
+    if (H < 0 || (H > 0 && (!rowptr || !b)))
+        return set_error(SDFGB_ERR_INVALID, "spmv: bad arguments");
+    if (H == 0) return SDFGB_OK;
+    const int64_t warps_needed = (H + 1) / 2;
+    const int64_t blocks_needed = (warps_needed * 32 + kSpmvBlock - 1) / kSpmvBlock;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * 8));
+    spmv_warp_row_kernel<I, T><<<(unsigned)blocks, kSpmvBlock, 0, as_stream(stream)>>>(
+        rowptr, col, val, x, b, H);
+    SDFGB_LAUNCHED("spmv_warp_row_kernel");
+    return SDFGB_OK;
+}
+
+}  // namespace
+}  // namespace sdfgb
+
+extern "C" int sdfgb_spmv_csr_f32(const int32_t* rowptr, const int32_t* col, const float* val,
+                                  const float* x, float* b, int64_t H, void* stream) {
+    return sdfgb::launch_spmv<int32_t, float>(rowptr, col, val, x, b, H, stream);
+}
+extern "C" int sdfgb_spmv_csr_f64(const int64_t* rowptr, const int64_t* col, const double* val,
+                                  const double* x, double* b, int64_t H, void* stream) {
+    return sdfgb::launch_spmv<int64_t, double>(rowptr, col, val, x, b, H, stream);
+}

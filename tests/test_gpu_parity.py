@@ -1,0 +1,319 @@
+"""GPU parity: the sm_100a kernels against the reference (golden fixtures from
+its interpreter) and against the C oracle, through the C ABI.
+
+Tolerances: histogram counts and query survivors bit-exact
+(query compared in order -- the compaction is order-preserving); Jacobi
+bit-exact against the same-op-order restatement (fp32) or the reference
+itself (native f64); SpMV 1e-5 rel (fp32) / 1e-12 (native); GEMM 1e-4 rel.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import graph_path, load_cases
+
+import paper_1902_10345_b200 as b200
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+DEV = "cuda"
+
+
+def marked(name, precision):
+    doc = json.load(open(graph_path(name)))
+    for d in doc["data"]:
+        if not d["transient"]:
+            d["storage"] = f"GPU_Global:{precision}"
+    return doc
+
+
+SUPPORTED = ["histogram", "histogram_int", "query", "query_gallery", "spmv", "jacobi2d", "matmul",
+             "matmul_raw", "matmul_tiled", "matmul_chain"]
+CASES = [c for m in SUPPORTED for c in load_cases(m)]
+
+
+# ------------------------------------------------ drop-in vs reference fixtures
+
+@pytest.mark.parametrize("precision", ["native", "fp32"])
+@pytest.mark.parametrize("c", CASES, ids=repr)
+def test_dropin_matches_reference_interpreter(c, precision):
+    if c.motif.startswith("matmul") and precision == "native":
+        pytest.skip("GEMM runs 3xTF32 only")
+    prog = b200.invoke_toolchain(b200.generate(marked(c.motif, precision)))
+    if c.error:
+        with pytest.raises(b200.OutOfBoundsError):
+            prog.run(c.inputs, c.symbols)
+        return
+    got = prog.run(c.inputs, c.symbols)
+    for name, exp in c.outputs.items():
+        g = got[name].reshape(exp.shape)
+        if exp.dtype.kind == "i" or c.motif.startswith(("histogram", "query")):
+            np.testing.assert_array_equal(g, exp, err_msg=name)
+        elif c.motif == "jacobi2d":
+            if precision == "native":
+                np.testing.assert_array_equal(g, exp, err_msg=name)
+            else:
+                ref32 = oracle.jacobi2d(c.inputs["A"].astype(np.float32), c.symbols["T"], fp32=True)
+                np.testing.assert_array_equal(g, ref32.astype(np.float64), err_msg=name)
+                nrm = np.linalg.norm(exp) or 1.0
+                assert np.linalg.norm(g - exp) / nrm < 1e-5
+        elif c.motif == "spmv":
+            rtol = 1e-12 if precision == "native" else 1e-5
+            np.testing.assert_allclose(g, exp, rtol=rtol, atol=rtol * (np.abs(exp).max() + 1e-30))
+        else:  # matmul, 3xTF32
+            scale = np.abs(exp).max() + 1e-30
+            assert np.abs(g - exp).max() / scale < 1e-4, name
+
+
+# ------------------------------------------------ device entries vs oracle
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+@pytest.mark.parametrize("shape", [(1000, 1003), (1, 5), (7, 33), (64, 4096)])
+def test_hist_f32_random_and_misaligned(shape, offset):
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(sum(shape) + offset)
+    img = rng.random(shape, dtype=np.float32)
+    base = t(np.concatenate([np.zeros(offset, np.float32), img.reshape(-1)]))
+    view = base[offset:]
+    h = torch.full((256,), 5, dtype=torch.int64, device=DEV)
+    oob = torch.zeros(1, dtype=torch.int64, device=DEV)
+    device.hist(view, h, oob)
+    ref, bad = oracle.histogram(img, np.full(256, 5, np.int64))
+    assert oob.item() == bad == 0
+    np.testing.assert_array_equal(h.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("kind", ["zeros", "half_one_bin", "boundaries", "oob", "nan"])
+def test_hist_f32_skewed_and_edge_values(kind):
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(1)
+    img = rng.random(300007, dtype=np.float32)
+    if kind == "zeros":
+        img[:] = 0
+    elif kind == "half_one_bin":
+        img[::2] = 0.5
+    elif kind == "boundaries":
+        img[:257] = np.concatenate([np.arange(256) / 256.0, [np.nextafter(np.float32(1), np.float32(0))]])
+    elif kind == "oob":
+        img[::1001] = 1.0
+        img[5::999] = -0.25
+    else:
+        img[3::777] = np.nan
+    h = torch.zeros(256, dtype=torch.int64, device=DEV)
+    oob = torch.zeros(1, dtype=torch.int64, device=DEV)
+    device.hist(t(img), h, oob)
+    ref, bad = oracle.histogram(img, np.zeros(256, np.int64))
+    assert oob.item() == bad
+    np.testing.assert_array_equal(h.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("bins,scale,div", [(100, 100.0, 1.0), (1000, 3000.0, 3.0), (20000, 20000.0, 1.0),
+                                            (7, 7.0, 1.0)])
+def test_hist_general_binning(bins, scale, div):
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(bins)
+    for dt in (np.float32, np.float64):
+        img = rng.random(123457).astype(dt)
+        h = torch.zeros(bins, dtype=torch.int64, device=DEV)
+        oob = torch.zeros(1, dtype=torch.int64, device=DEV)
+        device.hist(t(img), h, oob, scale, div)
+        ref, bad = oracle.histogram(img, np.zeros(bins, np.int64), scale, div)
+        assert oob.item() == bad
+        np.testing.assert_array_equal(h.cpu().numpy(), ref)
+
+
+def test_hist_i64():
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(2)
+    img = rng.integers(-3, 70, 99991).astype(np.int64)
+    h = torch.zeros(64, dtype=torch.int64, device=DEV)
+    oob = torch.zeros(1, dtype=torch.int64, device=DEV)
+    device.hist(t(img), h, oob)
+    ref, bad = oracle.histogram(img, np.zeros(64, np.int64), integer=True)
+    assert oob.item() == bad
+    np.testing.assert_array_equal(h.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("op", ["<", "<=", ">", ">=", "==", "!="])
+@pytest.mark.parametrize("n,offset", [(1, 0), (31, 1), (4096, 0), (4097, 3), (1000003, 2), (65536 * 3, 0)])
+def test_query_order_preserving(n, offset, op):
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(n + offset)
+    col = rng.random(n, dtype=np.float32)
+    col[::5] = 0.5
+    base = t(np.concatenate([np.zeros(offset, np.float32), col]))
+    view = base[offset:]
+    out = torch.full((n,), -1.0, dtype=torch.float32, device=DEV)
+    cnt = torch.full((1,), 11, dtype=torch.int64, device=DEV)
+    ws = device.query_workspace(n, 4, DEV)
+    for rep in range(3):  # workspace reuse across launches (epoch + self-reset)
+        out.fill_(-1.0)
+        cnt.fill_(11)
+        device.query(view, 0.5, out, cnt, ws, op)
+        rout, rcnt = oracle.query(col, 0.5, np.full(n, -1.0, np.float32), np.array([11]), op)
+        np.testing.assert_array_equal(cnt.cpu().numpy(), rcnt)
+        np.testing.assert_array_equal(out.cpu().numpy(), rout)
+
+
+def test_query_f64():
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(9)
+    col = rng.random(777777)
+    out = torch.zeros(col.size, dtype=torch.float64, device=DEV)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    ws = device.query_workspace(col.size, 8, DEV)
+    device.query(t(col), 0.3, out, cnt, ws, ">=")
+    rout, rcnt = oracle.query(col, 0.3, np.zeros(col.size), np.zeros(1, np.int64), ">=")
+    assert cnt.item() == rcnt[0]
+    np.testing.assert_array_equal(out.cpu().numpy(), rout)
+
+
+def random_csr(rng, H, W, max_len):
+    lens = rng.integers(0, max_len + 1, H)
+    rowptr = np.concatenate([[0], np.cumsum(lens)])
+    nnz = int(rowptr[-1])
+    col = np.concatenate([np.sort(rng.integers(0, W, l)) for l in lens]) if nnz else np.zeros(0, np.int64)
+    return rowptr, col, rng.random(nnz, dtype=np.float32), rng.random(W, dtype=np.float32)
+
+
+@pytest.mark.parametrize("H,W,max_len", [(1, 1, 1), (1000, 2000, 200), (50001, 4000, 10), (8, 5, 0)])
+def test_spmv(H, W, max_len):
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(H)
+    rowptr, col, val, x = random_csr(rng, H, W, max_len)
+    b0 = rng.random(H, dtype=np.float32)
+    ref = oracle.spmv(rowptr, col, val.astype(np.float64), x.astype(np.float64), b0.astype(np.float64))
+    b = t(b0)
+    device.spmv(t(rowptr.astype(np.int32)), t(col.astype(np.int32)), t(val), t(x), b)
+    np.testing.assert_allclose(b.cpu().numpy(), ref, rtol=1e-5, atol=1e-6)
+    b64 = t(b0.astype(np.float64))
+    device.spmv(t(rowptr.astype(np.int64)), t(col.astype(np.int64)), t(val.astype(np.float64)),
+                t(x.astype(np.float64)), b64)
+    np.testing.assert_allclose(b64.cpu().numpy(), ref, rtol=1e-12, atol=1e-13)
+
+
+NINE = [(1, 1), (0, 0), (-1, 0), (1, 0), (0, -1), (0, 1), (-1, -1), (-1, 1), (1, -1)]
+
+
+@pytest.mark.parametrize("N,T", [(3, 2), (4, 3), (5, 1), (67, 5), (130, 4), (515, 3), (1024, 2)])
+@pytest.mark.parametrize("terms", ["canon", "nine"])
+def test_jacobi_bit_exact(N, T, terms):
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(N * 10 + T)
+    A = rng.random((2, N, N), dtype=np.float32)  # non-zero borders, distinct planes
+    tm = oracle.JACOBI5 if terms == "canon" else NINE
+    coef = 0.2 if terms == "canon" else 1.0 / 9.0
+    ref = oracle.jacobi2d(A, T, coef=np.float32(coef), terms=tm, fp32=True)
+    At = t(A)
+    device.jacobi2d(At, T, coef=float(np.float32(coef)), terms=tm)
+    np.testing.assert_array_equal(At.cpu().numpy(), ref)
+    A64 = A.astype(np.float64)
+    ref64 = oracle.jacobi2d(A64, T, coef=coef, terms=tm)
+    At64 = t(A64)
+    device.jacobi2d(At64, T, coef=coef, terms=tm)
+    np.testing.assert_array_equal(At64.cpu().numpy(), ref64)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 384, 128), (1000, 777, 300), (64, 200, 4),
+                                   (129, 130, 36), (512, 512, 4096)])
+def test_gemm_3xtf32(M, N, K):
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(M + N + K)
+    a = rng.random((M, K), dtype=np.float32) - 0.5
+    b = rng.random((K, N), dtype=np.float32) - 0.5
+    ref = oracle.matmul(a, b)
+    C = torch.full((M, N), 7.0, dtype=torch.float32, device=DEV)
+    device.gemm(t(a), t(b), C, device.gemm_workspace(M, N, K, DEV))
+    got = C.cpu().numpy().astype(np.float64)
+    scale = np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64)
+    err = np.abs(got - ref) / scale
+    assert err.max() < 1e-5, f"max rel (to |A||B|) err {err.max():.3e}"
+    C2 = torch.zeros((M, N), dtype=torch.float32, device=DEV)
+    device.gemm_simt(t(a), t(b), C2)
+    assert (np.abs(C2.cpu().numpy() - ref) / scale).max() < 1e-5
+
+
+# ------------------------------------------------ BASELINE shapes (properties)
+
+def test_full_histogram_4096():
+    from paper_1902_10345_b200 import device
+    img = np.random.default_rng(0).random((4096, 4096), dtype=np.float32)
+    h = torch.zeros(256, dtype=torch.int64, device=DEV)
+    oob = torch.zeros(1, dtype=torch.int64, device=DEV)
+    device.hist(t(img), h, oob)
+    ref, _ = oracle.histogram(img, np.zeros(256, np.int64))
+    np.testing.assert_array_equal(h.cpu().numpy(), ref)
+    assert int(h.sum()) == img.size
+
+
+def test_full_query_2pow26():
+    from paper_1902_10345_b200 import device
+    col = np.random.default_rng(1).random(1 << 26, dtype=np.float32)
+    out = torch.zeros(col.size, dtype=torch.float32, device=DEV)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    device.query(t(col), 0.5, out, cnt, device.query_workspace(col.size, 4, DEV), "<")
+    k = int(cnt.item())
+    sel = col[col < 0.5]
+    assert k == sel.size
+    np.testing.assert_array_equal(out[:k].cpu().numpy(), sel)
+
+
+def test_full_jacobi_8192_three_steps():
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(2)
+    A = np.zeros((2, 8192, 8192), np.float32)
+    A[0, 1:-1, 1:-1] = rng.random((8190, 8190), dtype=np.float32)
+    A[1] = A[0]
+    ref = oracle.jacobi2d(A, 3, fp32=True)
+    At = t(A)
+    device.jacobi2d(At, 3)
+    np.testing.assert_array_equal(At.cpu().numpy(), ref)
+
+
+def test_full_spmv_2pow22_rows_sampled():
+    from paper_1902_10345_b200 import device
+    H = W = 1 << 22
+    rng = np.random.default_rng(3)
+    col = np.sort(rng.integers(0, W, (H, 64), dtype=np.int32), axis=1).reshape(-1)
+    val = rng.random(H * 64, dtype=np.float32)
+    x = rng.random(W, dtype=np.float32)
+    rowptr = (np.arange(H + 1, dtype=np.int64) * 64).astype(np.int32)
+    b = torch.zeros(H, dtype=torch.float32, device=DEV)
+    device.spmv(t(rowptr), t(col), t(val), t(x), b)
+    rows = rng.integers(0, H, 4096)
+    got = b.cpu().numpy()[rows]
+    ref = np.array([np.dot(val[r * 64:(r + 1) * 64].astype(np.float64),
+                           x[col[r * 64:(r + 1) * 64]].astype(np.float64)) for r in rows])
+    np.testing.assert_allclose(got, ref, rtol=1e-5)
+
+
+@pytest.mark.parametrize("n", [4096, 16384])
+def test_full_gemm_rows_sampled(n):
+    from paper_1902_10345_b200 import device
+    g = torch.Generator(device=DEV).manual_seed(4)
+    A = torch.rand(n, n, device=DEV, generator=g)
+    B = torch.rand(n, n, device=DEV, generator=g)
+    C = torch.empty(n, n, device=DEV)
+    device.gemm(A, B, C, device.gemm_workspace(n, n, n, DEV))
+    rows = [0, 1, n // 3, n // 2, n - 2, n - 1]
+    a = A[rows].cpu().numpy()
+    bh = B.cpu().numpy()
+    ref = oracle.matmul(a, bh)
+    got = C[rows].cpu().numpy()
+    assert (np.abs(got - ref) / np.abs(ref)).max() < 1e-4
