@@ -16,8 +16,13 @@
 //   * warp 0: TMA producer over a 3-stage smem ring (64 KB/stage), mbarrier
 //     full/empty pipeline;
 //   * warp 1: single-thread tcgen05.mma.kind::tf32 issuer, M=128 N=128 K=8,
-//     3 MMAs per K=8 step into one TMEM accumulator (128 lanes x 128 cols),
-//     tcgen05.commit frees smem stages and finally signals the epilogue;
+//     3 MMAs per K=8 step; k-blocks go round-robin into NACC = 4 TMEM
+//     accumulators (4 x 128 cols = all 512 columns).  The tensor core's fp32
+//     accumulation is biased (measured: -1.7e-4 rel at K=16384 with one
+//     accumulator on positive data); four partial sums cut the accumulated
+//     magnitude per accumulator by 4x and are combined in the epilogue with
+//     IEEE round-to-nearest adds;
+//   * tcgen05.commit frees smem stages and finally signals the epilogue;
 //   * warp 2: TMEM allocator; warps 4-7: tcgen05.ld -> registers -> C.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -151,6 +156,7 @@ constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
 constexpr int TILE_BYTES = BM * BK * 4;              // 16 KB (BM == BN)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo
 constexpr int GEMM_THREADS = 256;
+constexpr int NACC = 4;                              // TMEM accumulators (512 columns)
 constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -217,6 +223,8 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_consta
                 mbar_wait(&full[s], ph);
                 tc_fence_after();
                 const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+                const uint32_t dacc = tmem_d + (uint32_t)((kb % NACC) * BN);
+                const uint32_t first = kb < NACC;
 #pragma unroll
                 for (int k = 0; k < BK / 8; ++k) {
                     const uint32_t off = k * 32;  // 8 tf32 = 32 B along K inside the 128 B atom
@@ -224,9 +232,9 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_consta
                     const uint64_t alo = sw128_kmajor_desc(base + 1 * TILE_BYTES + off);
                     const uint64_t bhi = sw128_kmajor_desc(base + 2 * TILE_BYTES + off);
                     const uint64_t blo = sw128_kmajor_desc(base + 3 * TILE_BYTES + off);
-                    tc_mma_tf32(tmem_d, alo, bhi, idesc, (kb | k) != 0);
-                    tc_mma_tf32(tmem_d, ahi, blo, idesc, 1u);
-                    tc_mma_tf32(tmem_d, ahi, bhi, idesc, 1u);
+                    tc_mma_tf32(dacc, alo, bhi, idesc, !(first && k == 0));
+                    tc_mma_tf32(dacc, ahi, blo, idesc, 1u);
+                    tc_mma_tf32(dacc, ahi, bhi, idesc, 1u);
                 }
                 tc_commit(&empty[s]);
             }
@@ -237,10 +245,17 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_consta
         tc_fence_after();
         const int rw = (warp & 3) * 32;
         const int row = m0 + rw + lane;
+        const int nacc = KB < NACC ? KB : NACC;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
             uint32_t r[16];
             tmem_ld16(tmem_d + ((uint32_t)rw << 16) + c, r);
+            for (int q = 1; q < nacc; ++q) {  // (acc0 + acc1) + acc2 ... in RN fp32
+                uint32_t o[16];
+                tmem_ld16(tmem_d + ((uint32_t)rw << 16) + q * BN + c, o);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) + __uint_as_float(o[e]));
+            }
             if (row < M) {
                 float* dst = C + (int64_t)row * N + n0 + c;
                 if (n0 + c + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -261,7 +276,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_consta
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN * NACC));
     }
 }
 

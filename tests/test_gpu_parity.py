@@ -46,6 +46,11 @@ CASES = [c for m in SUPPORTED for c in load_cases(m)]
 
 # ------------------------------------------------ drop-in vs reference fixtures
 
+def _f32_exact(a):
+    a = np.asarray(a, np.float64)
+    return np.array_equal(a, a.astype(np.float32).astype(np.float64))
+
+
 @pytest.mark.parametrize("precision", ["native", "fp32"])
 @pytest.mark.parametrize("c", CASES, ids=repr)
 def test_dropin_matches_reference_interpreter(c, precision):
@@ -57,7 +62,21 @@ def test_dropin_matches_reference_interpreter(c, precision):
             prog.run(c.inputs, c.symbols)
         return
     got = prog.run(c.inputs, c.symbols)
-    for name, exp in c.outputs.items():
+    outputs = dict(c.outputs)
+    if precision == "fp32" and not all(_f32_exact(v) for v in c.inputs.values() if v.dtype.kind == "f"):
+        # fp32 precision rounds the inputs on the device (declared semantics):
+        # the expectation is the oracle on the rounded inputs
+        if c.motif == "histogram":
+            outputs["hist"] = oracle.histogram(c.inputs["img"].astype(np.float32), c.inputs["hist"])[0]
+        elif c.motif.startswith("query"):
+            op = ">" if c.motif == "query_gallery" else "<"
+            o, n = oracle.query(c.inputs["col"].astype(np.float32), c.inputs["thr"][0],
+                                np.zeros(c.inputs["col"].size, np.float32), c.inputs["count"], op)
+            k = int(n[0] - c.inputs["count"][0])
+            full = np.array(c.inputs["out_vals"], np.float64)
+            full[:k] = o[:k]
+            outputs["out_vals"], outputs["count"] = full, n
+    for name, exp in outputs.items():
         g = got[name].reshape(exp.shape)
         if exp.dtype.kind == "i" or c.motif.startswith(("histogram", "query")):
             np.testing.assert_array_equal(g, exp, err_msg=name)
