@@ -156,7 +156,14 @@ constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
 constexpr int TILE_BYTES = BM * BK * 4;              // 16 KB (BM == BN)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo
 constexpr int GEMM_THREADS = 256;
-constexpr int NACC = 4;                              // TMEM accumulators (512 columns)
+#ifndef SDFGB_GEMM_NACC
+#define SDFGB_GEMM_NACC 4
+#endif
+#ifndef SDFGB_GEMM_TMEM_COLS
+#define SDFGB_GEMM_TMEM_COLS (BN * SDFGB_GEMM_NACC)
+#endif
+constexpr int NACC = SDFGB_GEMM_NACC;                // TMEM accumulators
+constexpr int TMEM_COLS = SDFGB_GEMM_TMEM_COLS;      // power of two >= 32
 constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -192,7 +199,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_consta
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(BN));
+                     "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -276,7 +283,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_consta
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN * NACC));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(TMEM_COLS));
     }
 }
 

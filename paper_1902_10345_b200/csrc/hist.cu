@@ -19,6 +19,7 @@
 //     grid/8 x bins global atomics (the 2 KB hist lives in 4 L2 slices, so
 //     per-CTA global merges would serialise there).
 #include <algorithm>
+#include <cmath>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -33,36 +34,30 @@ constexpr int kHistUnroll = 4;
 constexpr int kHistCluster = 8;
 constexpr int kMaxSmemBins = 12288;  // 48 KB of uint32 counters per replica set
 
-enum BinMode { kScaled = 0, kIdentity = 1 };
+enum BinMode { kScaled = 0, kIdentity = 1, kPow2 = 2 };
 
+// bin of one element; false when out of [0, bins) (NaN included)
 template <typename T, int MODE>
-__device__ __forceinline__ bool bin_of(T v, double scale, double div, bool has_div,
+__device__ __forceinline__ bool bin_of(T v, double scale, double div, bool has_div, float scale_f,
                                        int64_t bins, int& bin) {
     if constexpr (MODE == kIdentity) {
         int64_t k = (int64_t)v;
         bin = (int)k;
         return k >= 0 && k < bins;
+    } else if constexpr (MODE == kPow2) {
+        // fp32 input, scale = 2^k (k >= 0), div = 1: v * scale is exact in fp32,
+        // so floor in fp32 equals the reference's floor in double.  floor via a
+        // round-down add of 2^23 (exact for 0 <= t < 2^23) keeps the XU pipe idle.
+        const float t = (float)v * scale_f;
+        const bool ok = (t >= 0.0f) & (t < (float)bins);
+        bin = __float_as_int(__fadd_rd(t, 8388608.0f)) - 0x4B000000;
+        return ok;
     } else {
         double q = (double)v * scale;
         if (has_div) q = q / div;
         q = floor(q);
         bin = (int)q;
         return q >= 0.0 && q < (double)bins;  // NaN -> false
-    }
-}
-
-template <typename T, int MODE>
-__device__ __forceinline__ void bump(uint32_t* h, T v, double scale, double div, bool has_div,
-                                     int64_t bins, uint32_t& bad) {
-    int b;
-    bool ok = bin_of<T, MODE>(v, scale, div, has_div, bins, b);
-    unsigned okm = __ballot_sync(0xffffffffu, ok);
-    bad += 32 - __popc(okm);
-    int b0 = __shfl_sync(0xffffffffu, b, 0);
-    if (okm == 0xffffffffu && __all_sync(0xffffffffu, b == b0)) {
-        if ((threadIdx.x & 31) == 0) atomicAdd(&h[b0], 32u);
-    } else if (ok) {
-        atomicAdd(&h[b], 1u);
     }
 }
 
@@ -75,6 +70,7 @@ hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale
     using V = typename Vec16<T>::type;
     constexpr int VN = Vec16<T>::n;
     const bool has_div = div != 1.0;
+    const float scale_f = (float)scale;
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
 
@@ -83,71 +79,42 @@ hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale
 
     uint32_t* h = sh + (warp % reps) * bins;
     uint32_t bad = 0;
+    auto bump = [&](T v) {
+        int b;
+        const bool ok = bin_of<T, MODE>(v, scale, div, has_div, scale_f, bins, b);
+        if (ok) atomicAdd(&h[b], 1u);
+        bad += !ok;
+    };
 
-    // misaligned head (< VN elements) and the ragged tail: whole warps, lane-masked
+    // misaligned head (< VN elements) and ragged tail: block 0, scalar
     const int64_t nvec = (n - head) / VN;
     const int64_t tail0 = head + nvec * VN;
-    if (blockIdx.x == 0 && warp == 0) {
-        const int lane = tid & 31;
-        for (int64_t base = 0; base < head; base += 32) {
-            int64_t p = base + lane;
-            // out-of-range lanes feed a sentinel the ballot discounts below
-            bool live = p < head;
-            T v = live ? in[p] : T(0);
-            int b;
-            bool ok = live && bin_of<T, MODE>(v, scale, div, has_div, bins, b);
-            unsigned okm = __ballot_sync(0xffffffffu, ok);
-            unsigned livem = __ballot_sync(0xffffffffu, live);
-            bad += __popc(livem) - __popc(okm);
-            if (ok) atomicAdd(&h[b], 1u);
-        }
-        for (int64_t base = tail0; base < n; base += 32) {
-            int64_t p = base + lane;
-            bool live = p < n;
-            T v = live ? in[p] : T(0);
-            int b;
-            bool ok = live && bin_of<T, MODE>(v, scale, div, has_div, bins, b);
-            unsigned okm = __ballot_sync(0xffffffffu, ok);
-            unsigned livem = __ballot_sync(0xffffffffu, live);
-            bad += __popc(livem) - __popc(okm);
-            if (ok) atomicAdd(&h[b], 1u);
-        }
+    if (blockIdx.x == 0) {
+        for (int64_t p = tid; p < head; p += blockDim.x) bump(in[p]);
+        for (int64_t p = tail0 + tid; p < n; p += blockDim.x) bump(in[p]);
     }
 
     const V* vin = reinterpret_cast<const V*>(in + head);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
     // main body: kHistUnroll vectors in flight per thread
-    const int lane = tid & 31;
-    // loop bounds are taken on the warp's first lane so whole warps stay
-    // converged for the votes in bump()
-    for (; (i - lane) + 31 + (kHistUnroll - 1) * stride < nvec; i += kHistUnroll * stride) {
+    for (; i + (kHistUnroll - 1) * stride < nvec; i += kHistUnroll * stride) {
         V v[kHistUnroll];
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u) v[u] = ldg_stream(vin + i + u * stride);
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u)
 #pragma unroll
-            for (int c = 0; c < VN; ++c)
-                bump<T, MODE>(h, vget<V, T>(v[u], c), scale, div, has_div, bins, bad);
+            for (int c = 0; c < VN; ++c) bump(vget<V, T>(v[u], c));
     }
-    // remainder vectors: keep whole warps converged for the warp votes
-    for (; i - lane < nvec; i += stride) {
-        bool live = i < nvec;
-        V v = live ? ldg_stream(vin + i) : V{};
+    for (; i < nvec; i += stride) {
+        V v = ldg_stream(vin + i);
 #pragma unroll
-        for (int c = 0; c < VN; ++c) {
-            T x = vget<V, T>(v, c);
-            int b;
-            bool ok = live && bin_of<T, MODE>(x, scale, div, has_div, bins, b);
-            unsigned okm = __ballot_sync(0xffffffffu, ok);
-            unsigned livem = __ballot_sync(0xffffffffu, live);
-            bad += __popc(livem) - __popc(okm);
-            if (ok) atomicAdd(&h[b], 1u);
-        }
+        for (int c = 0; c < VN; ++c) bump(vget<V, T>(v, c));
     }
 
-    // out-of-range count (lane 0 of each warp holds the warp's ballot totals)
+#pragma unroll
+    for (int d = 16; d; d >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, d);
     if ((tid & 31) == 0 && bad) atomicAdd(oob, (unsigned long long)bad);
 
     __syncthreads();
@@ -184,7 +151,7 @@ hist_global_kernel(const T* __restrict__ in, int64_t n, double scale, double div
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         int b;
-        if (bin_of<T, MODE>(in[p], scale, div, has_div, bins, b))
+        if (bin_of<T, MODE>(in[p], scale, div, has_div, (float)scale, bins, b))
             atomicAdd(&hist[b], 1ull);
         else
             atomicAdd(oob, 1ull);
@@ -230,8 +197,19 @@ int launch_hist(const T* img, int64_t n, double scale, double div, int64_t* hist
 }  // namespace
 }  // namespace sdfgb
 
+namespace {
+// scale = 2^k with k >= 0, div == 1, and bins < 2^23: the fp32 fast path is exact
+bool pow2_exact(double scale, double div, int64_t bins) {
+    if (div != 1.0 || !(scale >= 1.0) || scale > 1073741824.0 || bins >= (1 << 23)) return false;
+    int e;
+    return frexp(scale, &e) == 0.5;
+}
+}  // namespace
+
 extern "C" int sdfgb_hist_f32(const float* img, int64_t n, double scale, double div,
                               int64_t* hist, int64_t bins, uint64_t* oob, void* stream) {
+    if (pow2_exact(scale, div, bins))
+        return sdfgb::launch_hist<float, sdfgb::kPow2>(img, n, scale, div, hist, bins, oob, stream);
     return sdfgb::launch_hist<float, sdfgb::kScaled>(img, n, scale, div, hist, bins, oob, stream);
 }
 extern "C" int sdfgb_hist_f64(const double* img, int64_t n, double scale, double div,

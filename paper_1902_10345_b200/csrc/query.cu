@@ -8,10 +8,12 @@
 // (codegen.py:123-143, :462-471); the FIFO order is the map's iteration order.
 //
 // B200 design: single pass, HBM-bound (read 4N, write 4n).  Each CTA owns a
-// tile of 16 elements x 256 threads; predicate bits -> per-thread counts ->
-// one 64-bit packed block scan (4 chunk counters in 16-bit lanes) -> tile
-// aggregate -> decoupled look-back over per-tile status words for the tile's
-// global offset -> survivors are written at their input-order rank.  The
+// tile of 16 elements x 512 threads (32 KB); predicate bits -> per-thread
+// counts -> one 64-bit packed block scan (4 chunk counters in 16-bit lanes)
+// -> survivors staged in smem at their tile-local rank -> decoupled look-back
+// (block-wide: 512 predecessor tiles per round, so the chain to the nearest
+// published prefix is resolved in ~1 round even with every SM's tiles in
+// flight) -> one contiguous, coalesced store of the tile's survivors.  The
 // output is therefore IDENTICAL to the CPU FIFO order, not just the same set.
 //
 // Tile ids come from an atomic ticket (a CTA only obtains a tile once running,
@@ -26,7 +28,7 @@
 namespace sdfgb {
 namespace {
 
-constexpr int kQBlock = 256;
+constexpr int kQBlock = 512;
 constexpr int kQVecPerThread = 4;
 
 constexpr uint64_t kFlagAgg = 1ull;
@@ -62,10 +64,13 @@ query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __rest
     constexpr int VN = Vec16<T>::n;
     constexpr int K = kQVecPerThread;
     constexpr int TILE = kQBlock * K * VN;
+    constexpr int NW = kQBlock / 32;
 
-    __shared__ int64_t s_tile;
-    __shared__ uint64_t s_warp[kQBlock / 32];
-    __shared__ int64_t s_excl;
+    __shared__ T s_stage[TILE];
+    __shared__ uint64_t s_warp[NW];
+    __shared__ int64_t s_red[NW];
+    __shared__ int64_t s_tile, s_excl;
+    __shared__ int s_first;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = (int64_t)atomicAdd(&ws->ticket, 1ull);
@@ -108,74 +113,72 @@ query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __rest
         if (lane >= d) incl += o;
     }
     if (lane == 31) s_warp[warp] = incl;
+    if (tid == 0) s_first = kQBlock;
     __syncthreads();
     uint64_t wpre = 0, total = 0;
 #pragma unroll
-    for (int w = 0; w < kQBlock / 32; ++w) {
+    for (int w = 0; w < NW; ++w) {
         uint64_t t = s_warp[w];
         if (w < warp) wpre += t;
         total += t;
     }
     const uint64_t excl = wpre + incl - mine;
-    uint32_t chunk_base[K];
     uint32_t agg = 0;
+    // ---- stage survivors in smem at their tile-local input-order rank
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        chunk_base[k] = agg;
+        uint32_t r = agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
+#pragma unroll
+        for (int c = 0; c < VN; ++c)
+            if (bits & (1u << (k * VN + c))) s_stage[r++] = v[k][c];
         agg += (uint32_t)((total >> (16 * k)) & 0xffff);
     }
 
-    // ---- decoupled look-back for the tile's global offset
-    if (warp == 0) {
-        int64_t prefix = 0;
-        if (tile == 0) {
-            if (lane == 0) st_relaxed(&ws->status[0], pack_status(epoch, kFlagPrefix, agg));
-        } else {
-            if (lane == 0) st_relaxed(&ws->status[tile], pack_status(epoch, kFlagAgg, agg));
-            int64_t pred = tile - 1;
-            while (true) {
-                const int64_t idx = pred - lane;
-                uint64_t w;
-                bool valid;
-                do {
-                    if (idx >= 0) {
-                        w = ld_relaxed(&ws->status[idx]);
-                        valid = (uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull);
-                    } else {
-                        w = pack_status(epoch, kFlagPrefix, 0);  // before tile 0
-                        valid = true;
-                    }
-                } while (!__all_sync(0xffffffffu, valid));
-                const bool is_prefix = ((w >> kValueBits) & 3ull) == kFlagPrefix;
-                const unsigned pm = __ballot_sync(0xffffffffu, is_prefix);
-                const int stop = pm ? __ffs(pm) - 1 : 31;  // lanes 0..stop contribute
-                uint64_t val = lane <= stop ? (w & kValueMask) : 0;
-#pragma unroll
-                for (int d = 16; d; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
-                prefix += (int64_t)val;
-                if (pm) break;
-                pred -= 32;
-            }
-            if (lane == 0)
-                st_relaxed(&ws->status[tile], pack_status(epoch, kFlagPrefix, prefix + agg));
+    // ---- decoupled look-back, block-wide: a 512-tile window per round
+    if (tile == 0) {
+        if (tid == 0) {
+            st_relaxed(&ws->status[0], pack_status(epoch, kFlagPrefix, agg));
+            s_excl = 0;
         }
-        if (lane == 0) {
+    } else {
+        if (tid == 0) st_relaxed(&ws->status[tile], pack_status(epoch, kFlagAgg, agg));
+        int64_t prefix = 0;
+        int64_t pred = tile - 1;
+        while (true) {
+            const int64_t idx = pred - tid;
+            uint64_t w = pack_status(epoch, kFlagPrefix, 0);  // before tile 0
+            if (idx >= 0) {
+                while (true) {
+                    w = ld_relaxed(&ws->status[idx]);
+                    if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
+                    __nanosleep(32);
+                }
+            }
+            if (((w >> kValueBits) & 3ull) == kFlagPrefix) atomicMin(&s_first, tid);
+            __syncthreads();
+            const int first = s_first;
+            int64_t val = tid <= first ? (int64_t)(w & kValueMask) : 0;
+#pragma unroll
+            for (int d = 16; d; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
+            if (lane == 0) s_red[warp] = val;
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < NW; ++q) prefix += s_red[q];
+            if (first < kQBlock) break;
+            pred -= kQBlock;
+            __syncthreads();  // s_red / s_first reuse
+        }
+        if (tid == 0) {
+            st_relaxed(&ws->status[tile], pack_status(epoch, kFlagPrefix, prefix + agg));
             s_excl = prefix;
-            if (tile == num_tiles - 1) atomicAdd(count, (unsigned long long)(prefix + agg));
         }
     }
     __syncthreads();
-
-    // ---- scatter survivors at their input-order rank
     const int64_t obase = s_excl;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        uint32_t r = chunk_base[k] + (uint32_t)((excl >> (16 * k)) & 0xffff);
-#pragma unroll
-        for (int c = 0; c < VN; ++c) {
-            if (bits & (1u << (k * VN + c))) out[obase + r++] = v[k][c];
-        }
-    }
+    if (tid == 0 && tile == num_tiles - 1) atomicAdd(count, (unsigned long long)(obase + agg));
+
+    // ---- drain: contiguous, coalesced stores of the staged survivors
+    for (uint32_t r = tid; r < agg; r += kQBlock) out[obase + r] = s_stage[r];
 
     // ---- last CTA out resets the counters for the next launch
     if (tid == 0) {
