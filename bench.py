@@ -296,7 +296,7 @@ def bench_spmv(args, dist, P):
     nnz = H * nz
     by = nnz * 8 + 4 * (H + 1) + 4 * W + 8 * H
     res = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms, "bytes_per_unit": by,
-           "launches_per_step": 1, "roofline": roof("hbm", by / ms / 1e6, P, "spmv_warp_row_kernel"),
+           "launches_per_step": 1, "roofline": roof("hbm", by / ms / 1e6, P, "spmv_hw_vec4_kernel"),
            "l2": "matrix 2 GiB > L2 (x, 16 MiB, is L2-resident by design)",
            "config": {"workload": "CSR SpMV 2^22 x 2^22, 64 nnz/row fp32/int32", "H": H, "nnz": nnz}}
     if args.e2e:

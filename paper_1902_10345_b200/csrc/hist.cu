@@ -97,20 +97,25 @@ hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale
     const V* vin = reinterpret_cast<const V*>(in + head);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + tid;
-    // main body: kHistUnroll vectors in flight per thread
-    for (; i + (kHistUnroll - 1) * stride < nvec; i += kHistUnroll * stride) {
-        V v[kHistUnroll];
+    // software pipeline: the next kHistUnroll vectors are in flight while the
+    // current ones are binned
+    V cur[kHistUnroll];
 #pragma unroll
-        for (int u = 0; u < kHistUnroll; ++u) v[u] = ldg_stream(vin + i + u * stride);
+    for (int u = 0; u < kHistUnroll; ++u)
+        cur[u] = (i + u * stride < nvec) ? ldg_stream(vin + i + u * stride) : V{};
+    for (; i < nvec; i += kHistUnroll * stride) {
+        V nxt[kHistUnroll];
+        const int64_t j = i + kHistUnroll * stride;
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u)
+            nxt[u] = (j + u * stride < nvec) ? ldg_stream(vin + j + u * stride) : V{};
 #pragma unroll
-            for (int c = 0; c < VN; ++c) bump(vget<V, T>(v[u], c));
-    }
-    for (; i < nvec; i += stride) {
-        V v = ldg_stream(vin + i);
+        for (int u = 0; u < kHistUnroll; ++u)
+            if (i + u * stride < nvec)
 #pragma unroll
-        for (int c = 0; c < VN; ++c) bump(vget<V, T>(v, c));
+                for (int c = 0; c < VN; ++c) bump(vget<V, T>(cur[u], c));
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; ++u) cur[u] = nxt[u];
     }
 
 #pragma unroll
@@ -186,7 +191,22 @@ int launch_hist(const T* img, int64_t n, double scale, double div, int64_t* hist
     if (head > n) head = n;
     int64_t nvec = (n - head) / VN;
     int64_t want = (nvec + (int64_t)kHistBlock * kHistUnroll - 1) / ((int64_t)kHistBlock * kHistUnroll);
-    int64_t cap = (int64_t)num_sms() * (2048 / kHistBlock);
+    // one wave of co-resident clusters (a second partial wave would double the tail)
+    static int clusters[3][2] = {};
+    int& nc = clusters[MODE][sizeof(T) == 8];
+    if (nc == 0) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kHistCluster * 64);
+        cfg.blockDim = dim3(kHistBlock);
+        cfg.dynamicSmemBytes = smem;
+        if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc <= 0) {
+            cudaGetLastError();
+            int per_sm = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHistBlock, smem);
+            nc = std::max(1, per_sm * num_sms() / kHistCluster * 7 / 8);
+        }
+    }
+    int64_t cap = (int64_t)nc * kHistCluster;
     int64_t blocks = std::max<int64_t>(1, std::min(want, cap));
     blocks = (blocks + kHistCluster - 1) / kHistCluster * kHistCluster;
     kern<<<(unsigned)blocks, kHistBlock, smem, s>>>(img, n, head, scale, div, bins, reps, H, O);

@@ -55,12 +55,32 @@ __device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, u
     return ((uint64_t)epoch << 44) | (flag << kValueBits) | (value & kValueMask);
 }
 
+template <typename T, bool VEC, int K, int VN>
+__device__ __forceinline__ void q_load(const T* __restrict__ col, int64_t n, int64_t base, int tid,
+                                       T (&v)[K][VN]) {
+    using V = typename Vec16<T>::type;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
+        if (VEC && e0 + VN <= n) {
+            V x = ldg_stream(reinterpret_cast<const V*>(col + e0));
+#pragma unroll
+            for (int c = 0; c < VN; ++c) v[k][c] = vget<V, T>(x, c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < VN; ++c) v[k][c] = (e0 + c < n) ? col[e0 + c] : T(0);
+        }
+    }
+}
+
+// Persistent CTAs: each loops over tiles taken from the ticket counter.  The
+// next tile's loads are issued before the current tile's look-back, so HBM
+// stays busy while a CTA waits for its predecessors.
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kQBlock)
 query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __restrict__ out,
              unsigned long long* __restrict__ count, QueryWs* __restrict__ ws,
              int64_t num_tiles, uint32_t epoch) {
-    using V = typename Vec16<T>::type;
     constexpr int VN = Vec16<T>::n;
     constexpr int K = kQVecPerThread;
     constexpr int TILE = kQBlock * K * VN;
@@ -75,116 +95,106 @@ query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __rest
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = (int64_t)atomicAdd(&ws->ticket, 1ull);
     __syncthreads();
-    const int64_t tile = s_tile;
-    const int64_t base = tile * TILE;
-
-    // ---- load + predicate (element e = base + k*kQBlock*VN + tid*VN + c)
+    int64_t tile = s_tile;
     T v[K][VN];
-    uint32_t bits = 0;  // bit k*VN+c
+    if (tile < num_tiles) q_load<T, VEC, K, VN>(col, n, tile * TILE, tid, v);
+
+    while (tile < num_tiles) {
+        const int64_t base = tile * TILE;
+        // ---- predicate (element e = base + k*kQBlock*VN + tid*VN + c)
+        uint32_t bits = 0;  // bit k*VN+c
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
-        if (VEC && e0 + VN <= n) {
-            V x = ldg_stream(reinterpret_cast<const V*>(col + e0));
-#pragma unroll
-            for (int c = 0; c < VN; ++c) v[k][c] = vget<V, T>(x, c);
+        for (int k = 0; k < K; ++k) {
+            const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
 #pragma unroll
             for (int c = 0; c < VN; ++c)
-                bits |= (uint32_t)cmp_apply((double)v[k][c], op, thr) << (k * VN + c);
-        } else {
-#pragma unroll
-            for (int c = 0; c < VN; ++c) {
-                const bool live = e0 + c < n;
-                v[k][c] = live ? col[e0 + c] : T(0);
-                bits |= (uint32_t)(live && cmp_apply((double)v[k][c], op, thr)) << (k * VN + c);
-            }
+                bits |= (uint32_t)((e0 + c < n) && cmp_apply((double)v[k][c], op, thr)) << (k * VN + c);
         }
-    }
-
-    // ---- packed block scan: 16-bit field k = this thread's count in chunk k
-    uint64_t mine = 0;
+        // ---- packed block scan: 16-bit field k = this thread's count in chunk k
+        uint64_t mine = 0;
 #pragma unroll
-    for (int k = 0; k < K; ++k)
-        mine |= (uint64_t)__popc((bits >> (k * VN)) & ((1u << VN) - 1)) << (16 * k);
-    uint64_t incl = mine;
+        for (int k = 0; k < K; ++k)
+            mine |= (uint64_t)__popc((bits >> (k * VN)) & ((1u << VN) - 1)) << (16 * k);
+        uint64_t incl = mine;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += o;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    if (tid == 0) s_first = kQBlock;
-    __syncthreads();
-    uint64_t wpre = 0, total = 0;
+        for (int d = 1; d < 32; d <<= 1) {
+            uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += o;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        if (tid == 0) s_first = kQBlock;
+        __syncthreads();
+        uint64_t wpre = 0, total = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        uint64_t t = s_warp[w];
-        if (w < warp) wpre += t;
-        total += t;
-    }
-    const uint64_t excl = wpre + incl - mine;
-    uint32_t agg = 0;
-    // ---- stage survivors in smem at their tile-local input-order rank
+        for (int w = 0; w < NW; ++w) {
+            uint64_t t = s_warp[w];
+            if (w < warp) wpre += t;
+            total += t;
+        }
+        const uint64_t excl = wpre + incl - mine;
+        // ---- stage survivors in smem at their tile-local input-order rank
+        uint32_t agg = 0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        uint32_t r = agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
+        for (int k = 0; k < K; ++k) {
+            uint32_t r = agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
 #pragma unroll
-        for (int c = 0; c < VN; ++c)
-            if (bits & (1u << (k * VN + c))) s_stage[r++] = v[k][c];
-        agg += (uint32_t)((total >> (16 * k)) & 0xffff);
-    }
-
-    // ---- decoupled look-back, block-wide: a 512-tile window per round
-    if (tile == 0) {
+            for (int c = 0; c < VN; ++c)
+                if (bits & (1u << (k * VN + c))) s_stage[r++] = v[k][c];
+            agg += (uint32_t)((total >> (16 * k)) & 0xffff);
+        }
         if (tid == 0) {
-            st_relaxed(&ws->status[0], pack_status(epoch, kFlagPrefix, agg));
-            s_excl = 0;
+            st_relaxed(&ws->status[tile],
+                       pack_status(epoch, tile == 0 ? kFlagPrefix : kFlagAgg, agg));
+            s_tile = (int64_t)atomicAdd(&ws->ticket, 1ull);
         }
-    } else {
-        if (tid == 0) st_relaxed(&ws->status[tile], pack_status(epoch, kFlagAgg, agg));
+        __syncthreads();
+        const int64_t next = s_tile;
+        // ---- prefetch the next tile while this one resolves its offset
+        if (next < num_tiles) q_load<T, VEC, K, VN>(col, n, next * TILE, tid, v);
+
+        // ---- decoupled look-back, block-wide: a kQBlock-tile window per round
         int64_t prefix = 0;
-        int64_t pred = tile - 1;
-        while (true) {
-            const int64_t idx = pred - tid;
-            uint64_t w = pack_status(epoch, kFlagPrefix, 0);  // before tile 0
-            if (idx >= 0) {
-                while (true) {
-                    w = ld_relaxed(&ws->status[idx]);
-                    if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
-                    __nanosleep(32);
+        if (tile > 0) {
+            int64_t pred = tile - 1;
+            while (true) {
+                const int64_t idx = pred - tid;
+                uint64_t w = pack_status(epoch, kFlagPrefix, 0);  // before tile 0
+                if (idx >= 0) {
+                    while (true) {
+                        w = ld_relaxed(&ws->status[idx]);
+                        if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
+                        __nanosleep(20);
+                    }
                 }
+                if (((w >> kValueBits) & 3ull) == kFlagPrefix) atomicMin(&s_first, tid);
+                __syncthreads();
+                const int first = s_first;
+                int64_t val = tid <= first ? (int64_t)(w & kValueMask) : 0;
+#pragma unroll
+                for (int d = 16; d; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
+                if (lane == 0) s_red[warp] = val;
+                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < NW; ++q) prefix += s_red[q];
+                if (first < kQBlock) break;
+                pred -= kQBlock;
+                __syncthreads();  // s_red reuse
             }
-            if (((w >> kValueBits) & 3ull) == kFlagPrefix) atomicMin(&s_first, tid);
-            __syncthreads();
-            const int first = s_first;
-            int64_t val = tid <= first ? (int64_t)(w & kValueMask) : 0;
-#pragma unroll
-            for (int d = 16; d; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
-            if (lane == 0) s_red[warp] = val;
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < NW; ++q) prefix += s_red[q];
-            if (first < kQBlock) break;
-            pred -= kQBlock;
-            __syncthreads();  // s_red / s_first reuse
+            if (tid == 0) st_relaxed(&ws->status[tile], pack_status(epoch, kFlagPrefix, prefix + agg));
         }
-        if (tid == 0) {
-            st_relaxed(&ws->status[tile], pack_status(epoch, kFlagPrefix, prefix + agg));
-            s_excl = prefix;
-        }
-    }
-    __syncthreads();
-    const int64_t obase = s_excl;
-    if (tid == 0 && tile == num_tiles - 1) atomicAdd(count, (unsigned long long)(obase + agg));
+        if (tid == 0 && tile == num_tiles - 1) atomicAdd(count, (unsigned long long)(prefix + agg));
 
-    // ---- drain: contiguous, coalesced stores of the staged survivors
-    for (uint32_t r = tid; r < agg; r += kQBlock) out[obase + r] = s_stage[r];
+        // ---- drain: contiguous, coalesced stores of the staged survivors
+        for (uint32_t r = tid; r < agg; r += kQBlock) out[prefix + r] = s_stage[r];
+        __syncthreads();  // s_stage / s_first / s_red reuse by the next tile
+        tile = next;
+    }
 
     // ---- last CTA out resets the counters for the next launch
     if (tid == 0) {
         __threadfence();
         unsigned long long d = atomicAdd(&ws->done, 1ull);
-        if (d == (unsigned long long)num_tiles - 1) {
+        if (d == (unsigned long long)gridDim.x - 1) {
             ws->ticket = 0;
             ws->done = 0;
             __threadfence();
@@ -226,12 +236,12 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
     auto* C = reinterpret_cast<unsigned long long*>(count);
     const uint32_t epoch = next_epoch();
     cudaStream_t s = as_stream(stream);
-    if (vec)
-        query_kernel<T, true><<<(unsigned)tiles, kQBlock, 0, s>>>(col, n, op, thr, out, C, W,
-                                                                   tiles, epoch);
-    else
-        query_kernel<T, false><<<(unsigned)tiles, kQBlock, 0, s>>>(col, n, op, thr, out, C, W,
-                                                                    tiles, epoch);
+    auto kern = vec ? query_kernel<T, true> : query_kernel<T, false>;
+    static int occ[2][2] = {};  // [f64][vec] resident CTAs per SM
+    int& o = occ[sizeof(T) == 8][vec];
+    if (o == 0) SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kQBlock, 0));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(o, 1) * num_sms()));
+    kern<<<(unsigned)grid, kQBlock, 0, s>>>(col, n, op, thr, out, C, W, tiles, epoch);
     SDFGB_LAUNCHED("query_kernel");
     return SDFGB_OK;
 }

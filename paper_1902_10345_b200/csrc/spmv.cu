@@ -58,12 +58,68 @@ spmv_warp_row_kernel(const I* __restrict__ rowptr, const I* __restrict__ col,
     }
 }
 
+__device__ __forceinline__ float ldg_na(const float* p) {
+    float r;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    return r;
+}
+
+// fp32/int32 path: half-warp per row, 4 consecutive nnz per lane through
+// 128-bit col/val loads (one LDG.128 pair covers 64 nnz per half-warp), x
+// gathered with L1::no_allocate so random lines do not churn L1.
+__global__ void __launch_bounds__(kSpmvBlock)
+spmv_hw_vec4_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                    const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ b,
+                    int64_t H) {
+    const int lane = threadIdx.x & 31, hl = lane & 15;
+    const unsigned hmask = (lane < 16) ? 0x0000ffffu : 0xffff0000u;
+    const int64_t hw = (((int64_t)blockIdx.x * kSpmvBlock + threadIdx.x) >> 4);
+    const int64_t nhw = ((int64_t)gridDim.x * kSpmvBlock) >> 4;
+    for (int64_t r = hw; r < H; r += nhw) {
+        const int64_t rb = rowptr[r], re = rowptr[r + 1];
+        float s = 0.f;
+        if ((rb & 3) == 0) {
+            for (int64_t j = rb + 4 * hl; j < re; j += 64) {
+                if (j + 3 < re) {
+                    const int4 c = __ldg(reinterpret_cast<const int4*>(col + j));
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(val + j));
+                    const float x0 = ldg_na(x + c.x), x1 = ldg_na(x + c.y);
+                    const float x2 = ldg_na(x + c.z), x3 = ldg_na(x + c.w);
+                    s += v.x * x0;
+                    s += v.y * x1;
+                    s += v.z * x2;
+                    s += v.w * x3;
+                } else {
+                    for (int64_t q = j; q < re; ++q) s += __ldg(val + q) * ldg_na(x + __ldg(col + q));
+                }
+            }
+        } else {
+            for (int64_t j = rb + hl; j < re; j += 16) s += __ldg(val + j) * ldg_na(x + __ldg(col + j));
+        }
+#pragma unroll
+        for (int d = 8; d; d >>= 1) s += __shfl_xor_sync(hmask, s, d, 16);
+        if (hl == 0) b[r] += s;
+    }
+}
+
 template <typename I, typename T>
 int launch_spmv(const I* rowptr, const I* col, const T* val, const T* x, T* b, int64_t H,
                 void* stream) {
     if (H < 0 || (H > 0 && (!rowptr || !b)))
         return set_error(SDFGB_ERR_INVALID, "spmv: bad arguments");
     if (H == 0) return SDFGB_OK;
+    if constexpr (sizeof(T) == 4 && sizeof(I) == 4) {
+        if ((reinterpret_cast<uintptr_t>(col) & 15) == 0 && (reinterpret_cast<uintptr_t>(val) & 15) == 0) {
+            const int64_t need = (H * 16 + kSpmvBlock - 1) / kSpmvBlock;
+            const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)num_sms() * 8));
+            spmv_hw_vec4_kernel<<<(unsigned)blocks, kSpmvBlock, 0, as_stream(stream)>>>(
+                reinterpret_cast<const int32_t*>(rowptr), reinterpret_cast<const int32_t*>(col),
+                reinterpret_cast<const float*>(val), reinterpret_cast<const float*>(x),
+                reinterpret_cast<float*>(b), H);
+            SDFGB_LAUNCHED("spmv_hw_vec4_kernel");
+            return SDFGB_OK;
+        }
+    }
     const int64_t warps_needed = (H + 1) / 2;
     const int64_t blocks_needed = (warps_needed * 32 + kSpmvBlock - 1) / kSpmvBlock;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)num_sms() * 8));
