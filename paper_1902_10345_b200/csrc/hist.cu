@@ -45,13 +45,15 @@ __device__ __forceinline__ bool bin_of(T v, double scale, double div, bool has_d
         bin = (int)k;
         return k >= 0 && k < bins;
     } else if constexpr (MODE == kPow2) {
-        // fp32 input, scale = 2^k (k >= 0), div = 1: v * scale is exact in fp32,
-        // so floor in fp32 equals the reference's floor in double.  floor via a
-        // round-down add of 2^23 (exact for 0 <= t < 2^23) keeps the XU pipe idle.
-        const float t = (float)v * scale_f;
-        const bool ok = (t >= 0.0f) & (t < (float)bins);
-        bin = __float_as_int(__fadd_rd(t, 8388608.0f)) - 0x4B000000;
-        return ok;
+        // fp32 input, scale = 2^k (k >= 0), div = 1: v * scale is exact, so the
+        // floor can be taken in fp32 and equals the reference's floor in double.
+        // fma_rd(v, scale, 2^23) = floor(v*scale) + 2^23 exactly for
+        // 0 <= v*scale < 2^23, so its bit pattern minus 0x4B000000 is the bin;
+        // negative, >= 2^23, inf and NaN inputs all land outside [0, bins) as
+        // unsigned -- one FFMA + IADD + ISETP, nothing on the XU pipe.
+        const uint32_t b = (uint32_t)__float_as_int(__fmaf_rd((float)v, scale_f, 8388608.0f)) - 0x4B000000u;
+        bin = (int)b;
+        return b < (uint32_t)bins;
     } else {
         double q = (double)v * scale;
         if (has_div) q = q / div;
@@ -78,20 +80,18 @@ hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale
     __syncthreads();
 
     uint32_t* h = sh + (warp % reps) * bins;
-    uint32_t bad = 0;
+    uint32_t seen = 0;  // elements this thread binned or rejected (oob = seen - counted)
     auto bump = [&](T v) {
         int b;
-        const bool ok = bin_of<T, MODE>(v, scale, div, has_div, scale_f, bins, b);
-        if (ok) atomicAdd(&h[b], 1u);
-        bad += !ok;
+        if (bin_of<T, MODE>(v, scale, div, has_div, scale_f, bins, b)) atomicAdd(&h[b], 1u);
     };
 
     // misaligned head (< VN elements) and ragged tail: block 0, scalar
     const int64_t nvec = (n - head) / VN;
     const int64_t tail0 = head + nvec * VN;
     if (blockIdx.x == 0) {
-        for (int64_t p = tid; p < head; p += blockDim.x) bump(in[p]);
-        for (int64_t p = tail0 + tid; p < n; p += blockDim.x) bump(in[p]);
+        for (int64_t p = tid; p < head; p += blockDim.x, ++seen) bump(in[p]);
+        for (int64_t p = tail0 + tid; p < n; p += blockDim.x, ++seen) bump(in[p]);
     }
 
     const V* vin = reinterpret_cast<const V*>(in + head);
@@ -111,24 +111,34 @@ hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale
             nxt[u] = (j + u * stride < nvec) ? ldg_stream(vin + j + u * stride) : V{};
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u)
-            if (i + u * stride < nvec)
+            if (i + u * stride < nvec) {
+                seen += VN;
 #pragma unroll
                 for (int c = 0; c < VN; ++c) bump(vget<V, T>(cur[u], c));
+            }
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u) cur[u] = nxt[u];
     }
 
+    __shared__ unsigned long long s_seen, s_counted;
+    if (tid == 0) s_seen = s_counted = 0;
 #pragma unroll
-    for (int d = 16; d; d >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, d);
-    if ((tid & 31) == 0 && bad) atomicAdd(oob, (unsigned long long)bad);
-
+    for (int d = 16; d; d >>= 1) seen += __shfl_xor_sync(0xffffffffu, seen, d);
     __syncthreads();
+    if ((tid & 31) == 0) atomicAdd(&s_seen, (unsigned long long)seen);
     // fold replicas into replica 0
+    uint32_t counted = 0;
     for (int64_t k = tid; k < bins; k += blockDim.x) {
         uint32_t s = 0;
-        for (int r = 1; r < reps; ++r) s += sh[r * bins + k];
-        sh[k] += s;
+        for (int r = 0; r < reps; ++r) s += sh[r * bins + k];
+        sh[k] = s;
+        counted += s;
     }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) counted += __shfl_xor_sync(0xffffffffu, counted, d);
+    if ((tid & 31) == 0) atomicAdd(&s_counted, (unsigned long long)counted);
+    __syncthreads();
+    if (tid == 0 && s_seen != s_counted) atomicAdd(oob, s_seen - s_counted);
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
     if (cluster.block_rank() != 0) {

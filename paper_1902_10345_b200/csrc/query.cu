@@ -10,16 +10,13 @@
 // B200 design: single pass, HBM-bound (read 4N, write 4n).  Each CTA owns a
 // tile of 16 elements x 512 threads (32 KB); predicate bits -> per-thread
 // counts -> one 64-bit packed block scan (4 chunk counters in 16-bit lanes)
-// -> survivors staged in smem at their tile-local rank -> decoupled look-back
-// (block-wide: 512 predecessor tiles per round, so the chain to the nearest
-// published prefix is resolved in ~1 round even with every SM's tiles in
-// flight) -> one contiguous, coalesced store of the tile's survivors.  The
+// -> survivors staged in smem at their tile-local rank -> the tile's global
+// offset from a per-round all-gather of tile counts between co-resident CTAs
+// (see query_kernel) -> one contiguous, coalesced store of the survivors.  The
 // output is therefore IDENTICAL to the CPU FIFO order, not just the same set.
 //
-// Tile ids come from an atomic ticket (a CTA only obtains a tile once running,
-// so every predecessor it waits on is resident -> forward progress).  Status
-// words carry a 20-bit launch epoch, so the workspace never needs clearing;
-// the last CTA to finish resets the ticket/done counters for the next launch.
+// Status words carry a 20-bit launch epoch, so the workspace never needs
+// clearing between launches.
 #include <algorithm>
 #include <atomic>
 
@@ -73,9 +70,13 @@ __device__ __forceinline__ void q_load(const T* __restrict__ col, int64_t n, int
     }
 }
 
-// Persistent CTAs: each loops over tiles taken from the ticket counter.  The
-// next tile's loads are issued before the current tile's look-back, so HBM
-// stays busy while a CTA waits for its predecessors.
+// Persistent, co-resident CTAs (cooperative launch) in lock-step rounds: in
+// round r CTA c owns tile r*G + c.  Every CTA publishes its tile's survivor
+// count, prefetches its next tile, then reads the round's G counts at once
+// (one block-wide load) -> its exclusive offset inside the round and the
+// round total, which every CTA adds to a private running base.  There is no
+// ticket counter and no prefix chain: a round costs one all-gather of counts
+// through L2 while the next tile's loads are already in flight.
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kQBlock)
 query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __restrict__ out,
@@ -88,118 +89,98 @@ query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __rest
 
     __shared__ T s_stage[TILE];
     __shared__ uint64_t s_warp[NW];
-    __shared__ int64_t s_red[NW];
-    __shared__ int64_t s_tile, s_excl;
-    __shared__ int s_first;
+    __shared__ int64_t s_red[NW], s_tot[NW];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = (int64_t)atomicAdd(&ws->ticket, 1ull);
-    __syncthreads();
-    int64_t tile = s_tile;
+    const int64_t G = gridDim.x, c = blockIdx.x;
+    const int64_t rounds = (num_tiles + G - 1) / G;
+    int64_t base_off = 0;
     T v[K][VN];
-    if (tile < num_tiles) q_load<T, VEC, K, VN>(col, n, tile * TILE, tid, v);
+    if (c < num_tiles) q_load<T, VEC, K, VN>(col, n, c * TILE, tid, v);
 
-    while (tile < num_tiles) {
+    for (int64_t r = 0; r < rounds; ++r) {
+        const int64_t tile = r * G + c;
         const int64_t base = tile * TILE;
-        // ---- predicate (element e = base + k*kQBlock*VN + tid*VN + c)
-        uint32_t bits = 0;  // bit k*VN+c
+        uint32_t agg = 0;
+        if (tile < num_tiles) {  // CTA-uniform
+            uint32_t bits = 0;  // bit k*VN+c
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
+            for (int k = 0; k < K; ++k) {
+                const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
 #pragma unroll
-            for (int c = 0; c < VN; ++c)
-                bits |= (uint32_t)((e0 + c < n) && cmp_apply((double)v[k][c], op, thr)) << (k * VN + c);
+                for (int cc = 0; cc < VN; ++cc)
+                    bits |= (uint32_t)((e0 + cc < n) && cmp_apply((double)v[k][cc], op, thr)) << (k * VN + cc);
+            }
+            // packed block scan: 16-bit field k = this thread's count in chunk k
+            uint64_t mine = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                mine |= (uint64_t)__popc((bits >> (k * VN)) & ((1u << VN) - 1)) << (16 * k);
+            uint64_t incl = mine;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += o;
+            }
+            if (lane == 31) s_warp[warp] = incl;
+            __syncthreads();
+            uint64_t wpre = 0, total = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                uint64_t t = s_warp[w];
+                if (w < warp) wpre += t;
+                total += t;
+            }
+            const uint64_t excl = wpre + incl - mine;
+            // stage survivors in smem at their tile-local input-order rank
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                uint32_t rr = agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc)
+                    if (bits & (1u << (k * VN + cc))) s_stage[rr++] = v[k][cc];
+                agg += (uint32_t)((total >> (16 * k)) & 0xffff);
+            }
+            if (tid == 0) st_relaxed(&ws->status[tile], pack_status(epoch, kFlagAgg, agg));
         }
-        // ---- packed block scan: 16-bit field k = this thread's count in chunk k
-        uint64_t mine = 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-            mine |= (uint64_t)__popc((bits >> (k * VN)) & ((1u << VN) - 1)) << (16 * k);
-        uint64_t incl = mine;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += o;
+        // prefetch the next round's tile while this round's counts gather
+        if (tile + G < num_tiles) q_load<T, VEC, K, VN>(col, n, (tile + G) * TILE, tid, v);
+
+        // all-gather of the round's counts (thread q reads CTA q's word)
+        int64_t val = 0;
+        const int64_t q = r * G + tid;
+        if (tid < G && q < num_tiles) {
+            uint64_t w;
+            while (true) {
+                w = ld_relaxed(&ws->status[q]);
+                if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
+                __nanosleep(16);
+            }
+            val = (int64_t)(w & kValueMask);
         }
-        if (lane == 31) s_warp[warp] = incl;
-        if (tid == 0) s_first = kQBlock;
+        int64_t lower = tid < c ? val : 0;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            lower += __shfl_xor_sync(0xffffffffu, lower, d);
+            val += __shfl_xor_sync(0xffffffffu, val, d);
+        }
+        if (lane == 0) {
+            s_red[warp] = lower;
+            s_tot[warp] = val;
+        }
         __syncthreads();
-        uint64_t wpre = 0, total = 0;
+        int64_t my_off = base_off, round_total = 0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-            uint64_t t = s_warp[w];
-            if (w < warp) wpre += t;
-            total += t;
+            my_off += s_red[w];
+            round_total += s_tot[w];
         }
-        const uint64_t excl = wpre + incl - mine;
-        // ---- stage survivors in smem at their tile-local input-order rank
-        uint32_t agg = 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            uint32_t r = agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
-#pragma unroll
-            for (int c = 0; c < VN; ++c)
-                if (bits & (1u << (k * VN + c))) s_stage[r++] = v[k][c];
-            agg += (uint32_t)((total >> (16 * k)) & 0xffff);
-        }
-        if (tid == 0) {
-            st_relaxed(&ws->status[tile],
-                       pack_status(epoch, tile == 0 ? kFlagPrefix : kFlagAgg, agg));
-            s_tile = (int64_t)atomicAdd(&ws->ticket, 1ull);
-        }
-        __syncthreads();
-        const int64_t next = s_tile;
-        // ---- prefetch the next tile while this one resolves its offset
-        if (next < num_tiles) q_load<T, VEC, K, VN>(col, n, next * TILE, tid, v);
-
-        // ---- decoupled look-back, block-wide: a kQBlock-tile window per round
-        int64_t prefix = 0;
-        if (tile > 0) {
-            int64_t pred = tile - 1;
-            while (true) {
-                const int64_t idx = pred - tid;
-                uint64_t w = pack_status(epoch, kFlagPrefix, 0);  // before tile 0
-                if (idx >= 0) {
-                    while (true) {
-                        w = ld_relaxed(&ws->status[idx]);
-                        if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
-                        __nanosleep(20);
-                    }
-                }
-                if (((w >> kValueBits) & 3ull) == kFlagPrefix) atomicMin(&s_first, tid);
-                __syncthreads();
-                const int first = s_first;
-                int64_t val = tid <= first ? (int64_t)(w & kValueMask) : 0;
-#pragma unroll
-                for (int d = 16; d; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
-                if (lane == 0) s_red[warp] = val;
-                __syncthreads();
-#pragma unroll
-                for (int q = 0; q < NW; ++q) prefix += s_red[q];
-                if (first < kQBlock) break;
-                pred -= kQBlock;
-                __syncthreads();  // s_red reuse
-            }
-            if (tid == 0) st_relaxed(&ws->status[tile], pack_status(epoch, kFlagPrefix, prefix + agg));
-        }
-        if (tid == 0 && tile == num_tiles - 1) atomicAdd(count, (unsigned long long)(prefix + agg));
-
-        // ---- drain: contiguous, coalesced stores of the staged survivors
-        for (uint32_t r = tid; r < agg; r += kQBlock) out[prefix + r] = s_stage[r];
-        __syncthreads();  // s_stage / s_first / s_red reuse by the next tile
-        tile = next;
+        // drain: contiguous, coalesced stores of the staged survivors
+        for (uint32_t rr = tid; rr < agg; rr += kQBlock) out[my_off + rr] = s_stage[rr];
+        base_off += round_total;
+        __syncthreads();  // s_stage / s_red reuse
     }
-
-    // ---- last CTA out resets the counters for the next launch
-    if (tid == 0) {
-        __threadfence();
-        unsigned long long d = atomicAdd(&ws->done, 1ull);
-        if (d == (unsigned long long)gridDim.x - 1) {
-            ws->ticket = 0;
-            ws->done = 0;
-            __threadfence();
-        }
-    }
+    if (c == 0 && tid == 0) atomicAdd(count, (unsigned long long)base_off);
 }
 
 std::atomic<uint32_t> g_epoch{0};
@@ -240,8 +221,12 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
     static int occ[2][2] = {};  // [f64][vec] resident CTAs per SM
     int& o = occ[sizeof(T) == 8][vec];
     if (o == 0) SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kQBlock, 0));
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(o, 1) * num_sms()));
-    kern<<<(unsigned)grid, kQBlock, 0, s>>>(col, n, op, thr, out, C, W, tiles, epoch);
+    // every CTA must be resident (rounds wait on all of them): cooperative launch
+    int64_t grid = std::min<int64_t>({tiles, (int64_t)std::max(o, 1) * num_sms(), (int64_t)kQBlock});
+    grid = std::max<int64_t>(grid, 1);
+    void* args[] = {(void*)&col, (void*)&n, (void*)&op, (void*)&thr, (void*)&out, (void*)&C, (void*)&W,
+                    (void*)&tiles, (void*)&epoch};
+    SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(kQBlock), args, 0, s));
     SDFGB_LAUNCHED("query_kernel");
     return SDFGB_OK;
 }

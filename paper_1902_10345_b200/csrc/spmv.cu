@@ -58,15 +58,40 @@ spmv_warp_row_kernel(const I* __restrict__ rowptr, const I* __restrict__ col,
     }
 }
 
-__device__ __forceinline__ float ldg_na(const float* p) {
+// L2 policies: the 2 GB matrix streams through with evict_first so it cannot
+// push the 16 MB x vector out of L2; x gathers carry evict_last.  (Without the
+// split, a no_allocate x gather measured 11 GB of DRAM reads -- x fell out.)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float ldg_keep(const float* p, uint64_t pol) {
     float r;
-    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int4 ldg_stream_i4(const int32_t* p, uint64_t pol) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float4 ldg_stream_f4(const float* p, uint64_t pol) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
     return r;
 }
 
 // fp32/int32 path: half-warp per row, 4 consecutive nnz per lane through
-// 128-bit col/val loads (one LDG.128 pair covers 64 nnz per half-warp), x
-// gathered with L1::no_allocate so random lines do not churn L1.
+// 128-bit col/val loads (one LDG.128 pair covers 64 nnz per half-warp);
+// matrix streams evict_first, x gathers evict_last.
 __global__ void __launch_bounds__(kSpmvBlock)
 spmv_hw_vec4_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                     const float* __restrict__ val, const float* __restrict__ x, float* __restrict__ b,
@@ -75,14 +100,16 @@ spmv_hw_vec4_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restric
     const unsigned hmask = (lane < 16) ? 0x0000ffffu : 0xffff0000u;
     const int64_t hw = (((int64_t)blockIdx.x * kSpmvBlock + threadIdx.x) >> 4);
     const int64_t nhw = ((int64_t)gridDim.x * kSpmvBlock) >> 4;
+    const uint64_t pstream = policy_evict_first(), pkeep = policy_evict_last();
+    auto ldg_na = [&](const float* p) { return ldg_keep(p, pkeep); };
     for (int64_t r = hw; r < H; r += nhw) {
         const int64_t rb = rowptr[r], re = rowptr[r + 1];
         float s = 0.f;
         if ((rb & 3) == 0) {
             for (int64_t j = rb + 4 * hl; j < re; j += 64) {
                 if (j + 3 < re) {
-                    const int4 c = __ldg(reinterpret_cast<const int4*>(col + j));
-                    const float4 v = __ldg(reinterpret_cast<const float4*>(val + j));
+                    const int4 c = ldg_stream_i4(col + j, pstream);
+                    const float4 v = ldg_stream_f4(val + j, pstream);
                     const float x0 = ldg_na(x + c.x), x1 = ldg_na(x + c.y);
                     const float x2 = ldg_na(x + c.z), x3 = ldg_na(x + c.w);
                     s += v.x * x0;
