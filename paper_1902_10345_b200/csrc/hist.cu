@@ -36,62 +36,64 @@ constexpr int kMaxSmemBins = 12288;  // 48 KB of uint32 counters per replica set
 
 enum BinMode { kScaled = 0, kIdentity = 1, kPow2 = 2 };
 
-// bin of one element; false when out of [0, bins) (NaN included)
+// Bin of one element, clamped: an out-of-range element (NaN included) maps to
+// the extra "trash" counter at index `bins`, so the update needs no branch and
+// the trash counters are exactly the out-of-bounds count.
 template <typename T, int MODE>
-__device__ __forceinline__ bool bin_of(T v, double scale, double div, bool has_div, float scale_f,
-                                       int64_t bins, int& bin) {
+__device__ __forceinline__ uint32_t bin_clamped(T v, double scale, double div, bool has_div, float scale_f,
+                                                uint32_t bins) {
     if constexpr (MODE == kIdentity) {
-        int64_t k = (int64_t)v;
-        bin = (int)k;
-        return k >= 0 && k < bins;
+        const uint64_t k = (uint64_t)(int64_t)v;
+        return k < bins ? (uint32_t)k : bins;
     } else if constexpr (MODE == kPow2) {
         // fp32 input, scale = 2^k (k >= 0), div = 1: v * scale is exact, so the
         // floor can be taken in fp32 and equals the reference's floor in double.
         // fma_rd(v, scale, 2^23) = floor(v*scale) + 2^23 exactly for
         // 0 <= v*scale < 2^23, so its bit pattern minus 0x4B000000 is the bin;
-        // negative, >= 2^23, inf and NaN inputs all land outside [0, bins) as
-        // unsigned -- one FFMA + IADD + ISETP, nothing on the XU pipe.
+        // negative, >= 2^23, inf and NaN inputs all land above `bins` as
+        // unsigned.  SASS: FFMA.RM + VIADDMNMX.U32.
         const uint32_t b = (uint32_t)__float_as_int(__fmaf_rd((float)v, scale_f, 8388608.0f)) - 0x4B000000u;
-        bin = (int)b;
-        return b < (uint32_t)bins;
+        return min(b, bins);
     } else {
         double q = (double)v * scale;
         if (has_div) q = q / div;
         q = floor(q);
-        bin = (int)q;
-        return q >= 0.0 && q < (double)bins;  // NaN -> false
+        return (q >= 0.0 && q < (double)bins) ? (uint32_t)q : bins;  // NaN -> trash
     }
+}
+
+__device__ __forceinline__ void smem_inc(uint32_t addr) {
+    // unused-result shared add of 1: ptxas emits ATOMS.POPC.INC (warp-aggregated)
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
 }
 
 template <typename T, int MODE>
 __global__ void __cluster_dims__(kHistCluster, 1, 1) __launch_bounds__(kHistBlock)
 hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale, double div,
-                 int64_t bins, int reps, unsigned long long* __restrict__ hist,
+                 int64_t bins64, int reps, unsigned long long* __restrict__ hist,
                  unsigned long long* __restrict__ oob) {
     extern __shared__ uint32_t sh[];
     using V = typename Vec16<T>::type;
     constexpr int VN = Vec16<T>::n;
     const bool has_div = div != 1.0;
     const float scale_f = (float)scale;
+    const uint32_t bins = (uint32_t)bins64;
+    const uint32_t row = bins + 1;  // + trash counter
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
 
-    for (int64_t k = tid; k < (int64_t)reps * bins; k += blockDim.x) sh[k] = 0u;
+    for (uint32_t k = tid; k < (uint32_t)reps * row; k += blockDim.x) sh[k] = 0u;
     __syncthreads();
 
-    uint32_t* h = sh + (warp % reps) * bins;
-    uint32_t seen = 0;  // elements this thread binned or rejected (oob = seen - counted)
-    auto bump = [&](T v) {
-        int b;
-        if (bin_of<T, MODE>(v, scale, div, has_div, scale_f, bins, b)) atomicAdd(&h[b], 1u);
-    };
+    const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(sh) + (uint32_t)(warp % reps) * row * 4u;
+    auto bump = [&](T v) { smem_inc(hbase + 4u * bin_clamped<T, MODE>(v, scale, div, has_div, scale_f, bins)); };
 
     // misaligned head (< VN elements) and ragged tail: block 0, scalar
     const int64_t nvec = (n - head) / VN;
     const int64_t tail0 = head + nvec * VN;
     if (blockIdx.x == 0) {
-        for (int64_t p = tid; p < head; p += blockDim.x, ++seen) bump(in[p]);
-        for (int64_t p = tail0 + tid; p < n; p += blockDim.x, ++seen) bump(in[p]);
+        for (int64_t p = tid; p < head; p += blockDim.x) bump(in[p]);
+        for (int64_t p = tail0 + tid; p < n; p += blockDim.x) bump(in[p]);
     }
 
     const V* vin = reinterpret_cast<const V*>(in + head);
@@ -112,47 +114,33 @@ hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u)
             if (i + u * stride < nvec) {
-                seen += VN;
 #pragma unroll
                 for (int c = 0; c < VN; ++c) bump(vget<V, T>(cur[u], c));
             }
 #pragma unroll
         for (int u = 0; u < kHistUnroll; ++u) cur[u] = nxt[u];
     }
-
-    __shared__ unsigned long long s_seen, s_counted;
-    if (tid == 0) s_seen = s_counted = 0;
-#pragma unroll
-    for (int d = 16; d; d >>= 1) seen += __shfl_xor_sync(0xffffffffu, seen, d);
     __syncthreads();
-    if ((tid & 31) == 0) atomicAdd(&s_seen, (unsigned long long)seen);
-    // fold replicas into replica 0
-    uint32_t counted = 0;
-    for (int64_t k = tid; k < bins; k += blockDim.x) {
+    // fold replicas into replica 0 (trash included)
+    for (uint32_t k = tid; k < row; k += blockDim.x) {
         uint32_t s = 0;
-        for (int r = 0; r < reps; ++r) s += sh[r * bins + k];
+        for (int r = 0; r < reps; ++r) s += sh[r * row + k];
         sh[k] = s;
-        counted += s;
     }
-#pragma unroll
-    for (int d = 16; d; d >>= 1) counted += __shfl_xor_sync(0xffffffffu, counted, d);
-    if ((tid & 31) == 0) atomicAdd(&s_counted, (unsigned long long)counted);
-    __syncthreads();
-    if (tid == 0 && s_seen != s_counted) atomicAdd(oob, s_seen - s_counted);
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
     if (cluster.block_rank() != 0) {
         uint32_t* lead = cluster.map_shared_rank(sh, 0);
-        for (int64_t k = tid; k < bins; k += blockDim.x) {
-            uint32_t c = sh[k];
+        for (uint32_t k = tid; k < row; k += blockDim.x) {
+            const uint32_t c = sh[k];
             if (c) atomicAdd(&lead[k], c);
         }
     }
     cluster.sync();
     if (cluster.block_rank() == 0) {
-        for (int64_t k = tid; k < bins; k += blockDim.x) {
-            uint32_t c = sh[k];
-            if (c) atomicAdd(&hist[k], (unsigned long long)c);
+        for (uint32_t k = tid; k < row; k += blockDim.x) {
+            const uint32_t c = sh[k];
+            if (c) atomicAdd(k < bins ? &hist[k] : oob, (unsigned long long)c);
         }
     }
 }
@@ -165,11 +153,8 @@ hist_global_kernel(const T* __restrict__ in, int64_t n, double scale, double div
     const bool has_div = div != 1.0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
-        int b;
-        if (bin_of<T, MODE>(in[p], scale, div, has_div, (float)scale, bins, b))
-            atomicAdd(&hist[b], 1ull);
-        else
-            atomicAdd(oob, 1ull);
+        const uint32_t b = bin_clamped<T, MODE>(in[p], scale, div, has_div, (float)scale, (uint32_t)bins);
+        atomicAdd(b < bins ? &hist[b] : oob, 1ull);
     }
 }
 
@@ -183,15 +168,15 @@ int launch_hist(const T* img, int64_t n, double scale, double div, int64_t* hist
     cudaStream_t s = as_stream(stream);
     auto* H = reinterpret_cast<unsigned long long*>(hist);
     auto* O = reinterpret_cast<unsigned long long*>(oob);
-    if (bins > kMaxSmemBins) {
+    if (bins + 1 > kMaxSmemBins || bins >= (1ll << 31)) {
         int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
         hist_global_kernel<T, MODE><<<blocks, 256, 0, s>>>(img, n, scale, div, bins, H, O);
         SDFGB_LAUNCHED("hist_global_kernel");
         return SDFGB_OK;
     }
     constexpr int VN = Vec16<T>::n;
-    int reps = (int)std::max<int64_t>(1, std::min<int64_t>(8, kMaxSmemBins / bins));
-    size_t smem = (size_t)reps * bins * sizeof(uint32_t);
+    int reps = (int)std::max<int64_t>(1, std::min<int64_t>(8, kMaxSmemBins / (bins + 1)));
+    size_t smem = (size_t)reps * (bins + 1) * sizeof(uint32_t);
     auto kern = hist_smem_kernel<T, MODE>;
     if (smem > 48 * 1024)
         SDFGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

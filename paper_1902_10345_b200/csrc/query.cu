@@ -27,6 +27,7 @@ namespace {
 
 constexpr int kQBlock = 512;
 constexpr int kQVecPerThread = 4;
+constexpr int kQSubs = 2;  // sub-tiles per CTA segment per round
 
 constexpr uint64_t kFlagAgg = 1ull;
 constexpr uint64_t kFlagPrefix = 2ull;
@@ -52,15 +53,38 @@ __device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, u
     return ((uint64_t)epoch << 44) | (flag << kValueBits) | (value & kValueMask);
 }
 
+__device__ __forceinline__ uint64_t make_policy(bool keep) {
+    uint64_t p;
+    if (keep)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float4 ldg_pol(const float4* p, uint64_t pol) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double2 ldg_pol(const double2* p, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+
+// Load one sub-tile (element e = base + k*kQBlock*VN + tid*VN + c) and return
+// the predicate bits (bit k*VN + c).
 template <typename T, bool VEC, int K, int VN>
-__device__ __forceinline__ void q_load(const T* __restrict__ col, int64_t n, int64_t base, int tid,
-                                       T (&v)[K][VN]) {
+__device__ __forceinline__ uint32_t q_load_pred(const T* __restrict__ col, int64_t n, int64_t base, int tid,
+                                                int op, double thr, uint64_t pol, T (&v)[K][VN]) {
     using V = typename Vec16<T>::type;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
         if (VEC && e0 + VN <= n) {
-            V x = ldg_stream(reinterpret_cast<const V*>(col + e0));
+            V x = ldg_pol(reinterpret_cast<const V*>(col + e0), pol);
 #pragma unroll
             for (int c = 0; c < VN; ++c) v[k][c] = vget<V, T>(x, c);
         } else {
@@ -68,91 +92,78 @@ __device__ __forceinline__ void q_load(const T* __restrict__ col, int64_t n, int
             for (int c = 0; c < VN; ++c) v[k][c] = (e0 + c < n) ? col[e0 + c] : T(0);
         }
     }
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
+#pragma unroll
+        for (int c = 0; c < VN; ++c)
+            bits |= (uint32_t)((e0 + c < n) && cmp_apply((double)v[k][c], op, thr)) << (k * VN + c);
+    }
+    return bits;
 }
 
-// Persistent, co-resident CTAs (cooperative launch) in lock-step rounds: in
-// round r CTA c owns tile r*G + c.  Every CTA publishes its tile's survivor
-// count, prefetches its next tile, then reads the round's G counts at once
-// (one block-wide load) -> its exclusive offset inside the round and the
-// round total, which every CTA adds to a private running base.  There is no
-// ticket counter and no prefix chain: a round costs one all-gather of counts
-// through L2 while the next tile's loads are already in flight.
+// Persistent, co-resident CTAs (cooperative launch) working in rounds over
+// L2-sized chunks.  Round r gives CTA c the contiguous segment
+// [r*G*S + c*S, +S) (S = kQSubs sub-tiles):
+//   count(r)  stream the segment from HBM (L2 evict_last), publish its
+//             survivor count in status[r*G + c];
+//   gather(r) one block-wide read of the round's G counts -> this CTA's
+//             offset inside the round and the round total;
+//   write(r)  re-read the segment (L2 hits, evict_first), block-scan each
+//             sub-tile, stage survivors in smem, store them contiguously.
+// count(r+1) runs before gather(r), so the counts of round r have a whole
+// segment's worth of HBM time to become visible: the only inter-CTA
+// synchronisation is one count all-gather per round, off the critical path.
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kQBlock)
 query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __restrict__ out,
              unsigned long long* __restrict__ count, QueryWs* __restrict__ ws,
-             int64_t num_tiles, uint32_t epoch) {
+             int64_t rounds, uint32_t epoch) {
     constexpr int VN = Vec16<T>::n;
     constexpr int K = kQVecPerThread;
-    constexpr int TILE = kQBlock * K * VN;
+    constexpr int SUB = kQBlock * K * VN;
+    constexpr int64_t S = (int64_t)SUB * kQSubs;
     constexpr int NW = kQBlock / 32;
 
-    __shared__ T s_stage[TILE];
+    __shared__ T s_stage[SUB];
     __shared__ uint64_t s_warp[NW];
     __shared__ int64_t s_red[NW], s_tot[NW];
+    __shared__ uint32_t s_cnt[NW];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
-    const int64_t rounds = (num_tiles + G - 1) / G;
-    int64_t base_off = 0;
+    const uint64_t keep = make_policy(true), drop = make_policy(false);
     T v[K][VN];
-    if (c < num_tiles) q_load<T, VEC, K, VN>(col, n, c * TILE, tid, v);
 
-    for (int64_t r = 0; r < rounds; ++r) {
-        const int64_t tile = r * G + c;
-        const int64_t base = tile * TILE;
-        uint32_t agg = 0;
-        if (tile < num_tiles) {  // CTA-uniform
-            uint32_t bits = 0;  // bit k*VN+c
+    auto count_round = [&](int64_t r) {
+        const int64_t seg = (r * G + c) * S;
+        uint32_t cnt = 0;
+#pragma unroll 1
+        for (int j = 0; j < kQSubs; ++j)
+            cnt += __popc(q_load_pred<T, VEC, K, VN>(col, n, seg + (int64_t)j * SUB, tid, op, thr, keep, v));
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
+        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+        if (lane == 0) s_cnt[warp] = cnt;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
 #pragma unroll
-                for (int cc = 0; cc < VN; ++cc)
-                    bits |= (uint32_t)((e0 + cc < n) && cmp_apply((double)v[k][cc], op, thr)) << (k * VN + cc);
-            }
-            // packed block scan: 16-bit field k = this thread's count in chunk k
-            uint64_t mine = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-                mine |= (uint64_t)__popc((bits >> (k * VN)) & ((1u << VN) - 1)) << (16 * k);
-            uint64_t incl = mine;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += o;
-            }
-            if (lane == 31) s_warp[warp] = incl;
-            __syncthreads();
-            uint64_t wpre = 0, total = 0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                uint64_t t = s_warp[w];
-                if (w < warp) wpre += t;
-                total += t;
-            }
-            const uint64_t excl = wpre + incl - mine;
-            // stage survivors in smem at their tile-local input-order rank
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                uint32_t rr = agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
-#pragma unroll
-                for (int cc = 0; cc < VN; ++cc)
-                    if (bits & (1u << (k * VN + cc))) s_stage[rr++] = v[k][cc];
-                agg += (uint32_t)((total >> (16 * k)) & 0xffff);
-            }
-            if (tid == 0) st_relaxed(&ws->status[tile], pack_status(epoch, kFlagAgg, agg));
+            for (int w = 0; w < NW; ++w) t += s_cnt[w];
+            st_relaxed(&ws->status[r * G + c], pack_status(epoch, kFlagAgg, t));
         }
-        // prefetch the next round's tile while this round's counts gather
-        if (tile + G < num_tiles) q_load<T, VEC, K, VN>(col, n, (tile + G) * TILE, tid, v);
+    };
 
-        // all-gather of the round's counts (thread q reads CTA q's word)
+    count_round(0);
+    int64_t base_off = 0;
+    for (int64_t r = 0; r < rounds; ++r) {
+        if (r + 1 < rounds) count_round(r + 1);
+        // ---- all-gather of round r's counts (thread q reads CTA q's word)
         int64_t val = 0;
-        const int64_t q = r * G + tid;
-        if (tid < G && q < num_tiles) {
+        if (tid < G) {
             uint64_t w;
             while (true) {
-                w = ld_relaxed(&ws->status[q]);
+                w = ld_relaxed(&ws->status[r * G + tid]);
                 if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
                 __nanosleep(16);
             }
@@ -169,16 +180,53 @@ query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __rest
             s_tot[warp] = val;
         }
         __syncthreads();
-        int64_t my_off = base_off, round_total = 0;
+        int64_t off = base_off, round_total = 0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-            my_off += s_red[w];
+            off += s_red[w];
             round_total += s_tot[w];
         }
-        // drain: contiguous, coalesced stores of the staged survivors
-        for (uint32_t rr = tid; rr < agg; rr += kQBlock) out[my_off + rr] = s_stage[rr];
+        // ---- write(r): re-read from L2, scan, stage, store contiguously
+        const int64_t seg = (r * G + c) * S;
+#pragma unroll 1
+        for (int j = 0; j < kQSubs; ++j) {
+            const uint32_t bits = q_load_pred<T, VEC, K, VN>(col, n, seg + (int64_t)j * SUB, tid, op, thr, drop, v);
+            uint64_t mine = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                mine |= (uint64_t)__popc((bits >> (k * VN)) & ((1u << VN) - 1)) << (16 * k);
+            uint64_t incl = mine;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += o;
+            }
+            __syncthreads();  // previous sub-tile's drain / s_red reads are done
+            if (lane == 31) s_warp[warp] = incl;
+            __syncthreads();
+            uint64_t wpre = 0, total = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                uint64_t t = s_warp[w];
+                if (w < warp) wpre += t;
+                total += t;
+            }
+            const uint64_t excl = wpre + incl - mine;
+            uint32_t agg = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                uint32_t rr = agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc)
+                    if (bits & (1u << (k * VN + cc))) s_stage[rr++] = v[k][cc];
+                agg += (uint32_t)((total >> (16 * k)) & 0xffff);
+            }
+            __syncthreads();
+            for (uint32_t rr = tid; rr < agg; rr += kQBlock) out[off + rr] = s_stage[rr];
+            off += agg;
+        }
         base_off += round_total;
-        __syncthreads();  // s_stage / s_red reuse
+        __syncthreads();
     }
     if (c == 0 && tid == 0) atomicAdd(count, (unsigned long long)base_off);
 }
@@ -194,9 +242,17 @@ uint32_t next_epoch() {
 }
 
 template <typename T>
-int64_t tiles_for(int64_t n) {
-    const int64_t tile = (int64_t)kQBlock * kQVecPerThread * Vec16<T>::n;
-    return (n + tile - 1) / tile;
+constexpr int64_t seg_elems() {
+    return (int64_t)kQBlock * kQVecPerThread * Vec16<T>::n * kQSubs;
+}
+
+// rounds and CTAs for n elements: G co-resident CTAs (<= kQBlock so one
+// block-wide read gathers a round), rounds = ceil(n / (G * S))
+template <typename T>
+void query_geometry(int64_t n, int64_t capacity, int64_t& G, int64_t& rounds) {
+    const int64_t segs = (n + seg_elems<T>() - 1) / seg_elems<T>();
+    G = std::max<int64_t>(1, std::min<int64_t>({segs, capacity, (int64_t)kQBlock}));
+    rounds = (segs + G - 1) / G;
 }
 
 template <typename T>
@@ -206,7 +262,6 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
         return set_error(SDFGB_ERR_INVALID, "query: bad arguments");
     if (n == 0) return SDFGB_OK;
     if ((uint64_t)n > kValueMask) return set_error(SDFGB_ERR_INVALID, "query: n too large");
-    const int64_t tiles = tiles_for<T>(n);
     if (ws_bytes < sdfgb_query_workspace_bytes(n, sizeof(T)))
         return set_error(SDFGB_ERR_WORKSPACE, "query: workspace %zu < %zu bytes", ws_bytes,
                          sdfgb_query_workspace_bytes(n, sizeof(T)));
@@ -221,13 +276,12 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
     static int occ[2][2] = {};  // [f64][vec] resident CTAs per SM
     int& o = occ[sizeof(T) == 8][vec];
     if (o == 0) SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kQBlock, 0));
+    int64_t G, rounds;
+    query_geometry<T>(n, (int64_t)std::max(o, 1) * num_sms(), G, rounds);
     // every CTA must be resident (rounds wait on all of them): cooperative launch
-    int64_t grid = std::min<int64_t>({tiles, (int64_t)std::max(o, 1) * num_sms(), (int64_t)kQBlock});
-    grid = std::max<int64_t>(grid, 1);
     void* args[] = {(void*)&col, (void*)&n, (void*)&op, (void*)&thr, (void*)&out, (void*)&C, (void*)&W,
-                    (void*)&tiles, (void*)&epoch};
-    SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(kQBlock), args, 0, s));
-    SDFGB_LAUNCHED("query_kernel");
+                    (void*)&rounds, (void*)&epoch};
+    SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)G), dim3(kQBlock), args, 0, s));
     return SDFGB_OK;
 }
 
@@ -235,8 +289,10 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
 }  // namespace sdfgb
 
 extern "C" size_t sdfgb_query_workspace_bytes(int64_t n, int elem_bytes) {
-    int64_t tiles = elem_bytes == 8 ? sdfgb::tiles_for<double>(n) : sdfgb::tiles_for<float>(n);
-    return offsetof(sdfgb::QueryWs, status) + (size_t)std::max<int64_t>(tiles, 1) * 8;
+    // one status word per (round, CTA) slot; rounds * G <= segments + G - 1 < 2 * segments + kQBlock
+    const int64_t seg = elem_bytes == 8 ? sdfgb::seg_elems<double>() : sdfgb::seg_elems<float>();
+    const int64_t segs = (n + seg - 1) / seg;
+    return offsetof(sdfgb::QueryWs, status) + (size_t)(segs + sdfgb::kQBlock) * 8;
 }
 extern "C" int sdfgb_query_f32(const float* col, int64_t n, int op, double thr, float* out_vals,
                                int64_t* count, void* ws, size_t ws_bytes, void* stream) {

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_workspace_queries_need_no_gpu():
     L = _lib.load()
-    assert L.sdfgb_query_workspace_bytes(1 << 26, 4) >= (1 << 26) // 8192 * 8
+    assert L.sdfgb_query_workspace_bytes(1 << 26, 4) >= (1 << 26) // 16384 * 8
     assert L.sdfgb_gemm_workspace_bytes(128, 256, 64) == 2 * 128 * 64 * 4 + 2 * 256 * 64 * 4
 
 
