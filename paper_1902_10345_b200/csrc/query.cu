@@ -19,6 +19,7 @@
 // clearing between launches.
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 
 #include "common.cuh"
 
@@ -74,11 +75,24 @@ __device__ __forceinline__ double2 ldg_pol(const double2* p, uint64_t pol) {
     return r;
 }
 
+// predicate in the element type; OP 6/7 = constant false/true (see fold_threshold)
+template <int OP, typename T>
+__device__ __forceinline__ bool pred(T v, T t) {
+    if constexpr (OP == SDFGB_CMP_LT) return v < t;
+    else if constexpr (OP == SDFGB_CMP_LE) return v <= t;
+    else if constexpr (OP == SDFGB_CMP_GT) return v > t;
+    else if constexpr (OP == SDFGB_CMP_GE) return v >= t;
+    else if constexpr (OP == SDFGB_CMP_EQ) return v == t;
+    else if constexpr (OP == SDFGB_CMP_NE) return v != t;
+    else if constexpr (OP == 6) return false;
+    else return true;
+}
+
 // Load one sub-tile (element e = base + k*kQBlock*VN + tid*VN + c) and return
 // the predicate bits (bit k*VN + c).
-template <typename T, bool VEC, int K, int VN>
+template <typename T, bool VEC, int OP, int K, int VN>
 __device__ __forceinline__ uint32_t q_load_pred(const T* __restrict__ col, int64_t n, int64_t base, int tid,
-                                                int op, double thr, uint64_t pol, T (&v)[K][VN]) {
+                                                T thr, uint64_t pol, T (&v)[K][VN]) {
     using V = typename Vec16<T>::type;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -98,7 +112,7 @@ __device__ __forceinline__ uint32_t q_load_pred(const T* __restrict__ col, int64
         const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
 #pragma unroll
         for (int c = 0; c < VN; ++c)
-            bits |= (uint32_t)((e0 + c < n) && cmp_apply((double)v[k][c], op, thr)) << (k * VN + c);
+            bits |= (uint32_t)((e0 + c < n) && pred<OP>(v[k][c], thr)) << (k * VN + c);
     }
     return bits;
 }
@@ -115,9 +129,9 @@ __device__ __forceinline__ uint32_t q_load_pred(const T* __restrict__ col, int64
 // count(r+1) runs before gather(r), so the counts of round r have a whole
 // segment's worth of HBM time to become visible: the only inter-CTA
 // synchronisation is one count all-gather per round, off the critical path.
-template <typename T, bool VEC>
-__global__ void __launch_bounds__(kQBlock)
-query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __restrict__ out,
+template <typename T, bool VEC, int OP>
+__global__ void __launch_bounds__(kQBlock, 2)
+query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
              unsigned long long* __restrict__ count, QueryWs* __restrict__ ws,
              int64_t rounds, uint32_t epoch) {
     constexpr int VN = Vec16<T>::n;
@@ -141,7 +155,7 @@ query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __rest
         uint32_t cnt = 0;
 #pragma unroll 1
         for (int j = 0; j < kQSubs; ++j)
-            cnt += __popc(q_load_pred<T, VEC, K, VN>(col, n, seg + (int64_t)j * SUB, tid, op, thr, keep, v));
+            cnt += __popc(q_load_pred<T, VEC, OP, K, VN>(col, n, seg + (int64_t)j * SUB, tid, thr, keep, v));
 #pragma unroll
         for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
         if (lane == 0) s_cnt[warp] = cnt;
@@ -190,7 +204,7 @@ query_kernel(const T* __restrict__ col, int64_t n, int op, double thr, T* __rest
         const int64_t seg = (r * G + c) * S;
 #pragma unroll 1
         for (int j = 0; j < kQSubs; ++j) {
-            const uint32_t bits = q_load_pred<T, VEC, K, VN>(col, n, seg + (int64_t)j * SUB, tid, op, thr, drop, v);
+            const uint32_t bits = q_load_pred<T, VEC, OP, K, VN>(col, n, seg + (int64_t)j * SUB, tid, thr, drop, v);
             uint64_t mine = 0;
 #pragma unroll
             for (int k = 0; k < K; ++k)
@@ -255,6 +269,45 @@ void query_geometry(int64_t n, int64_t capacity, int64_t& G, int64_t& rounds) {
     rounds = (segs + G - 1) / G;
 }
 
+// Exact predicate in the element type: for a float v and a double t,
+//   v <  t  <=>  v <  up(t)      v <= t  <=>  v <= down(t)
+//   v >  t  <=>  v >  down(t)    v >= t  <=>  v >= up(t)
+//   v == t  <=>  t representable && v == (float)t   (else constant false)
+// with up/down = t rounded toward +/-inf; NaN thresholds stay NaN.  So the
+// kernel runs one FSETP per element instead of widening to double.
+template <typename T>
+void fold_threshold(int op, double thr, int& op_out, T& t_out) {
+    op_out = op;
+    t_out = (T)thr;
+    if constexpr (sizeof(T) == 4) {
+        if (thr != thr) return;
+        const float f = (float)thr;
+        const float up = (double)f < thr ? std::nextafter(f, INFINITY) : f;
+        const float dn = (double)f > thr ? std::nextafter(f, -INFINITY) : f;
+        const bool exact = (double)f == thr;
+        switch (op) {
+        case SDFGB_CMP_LT: case SDFGB_CMP_GE: t_out = up; break;
+        case SDFGB_CMP_LE: case SDFGB_CMP_GT: t_out = dn; break;
+        case SDFGB_CMP_EQ: if (!exact) op_out = 6; break;
+        default: if (!exact) op_out = 7; break;
+        }
+    }
+}
+
+template <typename T, bool VEC>
+auto query_kernel_for(int op) {
+    switch (op) {
+    case 0: return query_kernel<T, VEC, 0>;
+    case 1: return query_kernel<T, VEC, 1>;
+    case 2: return query_kernel<T, VEC, 2>;
+    case 3: return query_kernel<T, VEC, 3>;
+    case 4: return query_kernel<T, VEC, 4>;
+    case 5: return query_kernel<T, VEC, 5>;
+    case 6: return query_kernel<T, VEC, 6>;
+    default: return query_kernel<T, VEC, 7>;
+    }
+}
+
 template <typename T>
 int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* count, void* ws,
                  size_t ws_bytes, void* stream) {
@@ -272,14 +325,17 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
     auto* C = reinterpret_cast<unsigned long long*>(count);
     const uint32_t epoch = next_epoch();
     cudaStream_t s = as_stream(stream);
-    auto kern = vec ? query_kernel<T, true> : query_kernel<T, false>;
-    static int occ[2][2] = {};  // [f64][vec] resident CTAs per SM
-    int& o = occ[sizeof(T) == 8][vec];
+    int kop;
+    T tt;
+    fold_threshold<T>(op, thr, kop, tt);
+    auto kern = vec ? query_kernel_for<T, true>(kop) : query_kernel_for<T, false>(kop);
+    static int occ[2][2][8] = {};  // [f64][vec][op] resident CTAs per SM
+    int& o = occ[sizeof(T) == 8][vec][kop];
     if (o == 0) SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kQBlock, 0));
     int64_t G, rounds;
     query_geometry<T>(n, (int64_t)std::max(o, 1) * num_sms(), G, rounds);
     // every CTA must be resident (rounds wait on all of them): cooperative launch
-    void* args[] = {(void*)&col, (void*)&n, (void*)&op, (void*)&thr, (void*)&out, (void*)&C, (void*)&W,
+    void* args[] = {(void*)&col, (void*)&n, (void*)&tt, (void*)&out, (void*)&C, (void*)&W,
                     (void*)&rounds, (void*)&epoch};
     SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)G), dim3(kQBlock), args, 0, s));
     return SDFGB_OK;
