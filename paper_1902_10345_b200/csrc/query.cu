@@ -88,31 +88,36 @@ __device__ __forceinline__ bool pred(T v, T t) {
     else return true;
 }
 
-// Load one sub-tile (element e = base + k*kQBlock*VN + tid*VN + c) and return
-// the predicate bits (bit k*VN + c).
-template <typename T, bool VEC, int OP, int K, int VN>
-__device__ __forceinline__ uint32_t q_load_pred(const T* __restrict__ col, int64_t n, int64_t base, int tid,
-                                                T thr, uint64_t pol, T (&v)[K][VN]) {
+// Load one sub-tile: element e = base + k*kQBlock*VN + tid*VN + c.  FULL
+// (CTA-uniform: the whole sub-tile lies inside [0, n)) drops every bounds test.
+template <typename T, bool VEC, bool FULL, int K, int VN>
+__device__ __forceinline__ void q_load(const T* __restrict__ col, int64_t n, int64_t base, int tid,
+                                       uint64_t pol, T (&v)[K][VN]) {
     using V = typename Vec16<T>::type;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
-        if (VEC && e0 + VN <= n) {
+        if (VEC && (FULL || e0 + VN <= n)) {
             V x = ldg_pol(reinterpret_cast<const V*>(col + e0), pol);
 #pragma unroll
             for (int c = 0; c < VN; ++c) v[k][c] = vget<V, T>(x, c);
         } else {
 #pragma unroll
-            for (int c = 0; c < VN; ++c) v[k][c] = (e0 + c < n) ? col[e0 + c] : T(0);
+            for (int c = 0; c < VN; ++c) v[k][c] = (FULL || e0 + c < n) ? col[e0 + c] : T(0);
         }
     }
+}
+
+// predicate bits, bit k*VN + c
+template <typename T, bool FULL, int OP, int K, int VN>
+__device__ __forceinline__ uint32_t q_bits(const T (&v)[K][VN], int64_t n, int64_t base, int tid, T thr) {
     uint32_t bits = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int64_t e0 = base + (int64_t)k * kQBlock * VN + (int64_t)tid * VN;
 #pragma unroll
         for (int c = 0; c < VN; ++c)
-            bits |= (uint32_t)((e0 + c < n) && pred<OP>(v[k][c], thr)) << (k * VN + c);
+            if ((FULL || e0 + c < n) && pred<OP>(v[k][c], thr)) bits |= 1u << (k * VN + c);
     }
     return bits;
 }
@@ -140,7 +145,7 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
     constexpr int64_t S = (int64_t)SUB * kQSubs;
     constexpr int NW = kQBlock / 32;
 
-    __shared__ T s_stage[SUB];
+    __shared__ __align__(16) T s_stage[SUB + 4];
     __shared__ uint64_t s_warp[NW];
     __shared__ int64_t s_red[NW], s_tot[NW];
     __shared__ uint32_t s_cnt[NW];
@@ -154,8 +159,19 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
         const int64_t seg = (r * G + c) * S;
         uint32_t cnt = 0;
 #pragma unroll 1
-        for (int j = 0; j < kQSubs; ++j)
-            cnt += __popc(q_load_pred<T, VEC, OP, K, VN>(col, n, seg + (int64_t)j * SUB, tid, thr, keep, v));
+        for (int j = 0; j < kQSubs; ++j) {
+            const int64_t base = seg + (int64_t)j * SUB;
+            if (base + SUB <= n) {
+                q_load<T, VEC, true, K, VN>(col, n, base, tid, keep, v);
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+#pragma unroll
+                    for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(v[k][cc], thr) ? 1u : 0u;
+            } else if (base < n) {
+                q_load<T, VEC, false, K, VN>(col, n, base, tid, keep, v);
+                cnt += __popc(q_bits<T, false, OP, K, VN>(v, n, base, tid, thr));
+            }
+        }
 #pragma unroll
         for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
         if (lane == 0) s_cnt[warp] = cnt;
@@ -204,7 +220,16 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
         const int64_t seg = (r * G + c) * S;
 #pragma unroll 1
         for (int j = 0; j < kQSubs; ++j) {
-            const uint32_t bits = q_load_pred<T, VEC, OP, K, VN>(col, n, seg + (int64_t)j * SUB, tid, thr, drop, v);
+            const int64_t base = seg + (int64_t)j * SUB;
+            if (base >= n) break;  // CTA-uniform
+            uint32_t bits;
+            if (base + SUB <= n) {
+                q_load<T, VEC, true, K, VN>(col, n, base, tid, drop, v);
+                bits = q_bits<T, true, OP, K, VN>(v, n, base, tid, thr);
+            } else {
+                q_load<T, VEC, false, K, VN>(col, n, base, tid, drop, v);
+                bits = q_bits<T, false, OP, K, VN>(v, n, base, tid, thr);
+            }
             uint64_t mine = 0;
 #pragma unroll
             for (int k = 0; k < K; ++k)
@@ -226,17 +251,35 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
                 total += t;
             }
             const uint64_t excl = wpre + incl - mine;
+            // stage at (off mod VEC16) + rank so smem and global indices are
+            // congruent mod 16 B and the drain can move 128-bit vectors
+            const uint32_t sh0 = (uint32_t)(off & (VN - 1));
             uint32_t agg = 0;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                uint32_t rr = agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
+                uint32_t rr = sh0 + agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
 #pragma unroll
-                for (int cc = 0; cc < VN; ++cc)
-                    if (bits & (1u << (k * VN + cc))) s_stage[rr++] = v[k][cc];
+                for (int cc = 0; cc < VN; ++cc) {
+                    const bool p = bits & (1u << (k * VN + cc));
+                    if (p) s_stage[rr] = v[k][cc];
+                    rr += p;
+                }
                 agg += (uint32_t)((total >> (16 * k)) & 0xffff);
             }
             __syncthreads();
-            for (uint32_t rr = tid; rr < agg; rr += kQBlock) out[off + rr] = s_stage[rr];
+            // drain: scalar head up to a 16 B boundary, 128-bit body, scalar tail
+            using V = typename Vec16<T>::type;
+            const uint32_t head = std::min<uint32_t>(agg, (VN - sh0) & (VN - 1));
+            if (tid < head) out[off + tid] = s_stage[sh0 + tid];
+            const uint32_t nv = (agg - head) / VN;
+            const V* sv = reinterpret_cast<const V*>(s_stage + sh0 + head);
+            V* gv = reinterpret_cast<V*>(out + off + head);
+            if (VEC && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+                for (uint32_t q = tid; q < nv; q += kQBlock) gv[q] = sv[q];
+                for (uint32_t rr = head + nv * VN + tid; rr < agg; rr += kQBlock) out[off + rr] = s_stage[sh0 + rr];
+            } else {
+                for (uint32_t rr = head + tid; rr < agg; rr += kQBlock) out[off + rr] = s_stage[sh0 + rr];
+            }
             off += agg;
         }
         base_off += round_total;
