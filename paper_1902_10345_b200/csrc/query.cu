@@ -243,13 +243,16 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
             __syncthreads();  // previous sub-tile's drain / s_red reads are done
             if (lane == 31) s_warp[warp] = incl;
             __syncthreads();
-            uint64_t wpre = 0, total = 0;
+            // warp-level scan of the NW warp totals (every warp redundantly)
+            uint64_t ws_ = lane < NW ? s_warp[lane] : 0;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                uint64_t t = s_warp[w];
-                if (w < warp) wpre += t;
-                total += t;
+            for (int d = 1; d < NW; d <<= 1) {
+                uint64_t o = __shfl_up_sync(0xffffffffu, ws_, d);
+                if (lane >= d) ws_ += o;
             }
+            const uint64_t wprev = __shfl_sync(0xffffffffu, ws_, (warp + 31) & 31);
+            const uint64_t wpre = warp ? wprev : 0;
+            const uint64_t total = __shfl_sync(0xffffffffu, ws_, NW - 1);
             const uint64_t excl = wpre + incl - mine;
             // stage at (off mod VEC16) + rank so smem and global indices are
             // congruent mod 16 B and the drain can move 128-bit vectors
