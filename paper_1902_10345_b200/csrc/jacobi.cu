@@ -21,7 +21,7 @@
 //     order of up to 9 neighbours runs the same kernel through a select chain.
 #include <algorithm>
 
-#include "common.cuh"
+#include "tma.cuh"
 
 namespace sdfgb {
 namespace {
@@ -216,6 +216,146 @@ int launch_step(const T* src, T* dst, int64_t N, int64_t rows, int64_t g0, int64
     return SDFGB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Temporal blocking (canonical 5-point order, fp32): one launch advances KT
+// time steps.  A CTA TMA-loads its output tile plus a halo (8 columns, KT
+// rows each side) into shared memory, ping-pongs KT steps between two smem
+// buffers, and writes only the tile's centre -- the points whose KT-step
+// dependency cone lies inside the loaded region.  Per KT steps HBM sees one
+// read of ~1.2 planes and one write instead of KT reads + KT writes, and
+// every point is still computed as coef * ((((c + n) + s) + w) + e) in fp32,
+// so results stay bit-identical to the one-step kernel.  Points on the global
+// border are re-copied every step (never written), points outside the array
+// only feed border points.
+constexpr int kTbX = 128, kTbY = 64, kTbPad = 8, kTbMaxK = 7, kTbThreads = 256;
+constexpr int kTbRX = kTbX + 2 * kTbPad;  // 144 floats = 576 B rows
+
+__host__ __device__ constexpr int tb_rows(int k) { return kTbY + 2 * k; }
+__host__ __device__ constexpr size_t tb_smem(int k) { return (size_t)2 * kTbRX * tb_rows(k) * 4 + 128 + 64; }
+
+template <int KT>
+__global__ void __launch_bounds__(kTbThreads, 2)
+jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, float* __restrict__ dst, int N, float coef, int steps) {
+    constexpr int RY = tb_rows(KT);
+    constexpr int G4 = kTbRX / 4;  // 4-float column groups per row
+    extern __shared__ uint8_t smem_raw[];
+    float* buf0 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    float* buf1 = buf0 + kTbRX * RY;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(buf1 + kTbRX * RY);
+
+    const int x0 = blockIdx.x * kTbX, y0 = blockIdx.y * kTbY;
+    const int gx0 = x0 - kTbPad, gy0 = y0 - KT;  // region origin (may be negative: TMA zero-fills)
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, (uint32_t)(kTbRX * RY * 4));
+        tma_load_2d(buf0, &src, bar, gx0, gy0);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+
+    for (int st = 0; st < steps; ++st) {
+        const float* in = (st & 1) ? buf1 : buf0;
+        float* out = (st & 1) ? buf0 : buf1;
+        for (int it = threadIdx.x; it < (RY - 2) * G4; it += kTbThreads) {
+            const int r = 1 + it / G4, g = it % G4;
+            const float* rc = in + r * kTbRX + 4 * g;
+            const float4 c4 = *reinterpret_cast<const float4*>(rc);
+            const float4 n4 = *reinterpret_cast<const float4*>(rc - kTbRX);
+            const float4 s4 = *reinterpret_cast<const float4*>(rc + kTbRX);
+            const float lft = g > 0 ? rc[-1] : 0.f;
+            const float rgt = g < G4 - 1 ? rc[4] : 0.f;
+            const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+            const float nn[4] = {n4.x, n4.y, n4.z, n4.w};
+            const float ss[4] = {s4.x, s4.y, s4.z, s4.w};
+            const float ww[4] = {lft, c4.x, c4.y, c4.z};
+            const float ee[4] = {c4.y, c4.z, c4.w, rgt};
+            const int gy = gy0 + r;
+            const int gxb = gx0 + 4 * g;
+            const bool rowb = gy <= 0 || gy >= N - 1;
+            float o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float acc = __fadd_rn(cc[j], nn[j]);
+                acc = __fadd_rn(acc, ss[j]);
+                acc = __fadd_rn(acc, ww[j]);
+                acc = __fadd_rn(acc, ee[j]);
+                const int gx = gxb + j;
+                o[j] = (rowb || gx <= 0 || gx >= N - 1) ? cc[j] : __fmul_rn(coef, acc);
+            }
+            *reinterpret_cast<float4*>(out + r * kTbRX + 4 * g) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        __syncthreads();
+    }
+    // write the tile centre (global interior only)
+    const float* fin = (steps & 1) ? buf1 : buf0;
+    constexpr int CG = kTbX / 4;
+    for (int it = threadIdx.x; it < kTbY * CG; it += kTbThreads) {
+        const int r = it / CG, g = it % CG;
+        const int gy = y0 + r, gx = x0 + 4 * g;
+        if (gy < 1 || gy > N - 2) continue;
+        const float4 v = *reinterpret_cast<const float4*>(fin + (KT + r) * kTbRX + kTbPad + 4 * g);
+        float* d = dst + (int64_t)gy * N + gx;
+        if (gx >= 1 && gx + 3 <= N - 2) {
+            *reinterpret_cast<float4*>(d) = v;
+        } else {
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (gx + j >= 1 && gx + j <= N - 2) d[j] = vv[j];
+        }
+    }
+}
+
+template <int KT>
+int launch_tb(const CUtensorMap& map, float* dst, int64_t N, float coef, int steps, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        SDFGB_CUDA(cudaFuncSetAttribute(jacobi_tb_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)tb_smem(KT)));
+        attr = true;
+    }
+    dim3 grid((unsigned)((N + kTbX - 1) / kTbX), (unsigned)((N + kTbY - 1) / kTbY));
+    jacobi_tb_kernel<KT><<<grid, kTbThreads, tb_smem(KT), s>>>(map, dst, (int)N, coef, steps);
+    SDFGB_LAUNCHED("jacobi_tb_kernel");
+    return SDFGB_OK;
+}
+
+// T steps on A[2, N, N] in fp32 with temporal blocking.  Launches advance an
+// odd number of steps each (so state s stays in plane s % 2, as in the
+// reference), and the last step is a one-step launch so the other plane ends
+// holding state T-1 exactly like A[(T+1) % 2] of the reference.
+int jacobi_f32_blocked(float* A, int64_t N, int64_t T_, float coef, const Terms& terms, cudaStream_t s) {
+    float* P[2] = {A, A + N * N};
+    CUtensorMap maps[2];
+    SDFGB_TRY(encode_tiled_2d(&maps[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P[0], N, N, kTbRX, tb_rows(5),
+                              CU_TENSOR_MAP_SWIZZLE_NONE));
+    SDFGB_TRY(encode_tiled_2d(&maps[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P[1], N, N, kTbRX, tb_rows(5),
+                              CU_TENSOR_MAP_SWIZZLE_NONE));
+    CUtensorMap maps3[2];
+    SDFGB_TRY(encode_tiled_2d(&maps3[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P[0], N, N, kTbRX, tb_rows(3),
+                              CU_TENSOR_MAP_SWIZZLE_NONE));
+    SDFGB_TRY(encode_tiled_2d(&maps3[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P[1], N, N, kTbRX, tb_rows(3),
+                              CU_TENSOR_MAP_SWIZZLE_NONE));
+    int64_t t = 0;
+    while (T_ - t > 1) {
+        int64_t k = std::min<int64_t>(5, T_ - 1 - t);
+        if ((k & 1) == 0) k -= 1;
+        const int p = (int)(t & 1);
+        if (k == 5)
+            SDFGB_TRY(launch_tb<5>(maps[p], P[p ^ 1], N, coef, 5, s));
+        else if (k == 3)
+            SDFGB_TRY(launch_tb<3>(maps3[p], P[p ^ 1], N, coef, 3, s));
+        else
+            SDFGB_TRY(launch_step<float>(P[p], P[p ^ 1], N, N, 0, 1, N - 1, coef, terms, true, s));
+        t += k;
+    }
+    const int p = (int)(t & 1);
+    SDFGB_TRY(launch_step<float>(P[p], P[p ^ 1], N, N, 0, 1, N - 1, coef, terms, true, s));
+    return SDFGB_OK;
+}
+
 template <typename T>
 int launch_jacobi(T* A, int64_t N, int64_t T_, double coef, const int32_t* di, const int32_t* dj,
                   int nterms, void* stream) {
@@ -226,6 +366,11 @@ int launch_jacobi(T* A, int64_t N, int64_t T_, double coef, const int32_t* di, c
                          (long long)N, (long long)T_, nterms);
     if (N < 3 || T_ == 0) return SDFGB_OK;  // empty interior map
     cudaStream_t s = as_stream(stream);
+    if constexpr (sizeof(T) == 4) {
+        // temporal blocking needs 16 B rows (TMA) and enough steps to pay off
+        if (canon && (N % 4) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && T_ >= 4 && N >= 16)
+            return jacobi_f32_blocked(reinterpret_cast<float*>(A), N, T_, (float)coef, terms, s);
+    }
     T* P[2] = {A, A + N * N};
     for (int64_t t = 0; t < T_; ++t)
         SDFGB_TRY(launch_step<T>(P[t & 1], P[(t + 1) & 1], N, N, 0, 1, N - 1, (T)coef, terms, canon, s));

@@ -249,6 +249,22 @@ def test_jacobi_bit_exact(N, T, terms):
     np.testing.assert_array_equal(At64.cpu().numpy(), ref64)
 
 
+@pytest.mark.parametrize("N,T", [(16, 4), (20, 5), (132, 6), (256, 7), (1000, 11), (1024, 12), (520, 1003)])
+def test_jacobi_temporal_blocking_bit_exact(N, T):
+    """fp32 canonical order with N % 4 == 0 and T >= 4 runs the TMA temporal-
+    blocking kernel (odd step blocks + a final single step): both planes must
+    equal the one-step-at-a-time fp32 restatement bit for bit."""
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(N + T)
+    A = rng.random((2, N, N), dtype=np.float32)
+    ref = oracle.jacobi2d(A, T, fp32=True)
+    At = t(A)
+    device.jacobi2d(At, T)
+    got = At.cpu().numpy()
+    np.testing.assert_array_equal(got[T % 2], ref[T % 2])
+    np.testing.assert_array_equal(got[(T + 1) % 2], ref[(T + 1) % 2])
+
+
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 384, 128), (1000, 777, 300), (64, 200, 4),
                                    (129, 130, 36), (512, 512, 4096)])
 def test_gemm_3xtf32(M, N, K):
