@@ -218,31 +218,39 @@ int launch_step(const T* src, T* dst, int64_t N, int64_t rows, int64_t g0, int64
 
 // ---------------------------------------------------------------------------
 // Temporal blocking (canonical 5-point order, fp32): one launch advances KT
-// time steps.  A CTA TMA-loads its output tile plus a halo (8 columns, KT
-// rows each side) into shared memory, ping-pongs KT steps between two smem
-// buffers, and writes only the tile's centre -- the points whose KT-step
-// dependency cone lies inside the loaded region.  Per KT steps HBM sees one
-// read of ~1.2 planes and one write instead of KT reads + KT writes, and
-// every point is still computed as coef * ((((c + n) + s) + w) + e) in fp32,
-// so results stay bit-identical to the one-step kernel.  Points on the global
-// border are re-copied every step (never written), points outside the array
-// only feed border points.
-constexpr int kTbX = 128, kTbY = 64, kTbPad = 8, kTbMaxK = 7, kTbThreads = 256;
-constexpr int kTbRX = kTbX + 2 * kTbPad;  // 144 floats = 576 B rows
+// (odd) time steps.  A CTA TMA-loads its 112 x 96 output tile plus a halo
+// (8 columns, KT rows each side: a 128 x (96 + 2KT) region) into shared
+// memory and ping-pongs KT steps between two smem buffers; only the tile
+// centre -- whose KT-step dependency cone lies inside the region -- is
+// written back.  Per KT steps HBM sees ~1.3 plane reads + 1 plane write
+// instead of KT of each, and every point is still
+// coef * ((((c + n) + s) + w) + e) in fp32: bit-identical to one-step.
+//
+// Borders: the reference never writes the global border, and step t reads
+// plane t % 2 -- whose border is that plane's own.  Buffer 0 (states read
+// from plane p) holds plane p's border from the TMA load; buffer 1 (states
+// of plane p^1) gets plane p^1's border copied in once; steps never write
+// border points, so each buffer keeps the right plane's border.
+//
+// Work mapping: warp w owns a band of rows, lane l owns columns 4l..4l+3
+// (one float4); a north/centre register window slides down the band so each
+// step costs one LDS.128 + two shuffles per 4 points.
+constexpr int kTbRX = 128, kTbPad = 8, kTbX = kTbRX - 2 * kTbPad, kTbY = 96, kTbThreads = 256;
 
 __host__ __device__ constexpr int tb_rows(int k) { return kTbY + 2 * k; }
 __host__ __device__ constexpr size_t tb_smem(int k) { return (size_t)2 * kTbRX * tb_rows(k) * 4 + 128 + 64; }
 
 template <int KT>
 __global__ void __launch_bounds__(kTbThreads, 2)
-jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, float* __restrict__ dst, int N, float coef, int steps) {
+jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restrict__ dst_in,
+                 float* __restrict__ dst, int N, float coef, int steps) {
     constexpr int RY = tb_rows(KT);
-    constexpr int G4 = kTbRX / 4;  // 4-float column groups per row
     extern __shared__ uint8_t smem_raw[];
     float* buf0 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     float* buf1 = buf0 + kTbRX * RY;
     uint64_t* bar = reinterpret_cast<uint64_t*>(buf1 + kTbRX * RY);
 
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int x0 = blockIdx.x * kTbX, y0 = blockIdx.y * kTbY;
     const int gx0 = x0 - kTbPad, gy0 = y0 - KT;  // region origin (may be negative: TMA zero-fills)
     if (threadIdx.x == 0) {
@@ -252,28 +260,39 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, float* __restrict__ ds
         mbar_expect_tx(bar, (uint32_t)(kTbRX * RY * 4));
         tma_load_2d(buf0, &src, bar, gx0, gy0);
     }
+    // does the region touch the global border (or beyond)?  CTA-uniform
+    const bool edge = gx0 <= 0 || gy0 <= 0 || gx0 + kTbRX - 1 >= N - 1 || gy0 + RY - 1 >= N - 1;
+    if (edge) {  // buffer 1 carries plane p^1's border
+        for (int q = threadIdx.x; q < kTbRX * RY; q += kTbThreads) {
+            const int gy = gy0 + q / kTbRX, gx = gx0 + q % kTbRX;
+            if (gy >= 0 && gy < N && gx >= 0 && gx < N && (gy == 0 || gy == N - 1 || gx == 0 || gx == N - 1))
+                buf1[q] = dst_in[(int64_t)gy * N + gx];
+        }
+    }
     __syncthreads();
     mbar_wait(bar, 0);
+
+    // this warp's row band inside [1, RY-2]
+    const int rb = 1 + (warp * (RY - 2)) / 8, re = 1 + ((warp + 1) * (RY - 2)) / 8;
+    const int gx = gx0 + 4 * lane;
+    bool colb[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) colb[j] = gx + j <= 0 || gx + j >= N - 1;
 
     for (int st = 0; st < steps; ++st) {
         const float* in = (st & 1) ? buf1 : buf0;
         float* out = (st & 1) ? buf0 : buf1;
-        for (int it = threadIdx.x; it < (RY - 2) * G4; it += kTbThreads) {
-            const int r = 1 + it / G4, g = it % G4;
-            const float* rc = in + r * kTbRX + 4 * g;
-            const float4 c4 = *reinterpret_cast<const float4*>(rc);
-            const float4 n4 = *reinterpret_cast<const float4*>(rc - kTbRX);
-            const float4 s4 = *reinterpret_cast<const float4*>(rc + kTbRX);
-            const float lft = g > 0 ? rc[-1] : 0.f;
-            const float rgt = g < G4 - 1 ? rc[4] : 0.f;
+        float4 n4 = *reinterpret_cast<const float4*>(in + (rb - 1) * kTbRX + 4 * lane);
+        float4 c4 = *reinterpret_cast<const float4*>(in + rb * kTbRX + 4 * lane);
+        for (int r = rb; r < re; ++r) {
+            const float4 s4 = *reinterpret_cast<const float4*>(in + (r + 1) * kTbRX + 4 * lane);
+            const float lft = __shfl_up_sync(0xffffffffu, c4.w, 1);   // lane 0: region edge, unused
+            const float rgt = __shfl_down_sync(0xffffffffu, c4.x, 1); // lane 31: region edge, unused
             const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
             const float nn[4] = {n4.x, n4.y, n4.z, n4.w};
             const float ss[4] = {s4.x, s4.y, s4.z, s4.w};
             const float ww[4] = {lft, c4.x, c4.y, c4.z};
             const float ee[4] = {c4.y, c4.z, c4.w, rgt};
-            const int gy = gy0 + r;
-            const int gxb = gx0 + 4 * g;
-            const bool rowb = gy <= 0 || gy >= N - 1;
             float o[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -281,10 +300,20 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, float* __restrict__ ds
                 acc = __fadd_rn(acc, ss[j]);
                 acc = __fadd_rn(acc, ww[j]);
                 acc = __fadd_rn(acc, ee[j]);
-                const int gx = gxb + j;
-                o[j] = (rowb || gx <= 0 || gx >= N - 1) ? cc[j] : __fmul_rn(coef, acc);
+                o[j] = __fmul_rn(coef, acc);
             }
-            *reinterpret_cast<float4*>(out + r * kTbRX + 4 * g) = make_float4(o[0], o[1], o[2], o[3]);
+            float* op = out + r * kTbRX + 4 * lane;
+            if (!edge) {
+                *reinterpret_cast<float4*>(op) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
+                const int gy = gy0 + r;
+                const bool rowb = gy <= 0 || gy >= N - 1;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (!rowb && !colb[j]) op[j] = o[j];
+            }
+            n4 = c4;
+            c4 = s4;
         }
         __syncthreads();
     }
@@ -293,31 +322,34 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, float* __restrict__ ds
     constexpr int CG = kTbX / 4;
     for (int it = threadIdx.x; it < kTbY * CG; it += kTbThreads) {
         const int r = it / CG, g = it % CG;
-        const int gy = y0 + r, gx = x0 + 4 * g;
+        const int gy = y0 + r, gxx = x0 + 4 * g;
         if (gy < 1 || gy > N - 2) continue;
         const float4 v = *reinterpret_cast<const float4*>(fin + (KT + r) * kTbRX + kTbPad + 4 * g);
-        float* d = dst + (int64_t)gy * N + gx;
-        if (gx >= 1 && gx + 3 <= N - 2) {
+        float* d = dst + (int64_t)gy * N + gxx;
+        if (gxx >= 1 && gxx + 3 <= N - 2) {
             *reinterpret_cast<float4*>(d) = v;
         } else {
             const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-                if (gx + j >= 1 && gx + j <= N - 2) d[j] = vv[j];
+                if (gxx + j >= 1 && gxx + j <= N - 2) d[j] = vv[j];
         }
     }
 }
 
 template <int KT>
-int launch_tb(const CUtensorMap& map, float* dst, int64_t N, float coef, int steps, cudaStream_t s) {
+int launch_tb(const float* src_plane, float* dst, int64_t N, float coef, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         SDFGB_CUDA(cudaFuncSetAttribute(jacobi_tb_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)tb_smem(KT)));
         attr = true;
     }
+    CUtensorMap map;
+    SDFGB_TRY(encode_tiled_2d(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, src_plane, N, N, kTbRX, tb_rows(KT),
+                              CU_TENSOR_MAP_SWIZZLE_NONE));
     dim3 grid((unsigned)((N + kTbX - 1) / kTbX), (unsigned)((N + kTbY - 1) / kTbY));
-    jacobi_tb_kernel<KT><<<grid, kTbThreads, tb_smem(KT), s>>>(map, dst, (int)N, coef, steps);
+    jacobi_tb_kernel<KT><<<grid, kTbThreads, tb_smem(KT), s>>>(map, dst, dst, (int)N, coef, KT);
     SDFGB_LAUNCHED("jacobi_tb_kernel");
     return SDFGB_OK;
 }
@@ -328,25 +360,17 @@ int launch_tb(const CUtensorMap& map, float* dst, int64_t N, float coef, int ste
 // holding state T-1 exactly like A[(T+1) % 2] of the reference.
 int jacobi_f32_blocked(float* A, int64_t N, int64_t T_, float coef, const Terms& terms, cudaStream_t s) {
     float* P[2] = {A, A + N * N};
-    CUtensorMap maps[2];
-    SDFGB_TRY(encode_tiled_2d(&maps[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P[0], N, N, kTbRX, tb_rows(5),
-                              CU_TENSOR_MAP_SWIZZLE_NONE));
-    SDFGB_TRY(encode_tiled_2d(&maps[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P[1], N, N, kTbRX, tb_rows(5),
-                              CU_TENSOR_MAP_SWIZZLE_NONE));
-    CUtensorMap maps3[2];
-    SDFGB_TRY(encode_tiled_2d(&maps3[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P[0], N, N, kTbRX, tb_rows(3),
-                              CU_TENSOR_MAP_SWIZZLE_NONE));
-    SDFGB_TRY(encode_tiled_2d(&maps3[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P[1], N, N, kTbRX, tb_rows(3),
-                              CU_TENSOR_MAP_SWIZZLE_NONE));
     int64_t t = 0;
     while (T_ - t > 1) {
-        int64_t k = std::min<int64_t>(5, T_ - 1 - t);
+        int64_t k = std::min<int64_t>(7, T_ - 1 - t);
         if ((k & 1) == 0) k -= 1;
         const int p = (int)(t & 1);
-        if (k == 5)
-            SDFGB_TRY(launch_tb<5>(maps[p], P[p ^ 1], N, coef, 5, s));
+        if (k == 7)
+            SDFGB_TRY(launch_tb<7>(P[p], P[p ^ 1], N, coef, s));
+        else if (k == 5)
+            SDFGB_TRY(launch_tb<5>(P[p], P[p ^ 1], N, coef, s));
         else if (k == 3)
-            SDFGB_TRY(launch_tb<3>(maps3[p], P[p ^ 1], N, coef, 3, s));
+            SDFGB_TRY(launch_tb<3>(P[p], P[p ^ 1], N, coef, s));
         else
             SDFGB_TRY(launch_step<float>(P[p], P[p ^ 1], N, N, 0, 1, N - 1, coef, terms, true, s));
         t += k;
