@@ -284,15 +284,15 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
         float* out = (st & 1) ? buf0 : buf1;
         float4 n4 = *reinterpret_cast<const float4*>(in + (rb - 1) * kTbRX + 4 * lane);
         float4 c4 = *reinterpret_cast<const float4*>(in + rb * kTbRX + 4 * lane);
-        for (int r = rb; r < re; ++r) {
-            const float4 s4 = *reinterpret_cast<const float4*>(in + (r + 1) * kTbRX + 4 * lane);
-            const float lft = __shfl_up_sync(0xffffffffu, c4.w, 1);   // lane 0: region edge, unused
-            const float rgt = __shfl_down_sync(0xffffffffu, c4.x, 1); // lane 31: region edge, unused
-            const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
-            const float nn[4] = {n4.x, n4.y, n4.z, n4.w};
-            const float ss[4] = {s4.x, s4.y, s4.z, s4.w};
-            const float ww[4] = {lft, c4.x, c4.y, c4.z};
-            const float ee[4] = {c4.y, c4.z, c4.w, rgt};
+        // one output row from its north/centre/south float4s
+        auto row = [&](int r, const float4& nq, const float4& cq, const float4& sq) {
+            const float lft = __shfl_up_sync(0xffffffffu, cq.w, 1);   // lane 0: region edge, unused
+            const float rgt = __shfl_down_sync(0xffffffffu, cq.x, 1); // lane 31: region edge, unused
+            const float cc[4] = {cq.x, cq.y, cq.z, cq.w};
+            const float nn[4] = {nq.x, nq.y, nq.z, nq.w};
+            const float ss[4] = {sq.x, sq.y, sq.z, sq.w};
+            const float ww[4] = {lft, cq.x, cq.y, cq.z};
+            const float ee[4] = {cq.y, cq.z, cq.w, rgt};
             float o[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -312,8 +312,19 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
                 for (int j = 0; j < 4; ++j)
                     if (!rowb && !colb[j]) op[j] = o[j];
             }
-            n4 = c4;
-            c4 = s4;
+        };
+        int r = rb;
+        for (; r + 1 < re; r += 2) {  // two rows per iteration: 2x ILP, no register rotation moves
+            const float4 sa = *reinterpret_cast<const float4*>(in + (r + 1) * kTbRX + 4 * lane);
+            const float4 sb = *reinterpret_cast<const float4*>(in + (r + 2) * kTbRX + 4 * lane);
+            row(r, n4, c4, sa);
+            row(r + 1, c4, sa, sb);
+            n4 = sa;
+            c4 = sb;
+        }
+        if (r < re) {
+            const float4 sa = *reinterpret_cast<const float4*>(in + (r + 1) * kTbRX + 4 * lane);
+            row(r, n4, c4, sa);
         }
         __syncthreads();
     }
