@@ -245,10 +245,13 @@ __global__ void __launch_bounds__(kTbThreads, 2)
 jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restrict__ dst_in,
                  float* __restrict__ dst, int N, float coef, int steps) {
     constexpr int RY = tb_rows(KT);
-    extern __shared__ uint8_t smem_raw[];
-    float* buf0 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-    float* buf1 = buf0 + kTbRX * RY;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(buf1 + kTbRX * RY);
+    // dynamic smem starts at the CTA window base (no static smem here), so it
+    // is 1 KB-aligned for TMA; indexing the extern array directly keeps the
+    // accesses in the shared state space (LDS/STS, not generic LD/ST)
+    extern __shared__ __align__(1024) float tb_smem_f[];
+    float* buf0 = tb_smem_f;
+    float* buf1 = tb_smem_f + kTbRX * RY;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tb_smem_f + 2 * kTbRX * RY);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int x0 = blockIdx.x * kTbX, y0 = blockIdx.y * kTbY;
