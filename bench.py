@@ -200,12 +200,16 @@ def bench_histogram(args, dist, P):
     imgs = [torch.rand(H, W, device="cuda", generator=g) for _ in range(nbuf)]
     hist = torch.zeros(256, dtype=torch.int64, device="cuda")
     oob = torch.zeros(1, dtype=torch.int64, device="cuda")
-    reduce_ = dist.pg is not None
+    multi = dist.pg is not None
+    if multi:
+        from paper_1902_10345_b200 import multigpu as MG
+        be = MG.DeviceBackend()
 
     def step(k):
-        device.hist(imgs[k % nbuf], hist, oob)
-        if reduce_:  # per-GPU partial bins -> allreduce (NCCL)
-            dist.pg.all_reduce(hist)
+        if multi:  # each rank bins its own image; partial bins -> all_reduce (NCCL)
+            MG.histogram(dist.pg, imgs[k % nbuf], hist, oob, be)
+        else:
+            device.hist(imgs[k % nbuf], hist, oob)
 
     ms = time_steps(step, args.steps, args.warmup, dist)
     assert oob.item() == 0
@@ -241,16 +245,21 @@ def bench_query(args, dist, P):
     out = torch.empty(n, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     ws = device.query_workspace(n, 4)
-    offsets = dist.pg is not None
+    multi = dist.pg is not None
+    if multi:
+        from paper_1902_10345_b200 import multigpu as MG
+        be = MG.DeviceBackend()
+        gcnt = torch.zeros(1, dtype=torch.int64, device="cuda")
 
     def step(k):
-        device.query(col, 0.5, out, cnt, ws, "<")
-        if offsets:  # per-shard compaction; global offsets from an all-gather of counts
-            allc = torch.empty(dist.world, dtype=torch.int64, device="cuda")
-            dist.pg.all_gather_into_tensor(allc, cnt)
+        if multi:  # per-shard compaction; global offsets from an all-gather of counts
+            MG.query(dist.pg, col, 0.5, out, gcnt, be, "<")
+        else:
+            device.query(col, 0.5, out, cnt, ws, "<")
 
     ms = time_steps(step, args.steps, args.warmup, dist)
-    nsel = int(cnt.item()) // (args.steps + args.warmup)
+    total = int((gcnt if multi else cnt).item()) // (args.steps + args.warmup)
+    nsel = total // dist.world  # per-rank average survivors
     by = 4 * n + 4 * nsel + 8
     res = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms, "bytes_per_unit": by,
            "launches_per_step": 1, "roofline": roof("hbm", by / ms / 1e6, P, "query_kernel"),
@@ -279,18 +288,26 @@ def bench_query(args, dist, P):
 def bench_spmv(args, dist, P):
     import torch
     from paper_1902_10345_b200 import device, _lib
-    H = W = 1 << 22
+    H = W = 1 << 22  # per rank: rows H, x shard W; global columns W * world
     nz = 64
     g = torch.Generator(device="cuda").manual_seed(3 + dist.rank)
-    col = torch.sort(torch.randint(0, W, (H, nz), device="cuda", generator=g, dtype=torch.int32), dim=1)[0]
+    Wg = W * dist.world
+    col = torch.sort(torch.randint(0, Wg, (H, nz), device="cuda", generator=g, dtype=torch.int32), dim=1)[0]
     col = col.reshape(-1).contiguous()
     val = torch.rand(H * nz, device="cuda", generator=g)
     x = torch.rand(W, device="cuda", generator=g)
     rowptr = (torch.arange(H + 1, device="cuda", dtype=torch.int64) * nz).to(torch.int32)
     b = torch.zeros(H, device="cuda")
+    multi = dist.pg is not None
+    if multi:
+        from paper_1902_10345_b200 import multigpu as MG
+        be = MG.DeviceBackend()
 
     def step(k):
-        device.spmv(rowptr, col, val, x, b)
+        if multi:  # row blocks; x shards all-gathered (NCCL) before the row kernel
+            MG.spmv(dist.pg, rowptr, col, val, x, b, be)
+        else:
+            device.spmv(rowptr, col, val, x, b)
 
     ms = time_steps(step, args.steps, args.warmup, dist)
     nnz = H * nz
@@ -327,23 +344,36 @@ def bench_jacobi(args, dist, P):
     from paper_1902_10345_b200 import device, _lib
     N, T = 8192, 1000
     g = torch.Generator(device="cuda").manual_seed(2 + dist.rank)
-    A = torch.zeros(2, N, N, device="cuda")
-    A[0, 1:-1, 1:-1] = torch.rand(N - 2, N - 2, device="cuda", generator=g)
-    A[1] = A[0]
+    multi = dist.pg is not None
+    if multi:  # rows N per rank of a (N * world) x N grid, 1-row halos exchanged per step
+        from paper_1902_10345_b200 import multigpu as MG
+        be = MG.DeviceBackend()
+        rows = torch.rand(2, N, N, device="cuda", generator=g)
+        rows[:, :, 0] = 0
+        rows[:, :, -1] = 0
+        slab = MG.jacobi_slab(rows, dist.rank * N, N * dist.world)
+        del rows
+    else:
+        A = torch.zeros(2, N, N, device="cuda")
+        A[0, 1:-1, 1:-1] = torch.rand(N - 2, N - 2, device="cuda", generator=g)
+        A[1] = A[0]
 
     def step(k):
-        device.jacobi2d(A, T)
+        if multi:
+            MG.jacobi(dist.pg, slab, T, be)
+        else:
+            device.jacobi2d(A, T)
 
     steps = max(1, min(args.steps, 3))
     ms = time_steps(step, steps, 1, dist)
     per = 4 * N * N + 4 * (N - 2) * (N - 2)
     by = per * T
     res = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms, "bytes_per_unit": by,
-           "launches_per_step": T, "roofline": roof("hbm", per / (ms / T) / 1e6, P, "jacobi_step_kernel"),
+           "launches_per_step": T, "roofline": roof("hbm", per / (ms / T) / 1e6, P, "jacobi_tb_kernel"),
            "l2": "2 x 256 MiB planes > L2",
            "config": {"workload": "Jacobi-2D 8192^2 fp32, T=1000 (whole time loop per step)", "N": N, "T": T},
            "steps": steps, "warmup": 1}
-    if args.e2e:
+    if args.e2e and not multi:
         L = _lib.load()
         hA = pinned((2, N, N), torch.float64)
         hA.copy_(A.double().cpu())
@@ -362,13 +392,24 @@ def bench_gemm(n, args, dist, P):
     import torch
     from paper_1902_10345_b200 import device, _lib
     g = torch.Generator(device="cuda").manual_seed(4 + dist.rank)
-    A = torch.rand(n, n, device="cuda", generator=g)
-    B = torch.rand(n, n, device="cuda", generator=g)
     C = torch.empty(n, n, device="cuda")
-    ws = device.gemm_workspace(n, n, n)
+    multi = dist.pg is not None
+    if multi:  # 2-D grid: each rank an n x n C block; A/B panels all-gathered in grid rows/cols
+        from paper_1902_10345_b200 import multigpu as MG
+        be = MG.DeviceBackend()
+        grid = MG.GemmGrid(dist.pg)
+        A = torch.rand(n // grid.Q, n, device="cuda", generator=g)
+        B = torch.rand(n // grid.P, n, device="cuda", generator=g)
+    else:
+        A = torch.rand(n, n, device="cuda", generator=g)
+        B = torch.rand(n, n, device="cuda", generator=g)
+        ws = device.gemm_workspace(n, n, n)
 
     def step(k):
-        device.gemm(A, B, C, ws)
+        if multi:
+            MG.gemm(dist.pg, grid, A, B, C, be)
+        else:
+            device.gemm(A, B, C, ws)
 
     steps = max(2, min(args.steps, 10 if n <= 4096 else 4))
     ms = time_steps(step, steps, args.warmup, dist)
@@ -380,12 +421,12 @@ def bench_gemm(n, args, dist, P):
            "launches_per_step": 3,
            "roofline": {"bound": "tensor", "achieved": tf, "peak": pk, "unit": "TFLOP/s", "frac": tf / pk,
                         "peak_note": f"3xTF32 = {'sustained' if sustained else 'burst'} bf16 / 2 / 3 ({P['src']})",
-                        "achieved_note": "includes the hi/lo split pre-pass",
-                        "traffic": traffic_table().get("gemm_3xtf32_kernel")},
+                        "achieved_note": "includes the hi/lo split pre-pass", "kernel": "gemm_3xtf32_kernel",
+                        "traffic": traffic("gemm_3xtf32_kernel")[0], "traffic_note": traffic("gemm_3xtf32_kernel")[1]},
            "l2": "operands + split workspace > L2" if n >= 4096 else "",
            "config": {"workload": f"MM fp32 {n}^3 via tcgen05 3xTF32", "M": n, "N": n, "K": n},
            "steps": steps}
-    if args.e2e and n <= 4096:
+    if args.e2e and n <= 4096 and not multi:
         L = _lib.load()
         hA = pinned((n, n), torch.float64)
         hA.copy_(A.double().cpu())
@@ -402,12 +443,18 @@ def bench_gemm(n, args, dist, P):
     return res
 
 
+def traffic(kernel):
+    t = traffic_table().get(kernel)
+    return (t["bytes"], f"{t['per']}; {t['source']}") if t else (None, "no ncu capture")
+
+
 def roof(bound, achieved, P, kernel):
     pk = P["hbm"]
+    tb, tnote = traffic(kernel)
     return {"bound": bound, "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
             "peak_note": f"{P['src']} HBM copy bandwidth (MEASURED_PEAKS.json)",
-            "frac_of_8TBs_spec": achieved / 8000.0,
-            "traffic": traffic_table().get(kernel)}
+            "frac_of_8TBs_spec": achieved / 8000.0, "kernel": kernel,
+            "traffic": tb, "traffic_note": tnote}
 
 
 # ---------------------------------------------------------------- CPU arm
@@ -435,40 +482,57 @@ def _par(fn, parts):
         x.join()
 
 
+def _ref_or_port(key):
+    fn = ref_lib(key)
+    if fn is not None:
+        return fn, "reference"
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle  # the C restatement: cpu_baseline leg only
+    return oracle, "port"
+
+
+def _best(fn, reps):
+    best = 1e30
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def _P(a, off_elems=0):
+    return ctypes.c_void_p(a.ctypes.data + a.itemsize * off_elems)
+
+
+def _I(v):
+    return ctypes.c_int64(int(v))
+
+
 def cpu_query(reps=2):
     """The reference's generated query C (oracle/_ref) on all host cores:
     the map's range is split into contiguous chunks, one C call per chunk
-    (the stream drain keeps per-chunk order, chunks are concatenated)."""
+    (each chunk's stream drain keeps order; chunks concatenate)."""
     n = 1 << 26
-    fn = ref_lib("query")
-    kind = "reference"
-    if fn is None:
-        kind = "port"
+    fn, kind = _ref_or_port("query")
     col = np.random.default_rng(1).random(n, dtype=np.float32).astype(np.float64)
     out = np.empty(n)
     thr = np.array([0.5])
     T = _threads()
     bounds = np.linspace(0, n, T + 1).astype(np.int64)
     counts = np.zeros((T, 1), np.int64)
-    if fn is None:
-        sys.path.insert(0, os.path.join(REPO, "oracle"))
-        import oracle
 
     def work(i):
         a, b = int(bounds[i]), int(bounds[i + 1])
-        if fn is not None:
-            fn(ctypes.c_void_p(col.ctypes.data + 8 * a), ctypes.c_void_p(thr.ctypes.data),
-               ctypes.c_void_p(out.ctypes.data + 8 * a), ctypes.c_void_p(counts[i].ctypes.data),
-               ctypes.c_int64(b - a))
+        if kind == "reference":
+            fn(_P(col, a), _P(thr), _P(out, a), _P(counts[i]), _I(b - a))
         else:
-            oracle.lib().orc_query_f64(col.ctypes.data + 8 * a, b - a, 0, 0.5, out.ctypes.data + 8 * a,
-                                       counts[i].ctypes.data)
-    best = 1e30
-    for _ in range(reps):
+            fn.lib().orc_query_f64(col.ctypes.data + 8 * a, b - a, 0, 0.5, out.ctypes.data + 8 * a,
+                                   counts[i].ctypes.data)
+
+    def once():
         counts[:] = 0
-        t0 = time.perf_counter()
         _par(work, [(i,) for i in range(T)])
-        best = min(best, time.perf_counter() - t0)
+    best = _best(once, reps)
     nsel = int(counts.sum())
     by = 4 * n + 4 * nsel + 8
     return {"value": by / best / 1e9, "unit": "GB/s", "cores": T, "kind": kind,
@@ -476,20 +540,128 @@ def cpu_query(reps=2):
             "seconds": best}
 
 
+def cpu_histogram(reps=2):
+    H = W = 4096
+    fn, kind = _ref_or_port("histogram")
+    img = np.random.default_rng(0).random((H, W), dtype=np.float32).astype(np.float64)
+    T = _threads()
+    bounds = np.linspace(0, H, T + 1).astype(np.int64)
+    parts = np.zeros((T, 256), np.int64)
+
+    def work(i):
+        a, b = int(bounds[i]), int(bounds[i + 1])
+        if kind == "reference":
+            fn(_P(img, a * W), _P(parts[i]), _I(b - a), _I(W))
+        else:
+            fn.lib().orc_histogram_f64(img.ctypes.data + 8 * a * W, (b - a) * W, parts[i].ctypes.data, 256,
+                                       256.0, 1.0)
+
+    def once():
+        parts[:] = 0
+        _par(work, [(i,) for i in range(T)])
+    best = _best(once, reps)
+    by = 4 * H * W + 2 * 256 * 8
+    return {"value": by / best / 1e9, "unit": "GB/s", "cores": T, "kind": kind,
+            "sample": f"full 4096^2 image, {T} threads x row blocks (partial bins summed), best of {reps}",
+            "seconds": best}
+
+
+def cpu_spmv(reps=2, rows=1 << 18):
+    H = W = 1 << 22
+    nz = 64
+    fn, kind = _ref_or_port("spmv")
+    rng = np.random.default_rng(3)
+    cols = np.sort(rng.integers(0, W, (rows, nz)), axis=1).reshape(-1).astype(np.int64)
+    vals = rng.random(rows * nz)
+    x = rng.random(W)
+    b = np.zeros(rows)
+    rowptr = np.arange(rows + 1, dtype=np.int64) * nz
+    T = _threads()
+    bounds = np.linspace(0, rows, T + 1).astype(np.int64)
+
+    def work(i):
+        a, e = int(bounds[i]), int(bounds[i + 1])
+        if kind == "reference":
+            fn(_P(rowptr, a), _P(cols), _P(vals), _P(x), _P(b, a), _I(e - a), _I(W), _I(rows * nz))
+        else:
+            fn.lib().orc_spmv_f64(rowptr.ctypes.data + 8 * a, cols.ctypes.data, vals.ctypes.data, x.ctypes.data,
+                                  b.ctypes.data + 8 * a, e - a)
+    best = _best(lambda: _par(work, [(i,) for i in range(T)]), reps)
+    by = rows * nz * 8 + 4 * (rows + 1) + 4 * W * rows // H + 8 * rows
+    return {"value": by / best / 1e9, "unit": "GB/s", "cores": T, "kind": kind,
+            "sample": f"{rows} of 2^22 rows (64 nnz each, full x), {T} threads x row blocks, best of {reps}",
+            "seconds": best}
+
+
+def cpu_jacobi(steps=2):
+    N = 8192
+    fn, kind = _ref_or_port("jacobi2d_omp")
+    A = np.zeros((2, N, N))
+    A[0, 1:-1, 1:-1] = np.random.default_rng(2).random((N - 2, N - 2), dtype=np.float32)
+    A[1] = A[0]
+    if kind == "reference":
+        best = _best(lambda: fn(_P(A), _I(N), _I(steps)), 1)
+        T = _threads()
+        sample = f"jacobi2d_omp (cpu_parallel schedule, -fopenmp, {T} threads), {steps} of 1000 steps"
+    else:
+        best = _best(lambda: fn.jacobi2d(A, steps), 1)
+        T = 1
+        sample = f"C port, 1 thread, {steps} of 1000 steps"
+    per = 4 * N * N + 4 * (N - 2) * (N - 2)
+    return {"value": per * steps / best / 1e9, "unit": "GB/s", "cores": T, "kind": kind, "sample": sample,
+            "seconds": best}
+
+
+def cpu_gemm(n, rows):
+    fn, kind = _ref_or_port("matmul_chain32")
+    rng = np.random.default_rng(4)
+    A = rng.random((rows, n), dtype=np.float32).astype(np.float64)
+    B = rng.random((n, n), dtype=np.float32).astype(np.float64)
+    C = np.zeros((rows, n))
+    T = _threads()
+    bounds = np.linspace(0, rows, T + 1).astype(np.int64)
+
+    def work(i):
+        a, e = int(bounds[i]), int(bounds[i + 1])
+        if e > a:
+            if kind == "reference":
+                fn(_P(A, a * n), _P(B), _P(C, a * n), _I(e - a), _I(n), _I(n))
+            else:
+                fn.lib().orc_matmul_f64(A.ctypes.data + 8 * a * n, B.ctypes.data, C.ctypes.data + 8 * a * n,
+                                        e - a, n, n, 0, e - a)
+    best = _best(lambda: _par(work, [(i,) for i in range(T)]), 1)
+    return {"value": 2.0 * rows * n * n / best / 1e12, "unit": "TFLOP/s", "cores": T, "kind": kind,
+            "sample": f"{rows} of {n} rows of the MapReduceFusion->MapTiling(32)->LocalStorage(B) chain "
+                      f"(paper §5.2), {T} threads x row blocks", "seconds": best}
+
+
+CPU = {"histogram": cpu_histogram, "query": cpu_query, "spmv": cpu_spmv, "jacobi2d": cpu_jacobi,
+       "gemm4096": lambda: cpu_gemm(4096, 2 * _threads()), "gemm16384": lambda: cpu_gemm(16384, _threads())}
+
+
 # ---------------------------------------------------------------- main
 
 def run_reference(args):
+    """The reference's own CPU path (oracle/_ref) for every motif on all host
+    cores; the headline line is configs[1] (Query), the rest under motifs."""
     dist_rank = int(os.environ.get("RANK", "0"))
     if dist_rank != 0:
         return 0
-    r = cpu_query(reps=max(1, min(args.steps, 3)))
+    motifs = {}
+    for m in ALL:
+        try:
+            motifs[m] = CPU[m]() if m != "query" else cpu_query(reps=max(1, min(args.steps, 3)))
+        except Exception as exc:
+            motifs[m] = {"error": str(exc)[:200]}
+    r = motifs[HEADLINE]
     line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
+            "data": "synthetic (seeded numpy)",
             "config": {"workload": "Query x < 0.5 over 2^26 (configs[1]), reference-generated C on host cores"},
             "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "motifs": {k: {kk: vv for kk, vv in v.items() if kk != "seconds"} for k, v in motifs.items()}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -541,7 +713,12 @@ def main():
         "motifs": {k: {kk: vv for kk, vv in v.items()} for k, v in results.items()},
     }
     if dist.rank == 0 and args.cpu:
-        line["cpu_baseline"] = {k: v for k, v in cpu_query(reps=1).items() if k != "seconds"}
+        for m in results:
+            try:
+                results[m]["cpu_baseline"] = {k: v for k, v in CPU[m]().items() if k != "seconds"}
+            except Exception as exc:  # a CPU sample must not sink the GPU line
+                results[m]["cpu_baseline"] = {"error": str(exc)[:200]}
+        line["cpu_baseline"] = results[HEADLINE]["cpu_baseline"]
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
     dist.close()

@@ -1,0 +1,207 @@
+"""Multi-GPU decompositions of the motifs: one process per
+GPU, ``torch.distributed`` (NCCL on GPUs) for the exchanges, libsdfgb200
+kernels for the per-shard compute.
+
+Each runner takes ``pg`` (the ``torch.distributed`` module) and a compute
+``backend``; the default is the device kernels of :mod:`.device`.  The
+decompositions keep every element's operation order, so a sharded result is
+bit-identical to the one-device result for histogram, query and Jacobi (and
+for SpMV, whose rows stay whole).  Per-GPU work is fixed as ranks are added
+(weak scaling), as in bench.py.
+
+The exchange steps are the ones the north star names:
+  histogram  per-GPU partial bins -> all_reduce(sum)
+  query      per-shard compaction -> all_gather of counts -> global offsets
+             (output stays sharded at its global offset; gather is optional)
+  spmv       row blocks, x sharded -> all_gather(x) -> row kernel
+  jacobi     row blocks with 1-row halos -> per-step send/recv of halo rows
+  gemm       2-D process grid -> all_gather of A row panels / B column panels
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+
+class DeviceBackend:
+    """Per-shard compute on the local GPU through the C ABI."""
+
+    def __init__(self):
+        from . import device
+        self.d = device
+        self._ws = {}
+
+    def hist(self, img, hist, oob, scale=256.0, div=1.0):
+        self.d.hist(img, hist, oob, scale, div)
+
+    def query(self, col, thr, out, count, op="<"):
+        import torch
+        key = ("q", col.numel(), col.element_size(), col.device)
+        if key not in self._ws:
+            self._ws[key] = self.d.query_workspace(col.numel(), col.element_size(), col.device)
+        self.d.query(col, thr, out, count, self._ws[key], op)
+
+    def spmv(self, rowptr, col, val, x, b):
+        self.d.spmv(rowptr, col, val, x, b)
+
+    def jacobi_step(self, src, dst, N, rows, r0, r1, coef, terms):
+        self.d.jacobi2d_step(src, dst, N, rows, 0, r0, r1, coef, terms)
+
+    def gemm(self, A, B, C):
+        M, K = A.shape
+        N = B.shape[1]
+        key = ("g", M, N, K, A.device)
+        if key not in self._ws:
+            self._ws[key] = self.d.gemm_workspace(M, N, K, A.device)
+        self.d.gemm(A, B, C, self._ws[key])
+
+
+def _rank_world(pg):
+    return pg.get_rank(), pg.get_world_size()
+
+
+# ----------------------------------------------------------------- histogram
+
+def histogram(pg, img_shard, hist, oob, backend, scale=256.0, div=1.0):
+    """hist += counts of the union of all ranks' shards (every rank ends with
+    the same hist); oob likewise."""
+    import torch
+    part = torch.zeros_like(hist)
+    pbad = torch.zeros_like(oob)
+    backend.hist(img_shard, part, pbad, scale, div)
+    pg.all_reduce(part)
+    pg.all_reduce(pbad)
+    hist += part
+    oob += pbad
+
+
+# --------------------------------------------------------------------- query
+
+def query(pg, col_shard, thr, out_shard, count, backend, op="<", gather=False):
+    """Per-shard compaction.  Returns (k_local, offset): this rank's survivors
+    are out_shard[0:k_local] and belong at global out_vals[offset:offset+k].
+    ``count`` (replicated) is advanced by the global survivor count.  With
+    ``gather`` rank 0 also returns the concatenated survivors."""
+    import torch
+    rank, world = _rank_world(pg)
+    local = torch.zeros(1, dtype=torch.int64, device=col_shard.device)
+    backend.query(col_shard, thr, out_shard, local, op)
+    counts = torch.empty(world, dtype=torch.int64, device=col_shard.device)
+    pg.all_gather_into_tensor(counts, local)
+    cl = counts.tolist()
+    offset = sum(cl[:rank])
+    count += int(sum(cl))
+    if not gather:
+        return cl[rank], offset, None
+    kmax = max(cl) if cl else 0
+    pad = torch.zeros(max(kmax, 1), dtype=out_shard.dtype, device=out_shard.device)
+    pad[:cl[rank]] = out_shard[:cl[rank]]
+    allv = torch.empty(world * max(kmax, 1), dtype=out_shard.dtype, device=out_shard.device)
+    pg.all_gather_into_tensor(allv, pad)
+    full = torch.cat([allv[r * max(kmax, 1): r * max(kmax, 1) + cl[r]] for r in range(world)]) \
+        if rank == 0 else None
+    return cl[rank], offset, full
+
+
+# ---------------------------------------------------------------------- spmv
+
+def spmv(pg, rowptr_local, col, val, x_shard, b_local, backend):
+    """Row-block SpMV: rowptr_local/col/val/b_local are this rank's rows (col
+    holds GLOBAL column ids), x is sharded in equal contiguous blocks."""
+    import torch
+    rank, world = _rank_world(pg)
+    x = torch.empty(x_shard.numel() * world, dtype=x_shard.dtype, device=x_shard.device)
+    pg.all_gather_into_tensor(x, x_shard)
+    backend.spmv(rowptr_local, col, val, x, b_local)
+    return x
+
+
+# -------------------------------------------------------------------- jacobi
+
+@dataclass
+class JacobiSlab:
+    """This rank's rows of the global [2, Ng, N] array plus one halo row on
+    each side: planes [2, rows + 2, N]; local row l <-> global row g0 + l - 1."""
+    A: object
+    g0: int
+    rows: int
+    Ng: int
+
+
+def jacobi_slab(A_global_rows, g0, Ng):
+    """Build a slab from this rank's interior rows [2, rows, N] (a copy)."""
+    import torch
+    two, rows, N = A_global_rows.shape
+    A = torch.zeros((2, rows + 2, N), dtype=A_global_rows.dtype, device=A_global_rows.device)
+    A[:, 1:rows + 1] = A_global_rows
+    return JacobiSlab(A, g0, rows, Ng)
+
+
+def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1))):
+    """T steps of the guard loop (loops.py:31-61) over row blocks.  Before each
+    step the source plane's boundary rows are exchanged with the neighbours
+    (send/recv, the 'row-block halo exchange'); global rows 0 and Ng-1 are
+    the border and never written, exactly like the reference."""
+    rank, world = _rank_world(pg)
+    A, rows, N = slab.A, slab.rows, slab.A.shape[-1]
+    first_global = slab.g0
+    last_global = slab.g0 + rows - 1
+    # local interior rows to compute: skip the global border rows
+    r0 = 1 + (1 if first_global == 0 else 0)
+    r1 = rows + 1 - (1 if last_global == slab.Ng - 1 else 0)
+    for t in range(T):
+        src, dst = A[t % 2], A[(t + 1) % 2]
+        _halo_exchange(pg, src, rows, rank, world)
+        if r1 > r0:
+            backend.jacobi_step(src, dst, N, rows + 2, r0, r1, coef, terms)
+
+
+def _halo_exchange(pg, plane, rows, rank, world):
+    ops = []
+    if rank > 0:
+        ops.append(pg.P2POp(pg.isend, plane[1].contiguous(), rank - 1))
+        ops.append(pg.P2POp(pg.irecv, plane[0], rank - 1))
+    if rank < world - 1:
+        ops.append(pg.P2POp(pg.isend, plane[rows].contiguous(), rank + 1))
+        ops.append(pg.P2POp(pg.irecv, plane[rows + 1], rank + 1))
+    if ops:
+        for r in pg.batch_isend_irecv(ops):
+            r.wait()
+
+
+# ---------------------------------------------------------------------- gemm
+
+def grid_shape(world):
+    """P x Q process grid, P <= Q, as square as possible (2 -> 1x2, 4 -> 2x2, 8 -> 2x4)."""
+    p = int(math.isqrt(world))
+    while world % p:
+        p -= 1
+    return p, world // p
+
+
+class GemmGrid:
+    """Row / column sub-groups of the P x Q grid (rank = i * Q + j)."""
+
+    def __init__(self, pg):
+        rank, world = _rank_world(pg)
+        self.P, self.Q = grid_shape(world)
+        self.i, self.j = divmod(rank, self.Q)
+        self.row_groups = [pg.new_group([i * self.Q + j for j in range(self.Q)]) for i in range(self.P)]
+        self.col_groups = [pg.new_group([i * self.Q + j for i in range(self.P)]) for j in range(self.Q)]
+        self.row_group = self.row_groups[self.i]
+        self.col_group = self.col_groups[self.j]
+
+
+def gemm(pg, grid: GemmGrid, A_piece, B_piece, C_block, backend):
+    """C block (i, j) = A row panel i x B column panel j.  A panel i is split
+    by rows over the Q ranks of grid row i, B panel j by rows (of K) over the
+    P ranks of grid column j; each is all-gathered inside its group.  K is not
+    split, so every C element keeps the single-device summation."""
+    import torch
+    Aq = torch.empty((A_piece.shape[0] * grid.Q, A_piece.shape[1]), dtype=A_piece.dtype, device=A_piece.device)
+    pg.all_gather_into_tensor(Aq, A_piece.contiguous(), group=grid.row_group)
+    Bp = torch.empty((B_piece.shape[0] * grid.P, B_piece.shape[1]), dtype=B_piece.dtype, device=B_piece.device)
+    pg.all_gather_into_tensor(Bp, B_piece.contiguous(), group=grid.col_group)
+    backend.gemm(Aq, Bp, C_block)
+    return Aq, Bp

@@ -1,0 +1,191 @@
+"""Multi-rank decompositions (paper_1902_10345_b200/multigpu.py) on CPU with
+the gloo backend: world sizes 2 and 4, per-shard compute by the C oracle.
+Every sharded result must equal the single-domain oracle bit for bit (the
+decompositions keep each element's operation order)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+
+from paper_1902_10345_b200 import multigpu as MG
+
+
+class OracleBackend:
+    """Per-shard compute on CPU tensors through the C oracle (test only)."""
+
+    def hist(self, img, hist, oob, scale=256.0, div=1.0):
+        h, bad = oracle.histogram(img.numpy(), hist.numpy(), scale, div)
+        hist.copy_(torch.from_numpy(h))
+        oob += bad
+
+    def query(self, col, thr, out, count, op="<"):
+        o, c = oracle.query(col.numpy(), thr, out.numpy(), count.numpy(), op)
+        out.copy_(torch.from_numpy(o))
+        count.copy_(torch.from_numpy(c))
+
+    def spmv(self, rowptr, col, val, x, b):
+        r = oracle.spmv(rowptr.numpy(), col.numpy(), val.numpy(), x.numpy(), b.numpy(), fp32=True)
+        b.copy_(torch.from_numpy(r))
+
+    def jacobi_step(self, src, dst, N, rows, r0, r1, coef, terms):
+        s = src.numpy()
+        d = dst.numpy()
+        c32 = np.float32(coef)
+        for i in range(r0, r1):
+            acc = s[i + terms[0][0], 1 + terms[0][1]:N - 1 + terms[0][1]].copy()
+            for di, dj in terms[1:]:
+                acc = acc + s[i + di, 1 + dj:N - 1 + dj]
+            d[i, 1:N - 1] = c32 * acc
+
+    def gemm(self, A, B, C):
+        C.copy_(torch.from_numpy(oracle.matmul(A.numpy(), B.numpy()).astype(np.float32)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+CASES = ["histogram", "query", "spmv", "jacobi", "gemm"]
+
+
+def _worker(rank, world, port, names, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    for name in names:
+        try:
+            res[name] = globals()["_case_" + name](rank, world)
+        except Exception:  # surface worker failures to the test
+            import traceback
+            res[name] = "ERROR " + traceback.format_exc()
+    q.put((rank, res))
+    dist.destroy_process_group()
+
+
+def run_ranks(names, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, names, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    return out  # rank -> {case: result}
+
+
+_RESULTS = {}
+
+
+def results(world):
+    if world not in _RESULTS:
+        _RESULTS[world] = run_ranks(CASES, world)
+    return _RESULTS[world]
+
+
+# ------------------------------------------------------------------ cases
+
+def _case_histogram(rank, world):
+    rng = np.random.default_rng(0)
+    img = rng.random((64 * world, 48), dtype=np.float32)
+    img[::37, ::5] = 1.5  # out of range
+    rows = img.shape[0] // world
+    hist = torch.full((256,), 3, dtype=torch.int64)
+    oob = torch.zeros(1, dtype=torch.int64)
+    MG.histogram(dist, torch.from_numpy(img[rank * rows:(rank + 1) * rows].copy()), hist, oob, OracleBackend())
+    ref, bad = oracle.histogram(img, np.full(256, 3, np.int64))
+    return bool(np.array_equal(hist.numpy(), ref) and oob.item() == bad)
+
+
+def _case_query(rank, world):
+    rng = np.random.default_rng(1)
+    col = rng.random(1000 * world + 0, dtype=np.float32)
+    n = col.size // world
+    shard = torch.from_numpy(col[rank * n:(rank + 1) * n].copy())
+    out = torch.zeros(n, dtype=torch.float32)
+    count = torch.full((1,), 5, dtype=torch.int64)
+    k, off, full = MG.query(dist, shard, 0.5, out, count, OracleBackend(), "<", gather=True)
+    ref = col[col < 0.5]
+    ok = count.item() == 5 + ref.size and np.array_equal(out[:k].numpy(), ref[off:off + k])
+    if rank == 0:
+        ok = ok and np.array_equal(full.numpy(), ref)
+    return bool(ok)
+
+
+def _case_spmv(rank, world):
+    rng = np.random.default_rng(2)
+    Hl, Wl, nz = 50, 40, 7
+    H, W = Hl * world, Wl * world
+    cols = np.sort(rng.integers(0, W, (H, nz)), axis=1).astype(np.int32)
+    vals = rng.random((H, nz), dtype=np.float32)
+    x = rng.random(W, dtype=np.float32)
+    b0 = rng.random(H, dtype=np.float32)
+    rp_local = torch.from_numpy((np.arange(Hl + 1) * nz).astype(np.int32))
+    b = torch.from_numpy(b0[rank * Hl:(rank + 1) * Hl].copy())
+    MG.spmv(dist, rp_local, torch.from_numpy(cols[rank * Hl:(rank + 1) * Hl].reshape(-1).copy()),
+            torch.from_numpy(vals[rank * Hl:(rank + 1) * Hl].reshape(-1).copy()),
+            torch.from_numpy(x[rank * Wl:(rank + 1) * Wl].copy()), b, OracleBackend())
+    ref = oracle.spmv((np.arange(H + 1) * nz).astype(np.int32), cols.reshape(-1), vals.reshape(-1), x, b0, fp32=True)
+    return bool(np.array_equal(b.numpy(), ref[rank * Hl:(rank + 1) * Hl]))
+
+
+def _case_jacobi(rank, world):
+    rng = np.random.default_rng(3)
+    rows, N, T = 9, 12, 5
+    Ng = rows * world
+    A = rng.random((2, Ng, N), dtype=np.float32)  # distinct planes, non-zero borders
+    # reference: the whole domain is square in the oracle, so embed it: run a
+    # non-square restatement with the same op order instead
+    ref = A.copy()
+    for t in range(T):
+        s, d = ref[t % 2], ref[(t + 1) % 2]
+        acc = s[1:-1, 1:-1] + s[0:-2, 1:-1]
+        acc = acc + s[2:, 1:-1]
+        acc = acc + s[1:-1, 0:-2]
+        acc = acc + s[1:-1, 2:]
+        d[1:-1, 1:-1] = np.float32(0.2) * acc
+    slab = MG.jacobi_slab(torch.from_numpy(A[:, rank * rows:(rank + 1) * rows].copy()), rank * rows, Ng)
+    MG.jacobi(dist, slab, T, OracleBackend())
+    got = slab.A[:, 1:rows + 1].numpy()
+    return bool(np.array_equal(got, ref[:, rank * rows:(rank + 1) * rows]))
+
+
+def _case_gemm(rank, world):
+    grid = MG.GemmGrid(dist)
+    rng = np.random.default_rng(4)
+    n, K = 8, 12
+    A = rng.random((grid.P * n, K), dtype=np.float32)
+    B = rng.random((K, grid.Q * n), dtype=np.float32)
+    Ai = A[grid.i * n:(grid.i + 1) * n]                 # A row panel i
+    Bj = B[:, grid.j * n:(grid.j + 1) * n]              # B column panel j
+    a_piece = Ai[grid.j * (n // grid.Q):(grid.j + 1) * (n // grid.Q)]
+    b_piece = Bj[grid.i * (K // grid.P):(grid.i + 1) * (K // grid.P)]
+    C = torch.zeros((n, n), dtype=torch.float32)
+    MG.gemm(dist, grid, torch.from_numpy(a_piece.copy()), torch.from_numpy(b_piece.copy()), C, OracleBackend())
+    ref = oracle.matmul(A, B).astype(np.float32)
+    return bool(np.array_equal(C.numpy(), ref[grid.i * n:(grid.i + 1) * n, grid.j * n:(grid.j + 1) * n]))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", CASES)
+def test_sharded_equals_single_domain(case, world):
+    per_rank = {r: v[case] for r, v in results(world).items()}
+    for r, v in per_rank.items():
+        assert v is True, f"rank {r}: {v}"
+
+
+def test_grid_shapes():
+    assert [MG.grid_shape(w) for w in (1, 2, 4, 8)] == [(1, 1), (1, 2), (2, 2), (2, 4)]
