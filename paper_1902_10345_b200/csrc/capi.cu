@@ -7,6 +7,7 @@
 // sm_100a kernel(s) and copy the non-transient containers back.
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -79,6 +80,9 @@ struct DevicePool {
     void* buf[8] = {};
     size_t cap[8] = {};
     cudaStream_t stream = nullptr;
+    cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams for the pipelined entries
+    int64_t* pinned = nullptr;                  // small pinned scratch (per-chunk counts)
+    size_t pinned_n = 0;
 };
 DevicePool g_pools[32];
 
@@ -91,6 +95,19 @@ struct Session {
         pool = &g_pools[dev & 31];
         lock = std::unique_lock<std::mutex>(pool->mu);
         if (!pool->stream) SDFGB_CUDA(cudaStreamCreateWithFlags(&pool->stream, cudaStreamNonBlocking));
+        if (!pool->h2d) SDFGB_CUDA(cudaStreamCreateWithFlags(&pool->h2d, cudaStreamNonBlocking));
+        if (!pool->d2h) SDFGB_CUDA(cudaStreamCreateWithFlags(&pool->d2h, cudaStreamNonBlocking));
+        return SDFGB_OK;
+    }
+    int pinned(size_t n, int64_t** out) {
+        if (pool->pinned_n < n) {
+            if (pool->pinned) SDFGB_CUDA(cudaFreeHost(pool->pinned));
+            pool->pinned = nullptr;
+            pool->pinned_n = 0;
+            SDFGB_CUDA(cudaHostAlloc(&pool->pinned, n * sizeof(int64_t), cudaHostAllocPortable));
+            pool->pinned_n = n;
+        }
+        *out = pool->pinned;
         return SDFGB_OK;
     }
     template <typename T>
@@ -204,57 +221,88 @@ extern "C" int sdfgb_host_histogram_i64(const int64_t* img, int64_t* hist, int64
 // --------------------------------------------------------------------- query
 extern "C" int sdfgb_host_query(const double* col, const double* thr, double* out_vals, int64_t* count,
                                 int64_t N, int op, int precision) {
+    // Pipelined: the column streams in chunks on a copy stream, each chunk is
+    // compacted (into its own slice of the device output) on the compute
+    // stream, and each chunk's survivors stream back on a second copy stream
+    // to their final offset (the running count) -- H2D, compute and D2H of
+    // different chunks overlap.  Order is the input order, as in the
+    // reference's FIFO drain.
     if (N < 0 || !thr || !count || (N > 0 && (!col || !out_vals)))
         return set_error(SDFGB_ERR_INVALID, "query: bad arguments");
+    if (N == 0) return SDFGB_OK;
     Session ss;
     SDFGB_TRY(ss.open());
-    cudaStream_t s = ss.s();
+    cudaStream_t cs = ss.s(), hs = ss.pool->h2d, ds = ss.pool->d2h;
     const bool f32 = precision == SDFGB_PREC_FP32;
-    double* dcol;
-    int64_t* dcount;
-    void* ws;
-    const size_t wsb = sdfgb_query_workspace_bytes(N, f32 ? 4 : 8);
+    const int64_t chunk = std::min<int64_t>(N, (int64_t)1 << 23);
+    const int64_t nch = (N + chunk - 1) / chunk;
+    double *dcol, *dout;
     SDFGB_TRY(ss.get(0, N, &dcol));
-    double* dout;
     SDFGB_TRY(ss.get(1, N, &dout));
-    SDFGB_TRY(ss.get(3, 1, &dcount));
+    float* df = nullptr;
+    if (f32) SDFGB_TRY(ss.get(2, 2 * N, &df));
+    int64_t* dcnt;
+    SDFGB_TRY(ss.get(3, nch, &dcnt));
+    const size_t wsb = sdfgb_query_workspace_bytes(chunk, f32 ? 4 : 8);
     uint8_t* wsp;
     SDFGB_TRY(ss.get(4, (int64_t)wsb, &wsp));
-    ws = wsp;
-    // the workspace self-resets after each launch; clear it when (re)allocated
     static thread_local void* cleared = nullptr;
     static thread_local size_t cleared_bytes = 0;
-    if (cleared != ws || cleared_bytes < wsb) {
-        SDFGB_CUDA(cudaMemsetAsync(ws, 0, wsb, s));
-        cleared = ws;
+    if (cleared != wsp || cleared_bytes < wsb) {
+        SDFGB_CUDA(cudaMemsetAsync(wsp, 0, wsb, cs));
+        cleared = wsp;
         cleared_bytes = wsb;
     }
-    SDFGB_TRY(h2d(dcol, col, N, s));
-    SDFGB_TRY(h2d(dcount, count, 1, s));
-    const int64_t before = count[0];
-    if (f32) {
-        float *dcf, *doutf;
-        SDFGB_TRY(ss.get(2, 2 * N, &dcf));
-        doutf = dcf + N;
-        SDFGB_TRY(convert(dcol, dcf, N, s));
-        SDFGB_TRY(sdfgb_query_f32(dcf, N, op, thr[0], doutf, dcount, ws, wsb, s));
-        int64_t after = 0;
-        SDFGB_TRY(d2h(&after, dcount, 1, s));
-        SDFGB_CUDA(cudaStreamSynchronize(s));
-        const int64_t k = after - before;
-        SDFGB_TRY(convert(doutf, dout, k, s));
-        SDFGB_TRY(d2h(out_vals, dout, k, s));
-        SDFGB_CUDA(cudaStreamSynchronize(s));
-        count[0] = after;
-    } else {
-        SDFGB_TRY(sdfgb_query_f64(dcol, N, op, thr[0], dout, dcount, ws, wsb, s));
-        int64_t after = 0;
-        SDFGB_TRY(d2h(&after, dcount, 1, s));
-        SDFGB_CUDA(cudaStreamSynchronize(s));
-        SDFGB_TRY(d2h(out_vals, dout, after - before, s));
-        SDFGB_CUDA(cudaStreamSynchronize(s));
-        count[0] = after;
+    int64_t* hcnt;
+    SDFGB_TRY(ss.pinned((size_t)nch, &hcnt));
+    SDFGB_CUDA(cudaMemsetAsync(dcnt, 0, (size_t)nch * 8, cs));
+    std::vector<cudaEvent_t> ev_in(nch), ev_cnt(nch);
+    for (int64_t i = 0; i < nch; ++i) {
+        SDFGB_CUDA(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+        SDFGB_CUDA(cudaEventCreateWithFlags(&ev_cnt[i], cudaEventDisableTiming));
     }
+    cudaEvent_t start;
+    SDFGB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    SDFGB_CUDA(cudaEventRecord(start, cs));
+    SDFGB_CUDA(cudaStreamWaitEvent(hs, start, 0));  // after the workspace/count clears
+    for (int64_t i = 0; i < nch; ++i) {
+        const int64_t off = i * chunk, len = std::min(chunk, N - off);
+        SDFGB_TRY(h2d(dcol + off, col + off, len, hs));
+        SDFGB_CUDA(cudaEventRecord(ev_in[i], hs));
+        SDFGB_CUDA(cudaStreamWaitEvent(cs, ev_in[i], 0));
+        if (f32) {
+            SDFGB_TRY(convert(dcol + off, df + off, len, cs));
+            SDFGB_TRY(sdfgb_query_f32(df + off, len, op, thr[0], df + N + off, dcnt + i, wsp, wsb, cs));
+        } else {
+            SDFGB_TRY(sdfgb_query_f64(dcol + off, len, op, thr[0], dout + off, dcnt + i, wsp, wsb, cs));
+        }
+        SDFGB_CUDA(cudaMemcpyAsync(hcnt + i, dcnt + i, 8, cudaMemcpyDeviceToHost, cs));
+        SDFGB_CUDA(cudaEventRecord(ev_cnt[i], cs));
+    }
+    int64_t running = count[0];
+    int rc = SDFGB_OK;
+    for (int64_t i = 0; i < nch && rc == SDFGB_OK; ++i) {
+        rc = check_cuda(cudaEventSynchronize(ev_cnt[i]), "query chunk");
+        if (rc != SDFGB_OK) break;
+        const int64_t off = i * chunk, k = hcnt[i];
+        if (k > 0) {
+            rc = check_cuda(cudaStreamWaitEvent(ds, ev_cnt[i], 0), "wait");
+            // widen this chunk's survivors on the D2H stream (not behind the
+            // remaining chunks' kernels), then ship them
+            if (f32 && rc == SDFGB_OK) rc = convert(df + N + off, dout + off, k, ds);
+            if (rc == SDFGB_OK) rc = d2h(out_vals + (running - count[0]), dout + off, k, ds);
+        }
+        running += k;
+    }
+    if (rc == SDFGB_OK) rc = check_cuda(cudaStreamSynchronize(ds), "D2H");
+    if (rc == SDFGB_OK) rc = check_cuda(cudaStreamSynchronize(cs), "query");
+    for (int64_t i = 0; i < nch; ++i) {
+        cudaEventDestroy(ev_in[i]);
+        cudaEventDestroy(ev_cnt[i]);
+    }
+    cudaEventDestroy(start);
+    if (rc != SDFGB_OK) return rc;
+    count[0] = running;
     return SDFGB_OK;
 }
 

@@ -21,7 +21,7 @@
 #include <atomic>
 #include <cmath>
 
-#include "common.cuh"
+#include "tma.cuh"
 
 namespace sdfgb {
 namespace {
@@ -291,6 +291,240 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
     if (c == 0 && tid == 0) atomicAdd(count, (unsigned long long)base_off);
 }
 
+// ---------------------------------------------------------------------------
+// TMA-pipelined variant (the common case: 16 B-aligned column).  One CTA per
+// SM; each round r gives CTA c the segment r*G + c of kTSegBytes.  A single
+// thread streams segments into a 3-deep ring of smem buffers with
+// cp.async.bulk (TMA) and mbarriers, so HBM never waits for the warps:
+//   prologue  bulk-load rounds 0, 1, 2; count(0)
+//   round r   count(r+1) (smem) -> publish;  gather(r);  write(r) from smem
+//             (scan, stage, 128-bit drain);  bulk-load round r+3 into the
+//             buffer round r just released.
+// The column is read from HBM exactly once and never re-read from L2.
+constexpr int kTSegBytes = 48 * 1024;
+constexpr int kTStages = 3;
+constexpr int kTVec = 3;  // float4 per thread per write sub-tile
+
+template <typename T>
+__host__ __device__ constexpr int tseg_elems() { return kTSegBytes / (int)sizeof(T); }
+template <typename T>
+__host__ __device__ constexpr int tsub_elems() { return kQBlock * kTVec * Vec16<T>::n; }
+template <typename T>
+__host__ __device__ constexpr size_t tma_query_smem() {
+    return (size_t)kTStages * kTSegBytes + (size_t)(tsub_elems<T>() + 4) * sizeof(T) + 256;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(kQBlock, 1)
+query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
+                 unsigned long long* __restrict__ count, QueryWs* __restrict__ ws, int64_t rounds,
+                 uint32_t epoch) {
+    using V = typename Vec16<T>::type;
+    constexpr int VN = Vec16<T>::n;
+    constexpr int SEG = tseg_elems<T>();
+    constexpr int SUB = tsub_elems<T>();
+    constexpr int NW = kQBlock / 32;
+    static_assert(SEG % SUB == 0 && SEG % (kQBlock * VN) == 0, "segment geometry");
+
+    extern __shared__ __align__(1024) uint8_t q_smem[];
+    T* segs = reinterpret_cast<T*>(q_smem);
+    T* s_stage = reinterpret_cast<T*>(q_smem + kTStages * kTSegBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(q_smem + kTStages * kTSegBytes + (SUB + 4) * sizeof(T));
+    __shared__ uint64_t s_warp[NW];
+    __shared__ int64_t s_red[NW], s_tot[NW];
+    __shared__ uint32_t s_cnt[NW];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t G = gridDim.x, c = blockIdx.x;
+
+    auto seg_len = [&](int64_t r) -> int64_t {
+        const int64_t start = (r * G + c) * (int64_t)SEG;
+        return start >= n ? 0 : (n - start < SEG ? n - start : SEG);
+    };
+    auto issue = [&](int64_t r) {  // thread 0 only
+        const int b = (int)(r % kTStages);
+        const int64_t len = seg_len(r);
+        const uint32_t bytes = (uint32_t)((len * (int64_t)sizeof(T)) & ~int64_t(15));
+        mbar_expect_tx(&bars[b], bytes);
+        if (bytes) bulk_g2s(segs + (size_t)b * SEG, col + (r * G + c) * (int64_t)SEG, bytes, &bars[b]);
+    };
+    auto wait = [&](int64_t r) -> const T* {
+        const int b = (int)(r % kTStages);
+        mbar_wait(&bars[b], (uint32_t)((r / kTStages) & 1));
+        T* buf = segs + (size_t)b * SEG;
+        const int64_t len = seg_len(r);
+        const int64_t done = ((len * (int64_t)sizeof(T)) & ~int64_t(15)) / (int64_t)sizeof(T);
+        if (done < len) {  // sub-16 B tail of the very last segment
+            if (tid < len - done) buf[done + tid] = col[(r * G + c) * (int64_t)SEG + done + tid];
+            __syncthreads();
+        }
+        return buf;
+    };
+    auto count_seg = [&](int64_t r, const T* buf) {
+        const int64_t len = seg_len(r);
+        uint32_t cnt = 0;
+        if (len == SEG) {
+#pragma unroll
+            for (int k = 0; k < SEG / (kQBlock * VN); ++k) {
+                const V x = reinterpret_cast<const V*>(buf)[k * kQBlock + tid];
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x, cc), thr) ? 1u : 0u;
+            }
+        } else {
+            for (int64_t e = tid; e < len; e += kQBlock) cnt += pred<OP>(buf[e], thr) ? 1u : 0u;
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+        if (lane == 0) s_cnt[warp] = cnt;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) t += s_cnt[w];
+            st_relaxed(&ws->status[r * G + c], pack_status(epoch, kFlagAgg, t));
+        }
+    };
+
+    if (tid == 0) {
+        for (int b = 0; b < kTStages; ++b) mbar_init(&bars[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int64_t r = 0; r < kTStages && r < rounds; ++r) issue(r);
+    }
+    __syncthreads();
+    count_seg(0, wait(0));
+
+    int64_t base_off = 0;
+    for (int64_t r = 0; r < rounds; ++r) {
+        if (r + 1 < rounds) count_seg(r + 1, wait(r + 1));
+        // ---- all-gather of round r's counts (thread q reads CTA q's word)
+        int64_t val = 0;
+        if (tid < G) {
+            uint64_t w;
+            while (true) {
+                w = ld_relaxed(&ws->status[r * G + tid]);
+                if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
+                __nanosleep(16);
+            }
+            val = (int64_t)(w & kValueMask);
+        }
+        int64_t lower = tid < c ? val : 0;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            lower += __shfl_xor_sync(0xffffffffu, lower, d);
+            val += __shfl_xor_sync(0xffffffffu, val, d);
+        }
+        if (lane == 0) {
+            s_red[warp] = lower;
+            s_tot[warp] = val;
+        }
+        __syncthreads();
+        int64_t off = base_off, round_total = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            off += s_red[w];
+            round_total += s_tot[w];
+        }
+        // ---- write(r) from the smem segment
+        const T* buf = segs + (size_t)(r % kTStages) * SEG;
+        const int64_t len = seg_len(r);
+        for (int j = 0; j * SUB < len; ++j) {
+            const T* sb = buf + j * SUB;
+            const int64_t sl = len - (int64_t)j * SUB;  // elements left from this sub-tile on
+            uint32_t bits = 0;
+            T v[kTVec][VN];
+#pragma unroll
+            for (int k = 0; k < kTVec; ++k) {
+                const int e0 = k * kQBlock * VN + tid * VN;
+                const V x = reinterpret_cast<const V*>(sb)[k * kQBlock + tid];
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) {
+                    v[k][cc] = vget<V, T>(x, cc);
+                    if ((sl >= SUB || e0 + cc < sl) && pred<OP>(v[k][cc], thr)) bits |= 1u << (k * VN + cc);
+                }
+            }
+            uint64_t mine = 0;
+#pragma unroll
+            for (int k = 0; k < kTVec; ++k)
+                mine |= (uint64_t)__popc((bits >> (k * VN)) & ((1u << VN) - 1)) << (16 * k);
+            uint64_t incl = mine;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += o;
+            }
+            __syncthreads();  // previous drain / s_red reads done
+            if (lane == 31) s_warp[warp] = incl;
+            __syncthreads();
+            uint64_t ws_ = lane < NW ? s_warp[lane] : 0;
+#pragma unroll
+            for (int d = 1; d < NW; d <<= 1) {
+                uint64_t o = __shfl_up_sync(0xffffffffu, ws_, d);
+                if (lane >= d) ws_ += o;
+            }
+            const uint64_t wprev = __shfl_sync(0xffffffffu, ws_, (warp + 31) & 31);
+            const uint64_t wpre = warp ? wprev : 0;
+            const uint64_t total = __shfl_sync(0xffffffffu, ws_, NW - 1);
+            const uint64_t excl = wpre + incl - mine;
+            const uint32_t sh0 = (uint32_t)(off & (VN - 1));
+            uint32_t agg = 0;
+#pragma unroll
+            for (int k = 0; k < kTVec; ++k) {
+                uint32_t rr = sh0 + agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) {
+                    const bool p = bits & (1u << (k * VN + cc));
+                    if (p) s_stage[rr] = v[k][cc];
+                    rr += p;
+                }
+                agg += (uint32_t)((total >> (16 * k)) & 0xffff);
+            }
+            __syncthreads();
+            const uint32_t head = min(agg, (uint32_t)((VN - sh0) & (VN - 1)));
+            if (tid < head) out[off + tid] = s_stage[sh0 + tid];
+            const uint32_t nv = (agg - head) / VN;
+            const V* sv = reinterpret_cast<const V*>(s_stage + sh0 + head);
+            V* gv = reinterpret_cast<V*>(out + off + head);
+            if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+                for (uint32_t q = tid; q < nv; q += kQBlock) gv[q] = sv[q];
+                for (uint32_t rr = head + nv * VN + tid; rr < agg; rr += kQBlock) out[off + rr] = s_stage[sh0 + rr];
+            } else {
+                for (uint32_t rr = head + tid; rr < agg; rr += kQBlock) out[off + rr] = s_stage[sh0 + rr];
+            }
+            off += agg;
+        }
+        base_off += round_total;
+        __syncthreads();  // segment r's buffer is free
+        if (tid == 0 && r + kTStages < rounds) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(r + kTStages);
+        }
+    }
+    if (c == 0 && tid == 0) atomicAdd(count, (unsigned long long)base_off);
+}
+
+template <typename T>
+auto query_tma_kernel_for(int op) {
+    switch (op) {
+    case 0: return query_tma_kernel<T, 0>;
+    case 1: return query_tma_kernel<T, 1>;
+    case 2: return query_tma_kernel<T, 2>;
+    case 3: return query_tma_kernel<T, 3>;
+    case 4: return query_tma_kernel<T, 4>;
+    case 5: return query_tma_kernel<T, 5>;
+    case 6: return query_tma_kernel<T, 6>;
+    default: return query_tma_kernel<T, 7>;
+    }
+}
+
 std::atomic<uint32_t> g_epoch{0};
 
 uint32_t next_epoch() {
@@ -374,6 +608,24 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
     int kop;
     T tt;
     fold_threshold<T>(op, thr, kop, tt);
+    if (vec) {
+        // TMA ring: one CTA per SM, segments of kTSegBytes
+        auto tk = query_tma_kernel_for<T>(kop);
+        static bool attr[2][8] = {};
+        if (!attr[sizeof(T) == 8][kop]) {
+            SDFGB_CUDA(cudaFuncSetAttribute((const void*)tk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)tma_query_smem<T>()));
+            attr[sizeof(T) == 8][kop] = true;
+        }
+        const int64_t segs = (n + tseg_elems<T>() - 1) / tseg_elems<T>();
+        const int64_t G = std::max<int64_t>(1, std::min<int64_t>({segs, (int64_t)num_sms(), (int64_t)kQBlock}));
+        const int64_t rounds = (segs + G - 1) / G;
+        void* args[] = {(void*)&col, (void*)&n, (void*)&tt, (void*)&out, (void*)&C, (void*)&W,
+                        (void*)&rounds, (void*)&epoch};
+        SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)tk, dim3((unsigned)G), dim3(kQBlock), args,
+                                               tma_query_smem<T>(), s));
+        return SDFGB_OK;
+    }
     auto kern = vec ? query_kernel_for<T, true>(kop) : query_kernel_for<T, false>(kop);
     static int occ[2][2][8] = {};  // [f64][vec][op] resident CTAs per SM
     int& o = occ[sizeof(T) == 8][vec][kop];
@@ -392,7 +644,10 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
 
 extern "C" size_t sdfgb_query_workspace_bytes(int64_t n, int elem_bytes) {
     // one status word per (round, CTA) slot; rounds * G <= segments + G - 1 < 2 * segments + kQBlock
-    const int64_t seg = elem_bytes == 8 ? sdfgb::seg_elems<double>() : sdfgb::seg_elems<float>();
+    // (both kernels: the TMA segments are larger than the register-path ones)
+    const int64_t seg = std::min<int64_t>(
+        elem_bytes == 8 ? sdfgb::seg_elems<double>() : sdfgb::seg_elems<float>(),
+        elem_bytes == 8 ? sdfgb::tseg_elems<double>() : sdfgb::tseg_elems<float>());
     const int64_t segs = (n + seg - 1) / seg;
     return offsetof(sdfgb::QueryWs, status) + (size_t)(segs + sdfgb::kQBlock) * 8;
 }
