@@ -303,7 +303,7 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
 // The column is read from HBM exactly once and never re-read from L2.
 constexpr int kTSegBytes = 48 * 1024;
 constexpr int kTStages = 3;
-constexpr int kTVec = 3;  // float4 per thread per write sub-tile
+constexpr int kTVec = 3;  // 16 B vectors per thread per write sub-tile (12 floats / 6 doubles)
 
 template <typename T>
 __host__ __device__ constexpr int tseg_elems() { return kTSegBytes / (int)sizeof(T); }
@@ -338,9 +338,8 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
     T* segs = reinterpret_cast<T*>(q_smem);
     T* s_stage = reinterpret_cast<T*>(q_smem + kTStages * kTSegBytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(q_smem + kTStages * kTSegBytes + (SUB + 4) * sizeof(T));
-    __shared__ uint64_t s_warp[NW];
-    __shared__ int64_t s_red[NW], s_tot[NW];
-    __shared__ uint32_t s_cnt[NW];
+    __shared__ int64_t s_red[NW + 1], s_tot[NW + 1];
+    __shared__ uint32_t s_cnt[NW], s_wsum[NW];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
@@ -405,7 +404,8 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
     int64_t base_off = 0;
     for (int64_t r = 0; r < rounds; ++r) {
         if (r + 1 < rounds) count_seg(r + 1, wait(r + 1));
-        // ---- all-gather of round r's counts (thread q reads CTA q's word)
+        // ---- all-gather of round r's counts (thread q reads CTA q's word);
+        // warp 0 folds the per-warp sums so each thread reads two values
         int64_t val = 0;
         if (tid < G) {
             uint64_t w;
@@ -427,65 +427,73 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
             s_tot[warp] = val;
         }
         __syncthreads();
-        int64_t off = base_off, round_total = 0;
+        if (warp == 0) {
+            int64_t lo = lane < NW ? s_red[lane] : 0, to = lane < NW ? s_tot[lane] : 0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            off += s_red[w];
-            round_total += s_tot[w];
+            for (int d = 16; d; d >>= 1) {
+                lo += __shfl_xor_sync(0xffffffffu, lo, d);
+                to += __shfl_xor_sync(0xffffffffu, to, d);
+            }
+            if (lane == 0) {
+                s_red[NW] = lo;
+                s_tot[NW] = to;
+            }
         }
-        // ---- write(r) from the smem segment
+        __syncthreads();
+        int64_t off = base_off + s_red[NW];
+        const int64_t round_total = s_tot[NW];
+        // ---- write(r) from the smem segment.  Thread t owns the contiguous
+        // elements [t*E, t*E + E) of each sub-tile (E = 12: 48 B per thread,
+        // conflict-free 128-bit smem reads), so input order = thread order and
+        // one 32-bit block scan of per-thread counts ranks every survivor.
+        constexpr int E = SUB / kQBlock;
+        constexpr int NV = E / VN;
         const T* buf = segs + (size_t)(r % kTStages) * SEG;
         const int64_t len = seg_len(r);
         for (int j = 0; j * SUB < len; ++j) {
             const T* sb = buf + j * SUB;
-            const int64_t sl = len - (int64_t)j * SUB;  // elements left from this sub-tile on
-            uint32_t bits = 0;
-            T v[kTVec][VN];
+            const int64_t sl = len - (int64_t)j * SUB;
+            T v[E];
 #pragma unroll
-            for (int k = 0; k < kTVec; ++k) {
-                const int e0 = k * kQBlock * VN + tid * VN;
-                const V x = reinterpret_cast<const V*>(sb)[k * kQBlock + tid];
+            for (int q = 0; q < NV; ++q) {
+                const V x = reinterpret_cast<const V*>(sb)[tid * NV + q];
 #pragma unroll
-                for (int cc = 0; cc < VN; ++cc) {
-                    v[k][cc] = vget<V, T>(x, cc);
-                    if ((sl >= SUB || e0 + cc < sl) && pred<OP>(v[k][cc], thr)) bits |= 1u << (k * VN + cc);
-                }
+                for (int cc = 0; cc < VN; ++cc) v[q * VN + cc] = vget<V, T>(x, cc);
             }
-            uint64_t mine = 0;
+            uint32_t bits = 0;
+            const int e0 = tid * E;
+            if (sl >= SUB) {
 #pragma unroll
-            for (int k = 0; k < kTVec; ++k)
-                mine |= (uint64_t)__popc((bits >> (k * VN)) & ((1u << VN) - 1)) << (16 * k);
-            uint64_t incl = mine;
+                for (int e = 0; e < E; ++e) bits |= (uint32_t)pred<OP>(v[e], thr) << e;
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) bits |= (uint32_t)(e0 + e < sl && pred<OP>(v[e], thr)) << e;
+            }
+            const uint32_t cnt = __popc(bits);
+            uint32_t incl = cnt;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
                 if (lane >= d) incl += o;
             }
-            __syncthreads();  // previous drain / s_red reads done
-            if (lane == 31) s_warp[warp] = incl;
+            __syncthreads();  // previous drain / s_wsum reads done
+            if (lane == 31) s_wsum[warp] = incl;
             __syncthreads();
-            uint64_t ws_ = lane < NW ? s_warp[lane] : 0;
+            uint32_t wt = lane < NW ? s_wsum[lane] : 0;
 #pragma unroll
             for (int d = 1; d < NW; d <<= 1) {
-                uint64_t o = __shfl_up_sync(0xffffffffu, ws_, d);
-                if (lane >= d) ws_ += o;
+                const uint32_t o = __shfl_up_sync(0xffffffffu, wt, d);
+                if (lane >= d) wt += o;
             }
-            const uint64_t wprev = __shfl_sync(0xffffffffu, ws_, (warp + 31) & 31);
-            const uint64_t wpre = warp ? wprev : 0;
-            const uint64_t total = __shfl_sync(0xffffffffu, ws_, NW - 1);
-            const uint64_t excl = wpre + incl - mine;
+            const uint32_t wprev = __shfl_sync(0xffffffffu, wt, (warp + 31) & 31);
+            const uint32_t agg = __shfl_sync(0xffffffffu, wt, NW - 1);
             const uint32_t sh0 = (uint32_t)(off & (VN - 1));
-            uint32_t agg = 0;
+            uint32_t rr = sh0 + (warp ? wprev : 0u) + incl - cnt;
 #pragma unroll
-            for (int k = 0; k < kTVec; ++k) {
-                uint32_t rr = sh0 + agg + (uint32_t)((excl >> (16 * k)) & 0xffff);
-#pragma unroll
-                for (int cc = 0; cc < VN; ++cc) {
-                    const bool p = bits & (1u << (k * VN + cc));
-                    if (p) s_stage[rr] = v[k][cc];
-                    rr += p;
-                }
-                agg += (uint32_t)((total >> (16 * k)) & 0xffff);
+            for (int e = 0; e < E; ++e) {
+                const bool p = (bits >> e) & 1u;
+                if (p) s_stage[rr] = v[e];
+                rr += p;
             }
             __syncthreads();
             const uint32_t head = min(agg, (uint32_t)((VN - sh0) & (VN - 1)));
@@ -495,9 +503,9 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
             V* gv = reinterpret_cast<V*>(out + off + head);
             if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
                 for (uint32_t q = tid; q < nv; q += kQBlock) gv[q] = sv[q];
-                for (uint32_t rr = head + nv * VN + tid; rr < agg; rr += kQBlock) out[off + rr] = s_stage[sh0 + rr];
+                for (uint32_t x = head + nv * VN + tid; x < agg; x += kQBlock) out[off + x] = s_stage[sh0 + x];
             } else {
-                for (uint32_t rr = head + tid; rr < agg; rr += kQBlock) out[off + rr] = s_stage[sh0 + rr];
+                for (uint32_t x = head + tid; x < agg; x += kQBlock) out[off + x] = s_stage[sh0 + x];
             }
             off += agg;
         }
