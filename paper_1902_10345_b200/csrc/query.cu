@@ -297,9 +297,11 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
 // thread streams segments into a 3-deep ring of smem buffers with
 // cp.async.bulk (TMA) and mbarriers, so HBM never waits for the warps:
 //   prologue  bulk-load rounds 0, 1, 2; count(0)
-//   round r   count(r+1) (smem) -> publish;  gather(r);  write(r) from smem
-//             (scan, stage, 128-bit drain);  bulk-load round r+3 into the
-//             buffer round r just released.
+//   round r   count(r+1) (smem, warp ballots) -> publish;  gather(r);
+//             write(r) from smem: each warp compacts its contiguous slice in
+//             order with ballots, starting at the CTA offset plus the lower
+//             warps' counts -- no block barrier inside;  bulk-load round r+3
+//             into the buffer round r just released.
 // The column is read from HBM exactly once and never re-read from L2.
 constexpr int kTSegBytes = 48 * 1024;
 constexpr int kTStages = 3;
@@ -311,7 +313,7 @@ template <typename T>
 __host__ __device__ constexpr int tsub_elems() { return kQBlock * kTVec * Vec16<T>::n; }
 template <typename T>
 __host__ __device__ constexpr size_t tma_query_smem() {
-    return (size_t)kTStages * kTSegBytes + (size_t)(tsub_elems<T>() + 4) * sizeof(T) + 256;
+    return (size_t)kTStages * kTSegBytes + 64;
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -327,21 +329,20 @@ __global__ void __launch_bounds__(kQBlock, 1)
 query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
                  unsigned long long* __restrict__ count, QueryWs* __restrict__ ws, int64_t rounds,
                  uint32_t epoch) {
-    using V = typename Vec16<T>::type;
-    constexpr int VN = Vec16<T>::n;
     constexpr int SEG = tseg_elems<T>();
-    constexpr int SUB = tsub_elems<T>();
     constexpr int NW = kQBlock / 32;
-    static_assert(SEG % SUB == 0 && SEG % (kQBlock * VN) == 0, "segment geometry");
+    constexpr int WSEG = SEG / NW;   // contiguous elements per warp per segment
+    constexpr int CH = WSEG / 32;    // 32-element chunks per warp
+    static_assert(SEG % (NW * 32) == 0, "segment geometry");
 
     extern __shared__ __align__(1024) uint8_t q_smem[];
     T* segs = reinterpret_cast<T*>(q_smem);
-    T* s_stage = reinterpret_cast<T*>(q_smem + kTStages * kTSegBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(q_smem + kTStages * kTSegBytes + (SUB + 4) * sizeof(T));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(q_smem + kTStages * kTSegBytes);
     __shared__ int64_t s_red[NW + 1], s_tot[NW + 1];
-    __shared__ uint32_t s_cnt[NW], s_wsum[NW];
+    __shared__ uint32_t s_wcnt[2][NW];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
     const int64_t G = gridDim.x, c = blockIdx.x;
 
     auto seg_len = [&](int64_t r) -> int64_t {
@@ -367,27 +368,27 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         }
         return buf;
     };
+    // warp-level count of this warp's contiguous slice; CTA total published
     auto count_seg = [&](int64_t r, const T* buf) {
         const int64_t len = seg_len(r);
+        const T* wb = buf + warp * WSEG;
+        const int64_t wl = len - (int64_t)warp * WSEG;  // valid elements in this warp's slice
         uint32_t cnt = 0;
-        if (len == SEG) {
-#pragma unroll
-            for (int k = 0; k < SEG / (kQBlock * VN); ++k) {
-                const V x = reinterpret_cast<const V*>(buf)[k * kQBlock + tid];
-#pragma unroll
-                for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x, cc), thr) ? 1u : 0u;
-            }
+        if (wl >= WSEG) {
+#pragma unroll 8
+            for (int q = 0; q < CH; ++q) cnt += __popc(__ballot_sync(0xffffffffu, pred<OP>(wb[q * 32 + lane], thr)));
         } else {
-            for (int64_t e = tid; e < len; e += kQBlock) cnt += pred<OP>(buf[e], thr) ? 1u : 0u;
+            for (int q = 0; q < CH; ++q) {
+                const int e = q * 32 + lane;
+                cnt += __popc(__ballot_sync(0xffffffffu, e < wl && pred<OP>(wb[e], thr)));
+            }
         }
-#pragma unroll
-        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-        if (lane == 0) s_cnt[warp] = cnt;
+        if (lane == 0) s_wcnt[r & 1][warp] = cnt;
         __syncthreads();
         if (tid == 0) {
             uint32_t t = 0;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) t += s_cnt[w];
+            for (int w = 0; w < NW; ++w) t += s_wcnt[r & 1][w];
             st_relaxed(&ws->status[r * G + c], pack_status(epoch, kFlagAgg, t));
         }
     };
@@ -440,76 +441,35 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
             }
         }
         __syncthreads();
-        int64_t off = base_off + s_red[NW];
-        const int64_t round_total = s_tot[NW];
-        // ---- write(r) from the smem segment.  Thread t owns the contiguous
-        // elements [t*E, t*E + E) of each sub-tile (E = 12: 48 B per thread,
-        // conflict-free 128-bit smem reads), so input order = thread order and
-        // one 32-bit block scan of per-thread counts ranks every survivor.
-        constexpr int E = SUB / kQBlock;
-        constexpr int NV = E / VN;
-        const T* buf = segs + (size_t)(r % kTStages) * SEG;
-        const int64_t len = seg_len(r);
-        for (int j = 0; j * SUB < len; ++j) {
-            const T* sb = buf + j * SUB;
-            const int64_t sl = len - (int64_t)j * SUB;
-            T v[E];
+        // ---- write(r): every warp compacts its own slice, in order, with
+        // ballots; its start is the CTA offset plus the lower warps' counts.
+        // Consecutive survivors go to consecutive addresses (coalesced).
+        uint32_t wc = lane < NW && lane < warp ? s_wcnt[r & 1][lane] : 0u;
 #pragma unroll
-            for (int q = 0; q < NV; ++q) {
-                const V x = reinterpret_cast<const V*>(sb)[tid * NV + q];
-#pragma unroll
-                for (int cc = 0; cc < VN; ++cc) v[q * VN + cc] = vget<V, T>(x, cc);
+        for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
+        int64_t off = base_off + s_red[NW] + wc;
+        const T* wb = segs + (size_t)(r % kTStages) * SEG + warp * WSEG;
+        const int64_t wl = seg_len(r) - (int64_t)warp * WSEG;
+        if (wl >= WSEG) {
+#pragma unroll 4
+            for (int q = 0; q < CH; ++q) {
+                const T v = wb[q * 32 + lane];
+                const bool p = pred<OP>(v, thr);
+                const unsigned b = __ballot_sync(0xffffffffu, p);
+                if (p) out[off + __popc(b & lt_mask)] = v;
+                off += __popc(b);
             }
-            uint32_t bits = 0;
-            const int e0 = tid * E;
-            if (sl >= SUB) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) bits |= (uint32_t)pred<OP>(v[e], thr) << e;
-            } else {
-#pragma unroll
-                for (int e = 0; e < E; ++e) bits |= (uint32_t)(e0 + e < sl && pred<OP>(v[e], thr)) << e;
+        } else {
+            for (int q = 0; q < CH; ++q) {
+                const int e = q * 32 + lane;
+                const T v = e < wl ? wb[e] : T(0);
+                const bool p = e < wl && pred<OP>(v, thr);
+                const unsigned b = __ballot_sync(0xffffffffu, p);
+                if (p) out[off + __popc(b & lt_mask)] = v;
+                off += __popc(b);
             }
-            const uint32_t cnt = __popc(bits);
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += o;
-            }
-            __syncthreads();  // previous drain / s_wsum reads done
-            if (lane == 31) s_wsum[warp] = incl;
-            __syncthreads();
-            uint32_t wt = lane < NW ? s_wsum[lane] : 0;
-#pragma unroll
-            for (int d = 1; d < NW; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, wt, d);
-                if (lane >= d) wt += o;
-            }
-            const uint32_t wprev = __shfl_sync(0xffffffffu, wt, (warp + 31) & 31);
-            const uint32_t agg = __shfl_sync(0xffffffffu, wt, NW - 1);
-            const uint32_t sh0 = (uint32_t)(off & (VN - 1));
-            uint32_t rr = sh0 + (warp ? wprev : 0u) + incl - cnt;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const bool p = (bits >> e) & 1u;
-                if (p) s_stage[rr] = v[e];
-                rr += p;
-            }
-            __syncthreads();
-            const uint32_t head = min(agg, (uint32_t)((VN - sh0) & (VN - 1)));
-            if (tid < head) out[off + tid] = s_stage[sh0 + tid];
-            const uint32_t nv = (agg - head) / VN;
-            const V* sv = reinterpret_cast<const V*>(s_stage + sh0 + head);
-            V* gv = reinterpret_cast<V*>(out + off + head);
-            if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-                for (uint32_t q = tid; q < nv; q += kQBlock) gv[q] = sv[q];
-                for (uint32_t x = head + nv * VN + tid; x < agg; x += kQBlock) out[off + x] = s_stage[sh0 + x];
-            } else {
-                for (uint32_t x = head + tid; x < agg; x += kQBlock) out[off + x] = s_stage[sh0 + x];
-            }
-            off += agg;
         }
-        base_off += round_total;
+        base_off += s_tot[NW];
         __syncthreads();  // segment r's buffer is free
         if (tid == 0 && r + kTStages < rounds) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
