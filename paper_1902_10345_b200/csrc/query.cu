@@ -331,9 +331,11 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
                  uint32_t epoch) {
     constexpr int SEG = tseg_elems<T>();
     constexpr int NW = kQBlock / 32;
+    using V = typename Vec16<T>::type;
+    constexpr int VN = Vec16<T>::n;
     constexpr int WSEG = SEG / NW;   // contiguous elements per warp per segment
-    constexpr int CH = WSEG / 32;    // 32-element chunks per warp
-    static_assert(SEG % (NW * 32) == 0, "segment geometry");
+    constexpr int CV = WSEG / (32 * VN);  // 16 B vectors per lane per segment
+    static_assert(WSEG % (32 * VN) == 0, "segment geometry");
 
     extern __shared__ __align__(1024) uint8_t q_smem[];
     T* segs = reinterpret_cast<T*>(q_smem);
@@ -368,21 +370,25 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         }
         return buf;
     };
-    // warp-level count of this warp's contiguous slice; CTA total published
+    // warp-level count of this warp's contiguous slice (lane-local counts,
+    // one warp reduction: no per-element POPC on the XU pipe); CTA total published
     auto count_seg = [&](int64_t r, const T* buf) {
         const int64_t len = seg_len(r);
         const T* wb = buf + warp * WSEG;
         const int64_t wl = len - (int64_t)warp * WSEG;  // valid elements in this warp's slice
         uint32_t cnt = 0;
         if (wl >= WSEG) {
-#pragma unroll 8
-            for (int q = 0; q < CH; ++q) cnt += __popc(__ballot_sync(0xffffffffu, pred<OP>(wb[q * 32 + lane], thr)));
-        } else {
-            for (int q = 0; q < CH; ++q) {
-                const int e = q * 32 + lane;
-                cnt += __popc(__ballot_sync(0xffffffffu, e < wl && pred<OP>(wb[e], thr)));
+#pragma unroll
+            for (int q = 0; q < CV; ++q) {
+                const V x = reinterpret_cast<const V*>(wb)[q * 32 + lane];
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x, cc), thr) ? 1u : 0u;
             }
+        } else {
+            for (int e = lane; e < wl; e += 32) cnt += pred<OP>(wb[e], thr) ? 1u : 0u;
         }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
         if (lane == 0) s_wcnt[r & 1][warp] = cnt;
         __syncthreads();
         if (tid == 0) {
@@ -451,21 +457,39 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         const T* wb = segs + (size_t)(r % kTStages) * SEG + warp * WSEG;
         const int64_t wl = seg_len(r) - (int64_t)warp * WSEG;
         if (wl >= WSEG) {
-#pragma unroll 4
-            for (int q = 0; q < CH; ++q) {
-                const T v = wb[q * 32 + lane];
-                const bool p = pred<OP>(v, thr);
-                const unsigned b = __ballot_sync(0xffffffffu, p);
-                if (p) out[off + __popc(b & lt_mask)] = v;
-                off += __popc(b);
+            // lane l holds elements 4l..4l+3 (float) of each 128-element chunk:
+            // exclusive scan of per-lane counts ranks them in input order
+#pragma unroll 2
+            for (int q = 0; q < CV; ++q) {
+                const V x = reinterpret_cast<const V*>(wb)[q * 32 + lane];
+                bool p[VN];
+                uint32_t k = 0;
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) {
+                    p[cc] = pred<OP>(vget<V, T>(x, cc), thr);
+                    k += p[cc];
+                }
+                uint32_t incl = k;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += o;
+                }
+                T* dst = out + off + (incl - k);
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) {
+                    if (p[cc]) *dst = vget<V, T>(x, cc);
+                    dst += p[cc];
+                }
+                off += __shfl_sync(0xffffffffu, incl, 31);
             }
         } else {
-            for (int q = 0; q < CH; ++q) {
+            for (int q = 0; q * 32 < wl; ++q) {
                 const int e = q * 32 + lane;
                 const T v = e < wl ? wb[e] : T(0);
-                const bool p = e < wl && pred<OP>(v, thr);
-                const unsigned b = __ballot_sync(0xffffffffu, p);
-                if (p) out[off + __popc(b & lt_mask)] = v;
+                const bool pp = e < wl && pred<OP>(v, thr);
+                const unsigned b = __ballot_sync(0xffffffffu, pp);
+                if (pp) out[off + __popc(b & lt_mask)] = v;
                 off += __popc(b);
             }
         }
