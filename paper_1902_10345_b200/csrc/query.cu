@@ -303,7 +303,8 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
 //             warps' counts -- no block barrier inside;  bulk-load round r+3
 //             into the buffer round r just released.
 // The column is read from HBM exactly once and never re-read from L2.
-constexpr int kTSegBytes = 48 * 1024;
+constexpr int kTSegBytes = 64 * 1024;
+constexpr int kTBlock = 1024;  // 32 warps: the write pass is latency-bound, so more warps
 constexpr int kTStages = 3;
 constexpr int kTVec = 3;  // 16 B vectors per thread per write sub-tile (12 floats / 6 doubles)
 
@@ -325,12 +326,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <typename T, int OP>
-__global__ void __launch_bounds__(kQBlock, 1)
+__global__ void __launch_bounds__(kTBlock, 1)
 query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
                  unsigned long long* __restrict__ count, QueryWs* __restrict__ ws, int64_t rounds,
                  uint32_t epoch) {
     constexpr int SEG = tseg_elems<T>();
-    constexpr int NW = kQBlock / 32;
+    constexpr int NW = kTBlock / 32;
     using V = typename Vec16<T>::type;
     constexpr int VN = Vec16<T>::n;
     constexpr int WSEG = SEG / NW;   // contiguous elements per warp per segment
@@ -610,11 +611,11 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
             attr[sizeof(T) == 8][kop] = true;
         }
         const int64_t segs = (n + tseg_elems<T>() - 1) / tseg_elems<T>();
-        const int64_t G = std::max<int64_t>(1, std::min<int64_t>({segs, (int64_t)num_sms(), (int64_t)kQBlock}));
+        const int64_t G = std::max<int64_t>(1, std::min<int64_t>({segs, (int64_t)num_sms(), (int64_t)kTBlock}));
         const int64_t rounds = (segs + G - 1) / G;
         void* args[] = {(void*)&col, (void*)&n, (void*)&tt, (void*)&out, (void*)&C, (void*)&W,
                         (void*)&rounds, (void*)&epoch};
-        SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)tk, dim3((unsigned)G), dim3(kQBlock), args,
+        SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)tk, dim3((unsigned)G), dim3(kTBlock), args,
                                                tma_query_smem<T>(), s));
         return SDFGB_OK;
     }
@@ -641,7 +642,7 @@ extern "C" size_t sdfgb_query_workspace_bytes(int64_t n, int elem_bytes) {
         elem_bytes == 8 ? sdfgb::seg_elems<double>() : sdfgb::seg_elems<float>(),
         elem_bytes == 8 ? sdfgb::tseg_elems<double>() : sdfgb::tseg_elems<float>());
     const int64_t segs = (n + seg - 1) / seg;
-    return offsetof(sdfgb::QueryWs, status) + (size_t)(segs + sdfgb::kQBlock) * 8;
+    return offsetof(sdfgb::QueryWs, status) + (size_t)(segs + sdfgb::kTBlock) * 8;
 }
 extern "C" int sdfgb_query_f32(const float* col, int64_t n, int op, double thr, float* out_vals,
                                int64_t* count, void* ws, size_t ws_bytes, void* stream) {
