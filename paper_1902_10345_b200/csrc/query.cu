@@ -330,23 +330,23 @@ __global__ void __launch_bounds__(kTBlock, 1)
 query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
                  unsigned long long* __restrict__ count, QueryWs* __restrict__ ws, int64_t rounds,
                  uint32_t epoch) {
-    constexpr int SEG = tseg_elems<T>();
-    constexpr int NW = kTBlock / 32;
     using V = typename Vec16<T>::type;
     constexpr int VN = Vec16<T>::n;
-    constexpr int WSEG = SEG / NW;   // contiguous elements per warp per segment
-    constexpr int CV = WSEG / (32 * VN);  // 16 B vectors per lane per segment
-    static_assert(WSEG % (32 * VN) == 0, "segment geometry");
+    constexpr int SEG = tseg_elems<T>();
+    constexpr int NW = kTBlock / 32;
+    constexpr int WSEG = SEG / NW;        // contiguous elements per warp per segment
+    constexpr int CV = WSEG / (32 * VN);  // 16 B vectors per lane per segment (one per 32*VN chunk)
+    static_assert(WSEG % (32 * VN) == 0 && CV * VN <= 32 && CV <= 4, "segment geometry");
 
     extern __shared__ __align__(1024) uint8_t q_smem[];
     T* segs = reinterpret_cast<T*>(q_smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(q_smem + kTStages * kTSegBytes);
-    __shared__ int64_t s_red[NW + 1], s_tot[NW + 1];
+    __shared__ uint32_t s_red[NW + 1], s_tot[NW + 1];
     __shared__ uint32_t s_wcnt[2][NW];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned lt_mask = (1u << lane) - 1u;
     const int64_t G = gridDim.x, c = blockIdx.x;
+    const int GW = (int)((G + 31) / 32);  // warps that gather the round's counts
 
     auto seg_len = [&](int64_t r) -> int64_t {
         const int64_t start = (r * G + c) * (int64_t)SEG;
@@ -359,7 +359,7 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         mbar_expect_tx(&bars[b], bytes);
         if (bytes) bulk_g2s(segs + (size_t)b * SEG, col + (r * G + c) * (int64_t)SEG, bytes, &bars[b]);
     };
-    auto wait = [&](int64_t r) -> const T* {
+    auto wait = [&](int64_t r) {
         const int b = (int)(r % kTStages);
         mbar_wait(&bars[b], (uint32_t)((r / kTStages) & 1));
         T* buf = segs + (size_t)b * SEG;
@@ -369,25 +369,31 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
             if (tid < len - done) buf[done + tid] = col[(r * G + c) * (int64_t)SEG + done + tid];
             __syncthreads();
         }
-        return buf;
     };
-    // warp-level count of this warp's contiguous slice (lane-local counts,
-    // one warp reduction: no per-element POPC on the XU pipe); CTA total published
-    auto count_seg = [&](int64_t r, const T* buf) {
-        const int64_t len = seg_len(r);
-        const T* wb = buf + warp * WSEG;
-        const int64_t wl = len - (int64_t)warp * WSEG;  // valid elements in this warp's slice
-        uint32_t cnt = 0;
-        if (wl >= WSEG) {
+    // Count this warp's slice and keep, per lane, the predicate bits (bit
+    // q*VN + cc) and the per-chunk counts packed in bytes: the write pass
+    // reuses both instead of re-evaluating the predicate.
+    auto count_seg = [&](int64_t r, uint32_t& bits, uint32_t& packed) {
+        const T* wb = segs + (size_t)(r % kTStages) * SEG + warp * WSEG;
+        const int64_t wl = seg_len(r) - (int64_t)warp * WSEG;  // valid elements in this warp's slice
+        bits = 0;
+        packed = 0;
 #pragma unroll
-            for (int q = 0; q < CV; ++q) {
-                const V x = reinterpret_cast<const V*>(wb)[q * 32 + lane];
+        for (int q = 0; q < CV; ++q) {
+            const V x = reinterpret_cast<const V*>(wb)[q * 32 + lane];
+            uint32_t k = 0;
 #pragma unroll
-                for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x, cc), thr) ? 1u : 0u;
+            for (int cc = 0; cc < VN; ++cc) {
+                const int e = (q * 32 + lane) * VN + cc;
+                const bool p = (wl >= WSEG || e < wl) && pred<OP>(vget<V, T>(x, cc), thr);
+                bits |= (uint32_t)p << (q * VN + cc);
+                k += p;
             }
-        } else {
-            for (int e = lane; e < wl; e += 32) cnt += pred<OP>(wb[e], thr) ? 1u : 0u;
+            packed |= k << (8 * q);
         }
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int q = 0; q < CV; ++q) cnt += (packed >> (8 * q)) & 0xffu;
 #pragma unroll
         for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
         if (lane == 0) s_wcnt[r & 1][warp] = cnt;
@@ -407,36 +413,44 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         for (int64_t r = 0; r < kTStages && r < rounds; ++r) issue(r);
     }
     __syncthreads();
-    count_seg(0, wait(0));
+    uint32_t nbits, npacked;
+    wait(0);
+    count_seg(0, nbits, npacked);
 
     int64_t base_off = 0;
     for (int64_t r = 0; r < rounds; ++r) {
-        if (r + 1 < rounds) count_seg(r + 1, wait(r + 1));
-        // ---- all-gather of round r's counts (thread q reads CTA q's word);
-        // warp 0 folds the per-warp sums so each thread reads two values
-        int64_t val = 0;
-        if (tid < G) {
-            uint64_t w;
-            while (true) {
-                w = ld_relaxed(&ws->status[r * G + tid]);
-                if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
-                __nanosleep(16);
+        const uint32_t bits = nbits, packed = npacked;
+        if (r + 1 < rounds) {
+            wait(r + 1);
+            count_seg(r + 1, nbits, npacked);
+        }
+        // ---- all-gather of round r's counts: warps [0, GW) read one word per
+        // lane (segment counts fit 32 bits), warp 0 folds
+        if (warp < GW) {
+            uint32_t val = 0;
+            if (tid < G) {
+                uint64_t w;
+                while (true) {
+                    w = ld_relaxed(&ws->status[r * G + tid]);
+                    if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
+                    __nanosleep(16);
+                }
+                val = (uint32_t)(w & kValueMask);
             }
-            val = (int64_t)(w & kValueMask);
-        }
-        int64_t lower = tid < c ? val : 0;
+            uint32_t lower = tid < c ? val : 0u;
 #pragma unroll
-        for (int d = 16; d; d >>= 1) {
-            lower += __shfl_xor_sync(0xffffffffu, lower, d);
-            val += __shfl_xor_sync(0xffffffffu, val, d);
-        }
-        if (lane == 0) {
-            s_red[warp] = lower;
-            s_tot[warp] = val;
+            for (int d = 16; d; d >>= 1) {
+                lower += __shfl_xor_sync(0xffffffffu, lower, d);
+                val += __shfl_xor_sync(0xffffffffu, val, d);
+            }
+            if (lane == 0) {
+                s_red[warp] = lower;
+                s_tot[warp] = val;
+            }
         }
         __syncthreads();
         if (warp == 0) {
-            int64_t lo = lane < NW ? s_red[lane] : 0, to = lane < NW ? s_tot[lane] : 0;
+            uint32_t lo = lane < GW ? s_red[lane] : 0u, to = lane < GW ? s_tot[lane] : 0u;
 #pragma unroll
             for (int d = 16; d; d >>= 1) {
                 lo += __shfl_xor_sync(0xffffffffu, lo, d);
@@ -448,51 +462,33 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
             }
         }
         __syncthreads();
-        // ---- write(r): every warp compacts its own slice, in order, with
-        // ballots; its start is the CTA offset plus the lower warps' counts.
-        // Consecutive survivors go to consecutive addresses (coalesced).
-        uint32_t wc = lane < NW && lane < warp ? s_wcnt[r & 1][lane] : 0u;
+        // ---- write(r): each warp compacts its slice in order.  One 32-bit
+        // shuffle scan of the byte-packed per-chunk counts ranks all CV chunks.
+        uint32_t wc = lane < warp ? s_wcnt[r & 1][lane] : 0u;
 #pragma unroll
         for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
-        int64_t off = base_off + s_red[NW] + wc;
+        uint32_t incl = packed;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - packed;
+        T* wout = out + (base_off + (int64_t)s_red[NW] + wc);
         const T* wb = segs + (size_t)(r % kTStages) * SEG + warp * WSEG;
-        const int64_t wl = seg_len(r) - (int64_t)warp * WSEG;
-        if (wl >= WSEG) {
-            // lane l holds elements 4l..4l+3 (float) of each 128-element chunk:
-            // exclusive scan of per-lane counts ranks them in input order
-#pragma unroll 2
-            for (int q = 0; q < CV; ++q) {
-                const V x = reinterpret_cast<const V*>(wb)[q * 32 + lane];
-                bool p[VN];
-                uint32_t k = 0;
+        uint32_t run = 0;  // survivors of this warp's earlier chunks
 #pragma unroll
-                for (int cc = 0; cc < VN; ++cc) {
-                    p[cc] = pred<OP>(vget<V, T>(x, cc), thr);
-                    k += p[cc];
-                }
-                uint32_t incl = k;
+        for (int q = 0; q < CV; ++q) {
+            const V x = reinterpret_cast<const V*>(wb)[q * 32 + lane];
+            uint32_t at = run + ((excl >> (8 * q)) & 0xffu);
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (lane >= d) incl += o;
-                }
-                T* dst = out + off + (incl - k);
-#pragma unroll
-                for (int cc = 0; cc < VN; ++cc) {
-                    if (p[cc]) *dst = vget<V, T>(x, cc);
-                    dst += p[cc];
-                }
-                off += __shfl_sync(0xffffffffu, incl, 31);
+            for (int cc = 0; cc < VN; ++cc) {
+                const bool p = (bits >> (q * VN + cc)) & 1u;
+                if (p) wout[at] = vget<V, T>(x, cc);
+                at += p;
             }
-        } else {
-            for (int q = 0; q * 32 < wl; ++q) {
-                const int e = q * 32 + lane;
-                const T v = e < wl ? wb[e] : T(0);
-                const bool pp = e < wl && pred<OP>(v, thr);
-                const unsigned b = __ballot_sync(0xffffffffu, pp);
-                if (pp) out[off + __popc(b & lt_mask)] = v;
-                off += __popc(b);
-            }
+            run += (tot >> (8 * q)) & 0xffu;
         }
         base_off += s_tot[NW];
         __syncthreads();  // segment r's buffer is free
