@@ -373,23 +373,38 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
     // Count this warp's slice and keep, per lane, the predicate bits (bit
     // q*VN + cc) and the per-chunk counts packed in bytes: the write pass
     // reuses both instead of re-evaluating the predicate.
+    // valid elements of this warp's slice, clamped to [0, WSEG] (32-bit)
+    auto warp_len = [&](int64_t r) -> int {
+        const int64_t wl = seg_len(r) - (int64_t)warp * WSEG;
+        return wl <= 0 ? 0 : (wl >= WSEG ? WSEG : (int)wl);
+    };
     auto count_seg = [&](int64_t r, uint32_t& bits, uint32_t& packed) {
-        const T* wb = segs + (size_t)(r % kTStages) * SEG + warp * WSEG;
-        const int64_t wl = seg_len(r) - (int64_t)warp * WSEG;  // valid elements in this warp's slice
+        const V* wv = reinterpret_cast<const V*>(segs + (size_t)(r % kTStages) * SEG + warp * WSEG) + lane;
+        const int wl = warp_len(r);
         bits = 0;
         packed = 0;
+        if (wl == WSEG) {
 #pragma unroll
-        for (int q = 0; q < CV; ++q) {
-            const V x = reinterpret_cast<const V*>(wb)[q * 32 + lane];
-            uint32_t k = 0;
+            for (int q = 0; q < CV; ++q) {
+                const V x = wv[q * 32];
+                uint32_t m = 0;
 #pragma unroll
-            for (int cc = 0; cc < VN; ++cc) {
-                const int e = (q * 32 + lane) * VN + cc;
-                const bool p = (wl >= WSEG || e < wl) && pred<OP>(vget<V, T>(x, cc), thr);
-                bits |= (uint32_t)p << (q * VN + cc);
-                k += p;
+                for (int cc = 0; cc < VN; ++cc) m |= (uint32_t)pred<OP>(vget<V, T>(x, cc), thr) << cc;
+                bits |= m << (q * VN);
+                packed |= (uint32_t)__popc(m) << (8 * q);
             }
-            packed |= k << (8 * q);
+        } else {
+            for (int q = 0; q < CV; ++q) {
+                const V x = wv[q * 32];
+                uint32_t m = 0;
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) {
+                    const int e = (q * 32 + lane) * VN + cc;
+                    m |= (uint32_t)(e < wl && pred<OP>(vget<V, T>(x, cc), thr)) << cc;
+                }
+                bits |= m << (q * VN);
+                packed |= (uint32_t)__popc(m) << (8 * q);
+            }
         }
         uint32_t cnt = 0;
 #pragma unroll
@@ -476,15 +491,15 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t excl = incl - packed;
         T* wout = out + (base_off + (int64_t)s_red[NW] + wc);
-        const T* wb = segs + (size_t)(r % kTStages) * SEG + warp * WSEG;
+        const V* wv = reinterpret_cast<const V*>(segs + (size_t)(r % kTStages) * SEG + warp * WSEG) + lane;
         uint32_t run = 0;  // survivors of this warp's earlier chunks
 #pragma unroll
         for (int q = 0; q < CV; ++q) {
-            const V x = reinterpret_cast<const V*>(wb)[q * 32 + lane];
+            const V x = wv[q * 32];
             uint32_t at = run + ((excl >> (8 * q)) & 0xffu);
 #pragma unroll
             for (int cc = 0; cc < VN; ++cc) {
-                const bool p = (bits >> (q * VN + cc)) & 1u;
+                const uint32_t p = (bits >> (q * VN + cc)) & 1u;
                 if (p) wout[at] = vget<V, T>(x, cc);
                 at += p;
             }
