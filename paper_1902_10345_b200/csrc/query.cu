@@ -317,6 +317,20 @@ __host__ __device__ constexpr size_t tma_query_smem() {
     return (size_t)kTStages * kTSegBytes + 64;
 }
 
+// predicated store of v to base[idx] with a single 32x32+64 address op
+__device__ __forceinline__ void st_pred(float* base, uint32_t idx, float v, uint32_t p) {
+    asm volatile(
+        "{\n .reg .pred q;\n .reg .u64 a;\n setp.ne.u32 q, %3, 0;\n mad.wide.u32 a, %0, 4, %1;\n"
+        " @q st.global.f32 [a], %2;\n}" ::"r"(idx), "l"(base), "f"(v), "r"(p)
+        : "memory");
+}
+__device__ __forceinline__ void st_pred(double* base, uint32_t idx, double v, uint32_t p) {
+    asm volatile(
+        "{\n .reg .pred q;\n .reg .u64 a;\n setp.ne.u32 q, %3, 0;\n mad.wide.u32 a, %0, 8, %1;\n"
+        " @q st.global.f64 [a], %2;\n}" ::"r"(idx), "l"(base), "d"(v), "r"(p)
+        : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -500,7 +514,7 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
 #pragma unroll
             for (int cc = 0; cc < VN; ++cc) {
                 const uint32_t p = (bits >> (q * VN + cc)) & 1u;
-                if (p) wout[at] = vget<V, T>(x, cc);
+                st_pred(wout, at, vget<V, T>(x, cc), p);
                 at += p;
             }
             run += (tot >> (8 * q)) & 0xffu;
