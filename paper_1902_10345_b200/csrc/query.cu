@@ -356,11 +356,11 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
     T* segs = reinterpret_cast<T*>(q_smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(q_smem + kTStages * kTSegBytes);
     __shared__ uint32_t s_red[NW + 1], s_tot[NW + 1];
-    __shared__ uint32_t s_wcnt[2][NW];
+    __shared__ uint32_t s_wcnt[3][NW];
+    __shared__ uint32_t s_csum[3], s_cdone[3];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
-    const int GW = (int)((G + 31) / 32);  // warps that gather the round's counts
 
     auto seg_len = [&](int64_t r) -> int64_t {
         const int64_t start = (r * G + c) * (int64_t)SEG;
@@ -425,13 +425,19 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         for (int q = 0; q < CV; ++q) cnt += (packed >> (8 * q)) & 0xffu;
 #pragma unroll
         for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-        if (lane == 0) s_wcnt[r & 1][warp] = cnt;
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t t = 0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) t += s_wcnt[r & 1][w];
-            st_relaxed(&ws->status[r * G + c], pack_status(epoch, kFlagAgg, t));
+        // no block barrier: the last warp to add its count publishes the CTA total
+        if (lane == 0) {
+            const int sl = (int)(r % 3);
+            s_wcnt[sl][warp] = cnt;
+            atomicAdd(&s_csum[sl], cnt);
+            __threadfence_block();
+            if (atomicAdd(&s_cdone[sl], 1u) == NW - 1) {
+                __threadfence_block();
+                const uint32_t t = atomicAdd(&s_csum[sl], 0u);
+                st_relaxed(&ws->status[r * G + c], pack_status(epoch, kFlagAgg, t));
+                s_csum[sl] = 0;
+                s_cdone[sl] = 0;
+            }
         }
     };
 
@@ -441,59 +447,45 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         for (int64_t r = 0; r < kTStages && r < rounds; ++r) issue(r);
     }
-    __syncthreads();
-    uint32_t nbits, npacked;
+    uint32_t nbits = 0, npacked = 0;
     wait(0);
     count_seg(0, nbits, npacked);
 
     int64_t base_off = 0;
     for (int64_t r = 0; r < rounds; ++r) {
         const uint32_t bits = nbits, packed = npacked;
-        if (r + 1 < rounds) {
+        if (r + 1 < rounds) {  // count one round ahead (its data landed two rounds ago)
             wait(r + 1);
             count_seg(r + 1, nbits, npacked);
         }
-        // ---- all-gather of round r's counts: warps [0, GW) read one word per
-        // lane (segment counts fit 32 bits), warp 0 folds
-        if (warp < GW) {
-            uint32_t val = 0;
-            if (tid < G) {
+        // ---- all-gather of round r's counts by warp 0 (published a round ago)
+        if (warp == 0) {
+            uint32_t lower = 0, total = 0;
+            for (int64_t q = lane; q < G; q += 32) {
                 uint64_t w;
                 while (true) {
-                    w = ld_relaxed(&ws->status[r * G + tid]);
+                    w = ld_relaxed(&ws->status[r * G + q]);
                     if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
                     __nanosleep(16);
                 }
-                val = (uint32_t)(w & kValueMask);
+                const uint32_t v = (uint32_t)(w & kValueMask);
+                total += v;
+                lower += q < c ? v : 0u;
             }
-            uint32_t lower = tid < c ? val : 0u;
 #pragma unroll
             for (int d = 16; d; d >>= 1) {
                 lower += __shfl_xor_sync(0xffffffffu, lower, d);
-                val += __shfl_xor_sync(0xffffffffu, val, d);
+                total += __shfl_xor_sync(0xffffffffu, total, d);
             }
             if (lane == 0) {
-                s_red[warp] = lower;
-                s_tot[warp] = val;
-            }
-        }
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t lo = lane < GW ? s_red[lane] : 0u, to = lane < GW ? s_tot[lane] : 0u;
-#pragma unroll
-            for (int d = 16; d; d >>= 1) {
-                lo += __shfl_xor_sync(0xffffffffu, lo, d);
-                to += __shfl_xor_sync(0xffffffffu, to, d);
-            }
-            if (lane == 0) {
-                s_red[NW] = lo;
-                s_tot[NW] = to;
+                s_red[NW] = lower;
+                s_tot[NW] = total;
             }
         }
         __syncthreads();
         // ---- write(r): each warp compacts its slice in order.  One 32-bit
         // shuffle scan of the byte-packed per-chunk counts ranks all CV chunks.
-        uint32_t wc = lane < warp ? s_wcnt[r & 1][lane] : 0u;
+        uint32_t wc = lane < warp ? s_wcnt[r % 3][lane] : 0u;
 #pragma unroll
         for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
         uint32_t incl = packed;
