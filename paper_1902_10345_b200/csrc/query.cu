@@ -447,6 +447,8 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         for (int64_t r = 0; r < kTStages && r < rounds; ++r) issue(r);
     }
+    if (tid < 3) s_csum[tid] = s_cdone[tid] = 0;
+    __syncthreads();  // barriers initialised, counters cleared
     uint32_t nbits = 0, npacked = 0;
     wait(0);
     count_seg(0, nbits, npacked);
