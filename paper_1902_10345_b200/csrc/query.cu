@@ -303,9 +303,9 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
 //             warps' counts -- no block barrier inside;  bulk-load round r+3
 //             into the buffer round r just released.
 // The column is read from HBM exactly once and never re-read from L2.
-constexpr int kTSegBytes = 64 * 1024;
+constexpr int kTSegBytes = 48 * 1024;
 constexpr int kTBlock = 1024;  // 32 warps: the write pass is latency-bound, so more warps
-constexpr int kTStages = 3;
+constexpr int kTStages = 4;
 constexpr int kTVec = 3;  // 16 B vectors per thread per write sub-tile (12 floats / 6 doubles)
 
 template <typename T>
@@ -356,8 +356,8 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
     T* segs = reinterpret_cast<T*>(q_smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(q_smem + kTStages * kTSegBytes);
     __shared__ uint32_t s_red[NW + 1], s_tot[NW + 1];
-    __shared__ uint32_t s_wcnt[3][NW];
-    __shared__ uint32_t s_csum[3], s_cdone[3];
+    __shared__ uint32_t s_wcnt[4][NW];
+    __shared__ uint32_t s_csum[4], s_cdone[4];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
@@ -427,7 +427,7 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
         // no block barrier: the last warp to add its count publishes the CTA total
         if (lane == 0) {
-            const int sl = (int)(r % 3);
+            const int sl = (int)(r % 4);
             s_wcnt[sl][warp] = cnt;
             atomicAdd(&s_csum[sl], cnt);
             __threadfence_block();
@@ -447,18 +447,26 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         for (int64_t r = 0; r < kTStages && r < rounds; ++r) issue(r);
     }
-    if (tid < 3) s_csum[tid] = s_cdone[tid] = 0;
+    if (tid < 4) s_csum[tid] = s_cdone[tid] = 0;
     __syncthreads();  // barriers initialised, counters cleared
-    uint32_t nbits = 0, npacked = 0;
+    // counts run two rounds ahead of the writes (4-stage ring), so the
+    // all-gather of round r reads counts published two iterations earlier
+    uint32_t b0 = 0, p0 = 0, b1 = 0, p1 = 0;
     wait(0);
-    count_seg(0, nbits, npacked);
+    count_seg(0, b0, p0);
+    if (rounds > 1) {
+        wait(1);
+        count_seg(1, b1, p1);
+    }
 
     int64_t base_off = 0;
     for (int64_t r = 0; r < rounds; ++r) {
-        const uint32_t bits = nbits, packed = npacked;
-        if (r + 1 < rounds) {  // count one round ahead (its data landed two rounds ago)
-            wait(r + 1);
-            count_seg(r + 1, nbits, npacked);
+        const uint32_t bits = b0, packed = p0;
+        b0 = b1;
+        p0 = p1;
+        if (r + 2 < rounds) {  // its data was issued two iterations ago
+            wait(r + 2);
+            count_seg(r + 2, b1, p1);
         }
         // ---- all-gather of round r's counts by warp 0 (published a round ago)
         if (warp == 0) {
@@ -487,7 +495,7 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         __syncthreads();
         // ---- write(r): each warp compacts its slice in order.  One 32-bit
         // shuffle scan of the byte-packed per-chunk counts ranks all CV chunks.
-        uint32_t wc = lane < warp ? s_wcnt[r % 3][lane] : 0u;
+        uint32_t wc = lane < warp ? s_wcnt[r % 4][lane] : 0u;
 #pragma unroll
         for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
         uint32_t incl = packed;
