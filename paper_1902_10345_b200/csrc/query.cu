@@ -303,9 +303,9 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
 //             warps' counts -- no block barrier inside;  bulk-load round r+3
 //             into the buffer round r just released.
 // The column is read from HBM exactly once and never re-read from L2.
-constexpr int kTSegBytes = 48 * 1024;
+constexpr int kTSegBytes = 64 * 1024;
 constexpr int kTBlock = 1024;  // 32 warps: the write pass is latency-bound, so more warps
-constexpr int kTStages = 4;
+constexpr int kTStages = 3;
 constexpr int kTVec = 3;  // 16 B vectors per thread per write sub-tile (12 floats / 6 doubles)
 
 template <typename T>
@@ -356,11 +356,11 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
     T* segs = reinterpret_cast<T*>(q_smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(q_smem + kTStages * kTSegBytes);
     __shared__ uint32_t s_red[NW + 1], s_tot[NW + 1];
-    __shared__ uint32_t s_wcnt[4][NW];
-    __shared__ uint32_t s_csum[4], s_cdone[4];
+    __shared__ uint32_t s_wcnt[2][NW];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
+    const int GW = (int)((G + 31) / 32);  // warps that gather the round's counts
 
     auto seg_len = [&](int64_t r) -> int64_t {
         const int64_t start = (r * G + c) * (int64_t)SEG;
@@ -425,19 +425,13 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         for (int q = 0; q < CV; ++q) cnt += (packed >> (8 * q)) & 0xffu;
 #pragma unroll
         for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-        // no block barrier: the last warp to add its count publishes the CTA total
-        if (lane == 0) {
-            const int sl = (int)(r % 4);
-            s_wcnt[sl][warp] = cnt;
-            atomicAdd(&s_csum[sl], cnt);
-            __threadfence_block();
-            if (atomicAdd(&s_cdone[sl], 1u) == NW - 1) {
-                __threadfence_block();
-                const uint32_t t = atomicAdd(&s_csum[sl], 0u);
-                st_relaxed(&ws->status[r * G + c], pack_status(epoch, kFlagAgg, t));
-                s_csum[sl] = 0;
-                s_cdone[sl] = 0;
-            }
+        if (lane == 0) s_wcnt[r & 1][warp] = cnt;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) t += s_wcnt[r & 1][w];
+            st_relaxed(&ws->status[r * G + c], pack_status(epoch, kFlagAgg, t));
         }
     };
 
@@ -447,55 +441,59 @@ query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ ou
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         for (int64_t r = 0; r < kTStages && r < rounds; ++r) issue(r);
     }
-    if (tid < 4) s_csum[tid] = s_cdone[tid] = 0;
-    __syncthreads();  // barriers initialised, counters cleared
-    // counts run two rounds ahead of the writes (4-stage ring), so the
-    // all-gather of round r reads counts published two iterations earlier
-    uint32_t b0 = 0, p0 = 0, b1 = 0, p1 = 0;
+    __syncthreads();
+    uint32_t nbits, npacked;
     wait(0);
-    count_seg(0, b0, p0);
-    if (rounds > 1) {
-        wait(1);
-        count_seg(1, b1, p1);
-    }
+    count_seg(0, nbits, npacked);
 
     int64_t base_off = 0;
     for (int64_t r = 0; r < rounds; ++r) {
-        const uint32_t bits = b0, packed = p0;
-        b0 = b1;
-        p0 = p1;
-        if (r + 2 < rounds) {  // its data was issued two iterations ago
-            wait(r + 2);
-            count_seg(r + 2, b1, p1);
+        const uint32_t bits = nbits, packed = npacked;
+        if (r + 1 < rounds) {
+            wait(r + 1);
+            count_seg(r + 1, nbits, npacked);
         }
-        // ---- all-gather of round r's counts by warp 0 (published a round ago)
-        if (warp == 0) {
-            uint32_t lower = 0, total = 0;
-            for (int64_t q = lane; q < G; q += 32) {
+        // ---- all-gather of round r's counts: warps [0, GW) read one word per
+        // lane (segment counts fit 32 bits), warp 0 folds
+        if (warp < GW) {
+            uint32_t val = 0;
+            if (tid < G) {
                 uint64_t w;
                 while (true) {
-                    w = ld_relaxed(&ws->status[r * G + q]);
+                    w = ld_relaxed(&ws->status[r * G + tid]);
                     if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
                     __nanosleep(16);
                 }
-                const uint32_t v = (uint32_t)(w & kValueMask);
-                total += v;
-                lower += q < c ? v : 0u;
+                val = (uint32_t)(w & kValueMask);
             }
+            uint32_t lower = tid < c ? val : 0u;
 #pragma unroll
             for (int d = 16; d; d >>= 1) {
                 lower += __shfl_xor_sync(0xffffffffu, lower, d);
-                total += __shfl_xor_sync(0xffffffffu, total, d);
+                val += __shfl_xor_sync(0xffffffffu, val, d);
             }
             if (lane == 0) {
-                s_red[NW] = lower;
-                s_tot[NW] = total;
+                s_red[warp] = lower;
+                s_tot[warp] = val;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t lo = lane < GW ? s_red[lane] : 0u, to = lane < GW ? s_tot[lane] : 0u;
+#pragma unroll
+            for (int d = 16; d; d >>= 1) {
+                lo += __shfl_xor_sync(0xffffffffu, lo, d);
+                to += __shfl_xor_sync(0xffffffffu, to, d);
+            }
+            if (lane == 0) {
+                s_red[NW] = lo;
+                s_tot[NW] = to;
             }
         }
         __syncthreads();
         // ---- write(r): each warp compacts its slice in order.  One 32-bit
         // shuffle scan of the byte-packed per-chunk counts ranks all CV chunks.
-        uint32_t wc = lane < warp ? s_wcnt[r % 4][lane] : 0u;
+        uint32_t wc = lane < warp ? s_wcnt[r & 1][lane] : 0u;
 #pragma unroll
         for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
         uint32_t incl = packed;
