@@ -21,7 +21,12 @@
 #include <atomic>
 #include <cmath>
 
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "tma.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sdfgb {
 namespace {
@@ -543,6 +548,167 @@ auto query_tma_kernel_for(int op) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Piece kernel (the default for 16 B-aligned columns).  The column is cut
+// into L2-sized pieces (64 MB); for each piece every co-resident CTA
+//   A  counts its contiguous chunk range warp by warp (HBM read, L2
+//      evict_last), keeping the per-warp counts in smem;
+//   -- one grid-wide barrier (cooperative groups) per piece --
+//   B  reads the G CTA counts (one block-wide load) for its offset, then
+//      every warp re-reads its slice from L2 (evict_first) and compacts it in
+//      order: per lane one 16 B vector per 32*VN-element chunk, byte-packed
+//      chunk counts, one 32-bit shuffle scan per 4 chunks, predicated stores.
+// No CTA ever polls another: the only cross-CTA synchronisation is one grid
+// barrier per 64 MB, and HBM sees each input byte once.
+constexpr int64_t kPieceBytes = 64ll << 20;
+
+template <typename T>
+__device__ __forceinline__ typename Vec16<T>::type ldg_hint(const T* p, uint64_t pol) {
+    return ldg_pol(reinterpret_cast<const typename Vec16<T>::type*>(p), pol);
+}
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(kQBlock, 2)
+query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
+                   unsigned long long* __restrict__ count, unsigned long long* __restrict__ cnts) {
+    using V = typename Vec16<T>::type;
+    constexpr int VN = Vec16<T>::n;
+    constexpr int NW = kQBlock / 32;
+    constexpr int CH = 32 * VN;  // elements per warp chunk
+    constexpr int64_t PIECE = kPieceBytes / (int64_t)sizeof(T);
+    __shared__ uint32_t s_wcnt[NW];
+    __shared__ int64_t s_lo[NW], s_to[NW];
+
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t G = gridDim.x, c = blockIdx.x;
+    const uint64_t keep = make_policy(true), drop = make_policy(false);
+    int64_t base = 0;
+    int64_t p = 0;
+    for (int64_t ps = 0; ps < n; ps += PIECE, ++p) {
+        const int64_t pl = n - ps < PIECE ? n - ps : PIECE;
+        const int64_t nch = (pl + CH - 1) / CH;
+        const int64_t per_cta = (nch + G - 1) / G;
+        const int64_t cs = c * per_cta < nch ? c * per_cta : nch;
+        const int64_t ce = cs + per_cta < nch ? cs + per_cta : nch;
+        const int64_t per_w = (ce - cs + NW - 1) / NW;
+        const int64_t w0 = cs + warp * per_w < ce ? cs + warp * per_w : ce;
+        const int64_t w1 = w0 + per_w < ce ? w0 + per_w : ce;
+        // ---- A: count this warp's chunks [w0, w1)
+        uint32_t cnt = 0;
+        for (int64_t q = w0; q < w1; ++q) {
+            const int64_t e0 = ps + q * CH + lane * VN;
+            if (e0 + VN <= n) {
+                const V x = ldg_hint(col + e0, keep);
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x, cc), thr) ? 1u : 0u;
+            } else {
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) cnt += (e0 + cc < n && pred<OP>(col[e0 + cc], thr)) ? 1u : 0u;
+            }
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+        if (lane == 0) s_wcnt[warp] = cnt;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) t += s_wcnt[w];
+            cnts[p * G + c] = t;
+        }
+        grid.sync();
+        // ---- B: this CTA's offset inside the piece, then per-warp compaction
+        int64_t lo = 0, to = 0;
+        for (int64_t q = tid; q < G; q += kQBlock) {
+            const int64_t v = (int64_t)__ldcg(cnts + p * G + q);
+            to += v;
+            lo += q < c ? v : 0;
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            lo += __shfl_xor_sync(0xffffffffu, lo, d);
+            to += __shfl_xor_sync(0xffffffffu, to, d);
+        }
+        if (lane == 0) {
+            s_lo[warp] = lo;
+            s_to[warp] = to;
+        }
+        __syncthreads();
+        int64_t cta_off = 0, piece_total = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            cta_off += s_lo[w];
+            piece_total += s_to[w];
+        }
+        uint32_t wc = lane < warp ? s_wcnt[lane] : 0u;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
+        T* wout = out + (base + cta_off + wc);
+        uint32_t run = 0;
+        for (int64_t q0 = w0; q0 < w1; q0 += 4) {
+            V x[4];
+            uint32_t bits = 0, packed = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t e0 = ps + (q0 + j) * CH + lane * VN;
+                uint32_t m = 0;
+                if (q0 + j < w1 && e0 + VN <= n) {
+                    x[j] = ldg_hint(col + e0, drop);
+#pragma unroll
+                    for (int cc = 0; cc < VN; ++cc) m |= (uint32_t)pred<OP>(vget<V, T>(x[j], cc), thr) << cc;
+                } else {
+                    T* xs = reinterpret_cast<T*>(&x[j]);
+#pragma unroll
+                    for (int cc = 0; cc < VN; ++cc) {
+                        const bool live = q0 + j < w1 && e0 + cc < n;
+                        xs[cc] = live ? col[e0 + cc] : T(0);
+                        m |= (uint32_t)(live && pred<OP>(xs[cc], thr)) << cc;
+                    }
+                }
+                bits |= m << (j * VN);
+                packed |= (uint32_t)__popc(m) << (8 * j);
+            }
+            uint32_t incl = packed;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += o;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+            const uint32_t excl = incl - packed;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t at = run + ((excl >> (8 * j)) & 0xffu);
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) {
+                    const uint32_t pp = (bits >> (j * VN + cc)) & 1u;
+                    st_pred(wout, at, vget<V, T>(x[j], cc), pp);
+                    at += pp;
+                }
+                run += (tot >> (8 * j)) & 0xffu;
+            }
+        }
+        base += piece_total;
+        __syncthreads();  // s_wcnt / s_lo reuse
+    }
+    if (c == 0 && tid == 0) atomicAdd(count, (unsigned long long)base);
+}
+
+template <typename T>
+auto query_piece_kernel_for(int op) {
+    switch (op) {
+    case 0: return query_piece_kernel<T, 0>;
+    case 1: return query_piece_kernel<T, 1>;
+    case 2: return query_piece_kernel<T, 2>;
+    case 3: return query_piece_kernel<T, 3>;
+    case 4: return query_piece_kernel<T, 4>;
+    case 5: return query_piece_kernel<T, 5>;
+    case 6: return query_piece_kernel<T, 6>;
+    default: return query_piece_kernel<T, 7>;
+    }
+}
+
 std::atomic<uint32_t> g_epoch{0};
 
 uint32_t next_epoch() {
@@ -626,6 +792,18 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
     int kop;
     T tt;
     fold_threshold<T>(op, thr, kop, tt);
+    if (vec && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && !getenv("SDFGB_QUERY_TMA")) {
+        // piece kernel: co-resident CTAs, one grid barrier per 64 MB piece
+        auto pk = query_piece_kernel_for<T>(kop);
+        static int pocc[2][8] = {};
+        int& po = pocc[sizeof(T) == 8][kop];
+        if (po == 0) SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&po, pk, kQBlock, 0));
+        const int64_t G = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(po, 1) * num_sms(), (int64_t)kTBlock));
+        auto* cnts = W->status;
+        void* args[] = {(void*)&col, (void*)&n, (void*)&tt, (void*)&out, (void*)&C, (void*)&cnts};
+        SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)pk, dim3((unsigned)G), dim3(kQBlock), args, 0, s));
+        return SDFGB_OK;
+    }
     if (vec) {
         // TMA ring: one CTA per SM, segments of kTSegBytes
         auto tk = query_tma_kernel_for<T>(kop);
