@@ -596,7 +596,18 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
         const int64_t w1 = w0 + per_w < ce ? w0 + per_w : ce;
         // ---- A: count this warp's chunks [w0, w1)
         uint32_t cnt = 0;
-        for (int64_t q = w0; q < w1; ++q) {
+        int64_t q = w0;
+        // 8 chunk loads in flight per lane before any is consumed
+        for (; q + 8 <= w1 && ps + (q + 8) * CH <= n; q += 8) {
+            V x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = ldg_hint(col + ps + (q + j) * CH + lane * VN, keep);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x[j], cc), thr) ? 1u : 0u;
+        }
+        for (; q < w1; ++q) {
             const int64_t e0 = ps + q * CH + lane * VN;
             if (e0 + VN <= n) {
                 const V x = ldg_hint(col + e0, keep);
@@ -649,11 +660,19 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
         for (int64_t q0 = w0; q0 < w1; q0 += 4) {
             V x[4];
             uint32_t bits = 0, packed = 0;
+            const bool full = q0 + 4 <= w1 && ps + (q0 + 4) * CH <= n;
+            if (full) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[j] = ldg_hint(col + ps + (q0 + j) * CH + lane * VN, drop);
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int64_t e0 = ps + (q0 + j) * CH + lane * VN;
                 uint32_t m = 0;
-                if (q0 + j < w1 && e0 + VN <= n) {
+                if (full) {
+#pragma unroll
+                    for (int cc = 0; cc < VN; ++cc) m |= (uint32_t)pred<OP>(vget<V, T>(x[j], cc), thr) << cc;
+                } else if (q0 + j < w1 && e0 + VN <= n) {
                     x[j] = ldg_hint(col + e0, drop);
 #pragma unroll
                     for (int cc = 0; cc < VN; ++cc) m |= (uint32_t)pred<OP>(vget<V, T>(x[j], cc), thr) << cc;
