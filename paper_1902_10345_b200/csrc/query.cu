@@ -560,7 +560,7 @@ auto query_tma_kernel_for(int op) {
 //      chunk counts, one 32-bit shuffle scan per 4 chunks, predicated stores.
 // No CTA ever polls another: the only cross-CTA synchronisation is one grid
 // barrier per 64 MB, and HBM sees each input byte once.
-constexpr int64_t kPieceBytes = 64ll << 20;
+constexpr int64_t kPieceBytes = 88ll << 20;  // upper bound; pieces are equalised
 
 template <typename T>
 __device__ __forceinline__ typename Vec16<T>::type ldg_hint(const T* p, uint64_t pol) {
@@ -575,7 +575,9 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
     constexpr int VN = Vec16<T>::n;
     constexpr int NW = kQBlock / 32;
     constexpr int CH = 32 * VN;  // elements per warp chunk
-    constexpr int64_t PIECE = kPieceBytes / (int64_t)sizeof(T);
+    // equal pieces of at most kPieceBytes, multiples of a chunk
+    const int64_t npieces = (n * (int64_t)sizeof(T) + kPieceBytes - 1) / kPieceBytes;
+    const int64_t PIECE = ((n + npieces - 1) / npieces + CH - 1) / CH * CH;
     __shared__ uint32_t s_wcnt[NW];
     __shared__ int64_t s_lo[NW], s_to[NW];
 
@@ -657,16 +659,16 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
         for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
         T* wout = out + (base + cta_off + wc);
         uint32_t run = 0;
-        for (int64_t q0 = w0; q0 < w1; q0 += 4) {
-            V x[4];
-            uint32_t bits = 0, packed = 0;
-            const bool full = q0 + 4 <= w1 && ps + (q0 + 4) * CH <= n;
-            if (full) {
+        for (int64_t q0 = w0; q0 < w1; q0 += 8) {
+            V x[8];
+            uint32_t bits = 0, pk[2] = {0u, 0u};
+            const bool full = q0 + 8 <= w1 && ps + (q0 + 8) * CH <= n;
+            if (full) {  // 8 loads in flight per lane
 #pragma unroll
-                for (int j = 0; j < 4; ++j) x[j] = ldg_hint(col + ps + (q0 + j) * CH + lane * VN, drop);
+                for (int j = 0; j < 8; ++j) x[j] = ldg_hint(col + ps + (q0 + j) * CH + lane * VN, drop);
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < 8; ++j) {
                 const int64_t e0 = ps + (q0 + j) * CH + lane * VN;
                 uint32_t m = 0;
                 if (full) {
@@ -686,26 +688,30 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
                     }
                 }
                 bits |= m << (j * VN);
-                packed |= (uint32_t)__popc(m) << (8 * j);
+                pk[j >> 2] |= (uint32_t)__popc(m) << (8 * (j & 3));
             }
-            uint32_t incl = packed;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += o;
-            }
-            const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-            const uint32_t excl = incl - packed;
+            for (int h = 0; h < 2; ++h) {
+                uint32_t incl = pk[h];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t at = run + ((excl >> (8 * j)) & 0xffu);
-#pragma unroll
-                for (int cc = 0; cc < VN; ++cc) {
-                    const uint32_t pp = (bits >> (j * VN + cc)) & 1u;
-                    st_pred(wout, at, vget<V, T>(x[j], cc), pp);
-                    at += pp;
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += o;
                 }
-                run += (tot >> (8 * j)) & 0xffu;
+                const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+                const uint32_t excl = incl - pk[h];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int j = 4 * h + jj;
+                    uint32_t at = run + ((excl >> (8 * jj)) & 0xffu);
+#pragma unroll
+                    for (int cc = 0; cc < VN; ++cc) {
+                        const uint32_t pp = (bits >> (j * VN + cc)) & 1u;
+                        st_pred(wout, at, vget<V, T>(x[j], cc), pp);
+                        at += pp;
+                    }
+                    run += (tot >> (8 * jj)) & 0xffu;
+                }
             }
         }
         base += piece_total;
