@@ -36,7 +36,7 @@ constexpr int kQVecPerThread = 4;
 constexpr int kQSubs = 2;  // sub-tiles per CTA segment per round
 
 constexpr uint64_t kFlagAgg = 1ull;
-constexpr uint64_t kFlagPrefix = 2ull;
+[[maybe_unused]] constexpr uint64_t kFlagPrefix = 2ull;
 constexpr int kValueBits = 42;
 constexpr uint64_t kValueMask = (1ull << kValueBits) - 1;
 
@@ -311,7 +311,7 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
 constexpr int kTSegBytes = 64 * 1024;
 constexpr int kTBlock = 1024;  // 32 warps: the write pass is latency-bound, so more warps
 constexpr int kTStages = 3;
-constexpr int kTVec = 3;  // 16 B vectors per thread per write sub-tile (12 floats / 6 doubles)
+[[maybe_unused]] constexpr int kTVec = 3;  // 16 B vectors per thread per write sub-tile (12 floats / 6 doubles)
 
 template <typename T>
 __host__ __device__ constexpr int tseg_elems() { return kTSegBytes / (int)sizeof(T); }
@@ -560,7 +560,13 @@ auto query_tma_kernel_for(int op) {
 //      chunk counts, one 32-bit shuffle scan per 4 chunks, predicated stores.
 // No CTA ever polls another: the only cross-CTA synchronisation is one grid
 // barrier per 64 MB, and HBM sees each input byte once.
-constexpr int64_t kPieceBytes = 88ll << 20;  // upper bound; pieces are equalised
+#ifndef SDFGB_Q_PIECE_MB
+#define SDFGB_Q_PIECE_MB 64
+#endif
+#ifndef SDFGB_Q_MINB
+#define SDFGB_Q_MINB 2
+#endif
+constexpr int64_t kPieceBytes = (int64_t)SDFGB_Q_PIECE_MB << 20;  // upper bound; pieces are equalised
 
 template <typename T>
 __device__ __forceinline__ typename Vec16<T>::type ldg_hint(const T* p, uint64_t pol) {
@@ -568,7 +574,7 @@ __device__ __forceinline__ typename Vec16<T>::type ldg_hint(const T* p, uint64_t
 }
 
 template <typename T, int OP>
-__global__ void __launch_bounds__(kQBlock, 2)
+__global__ void __launch_bounds__(kQBlock, SDFGB_Q_MINB)
 query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
                    unsigned long long* __restrict__ count, unsigned long long* __restrict__ cnts) {
     using V = typename Vec16<T>::type;
