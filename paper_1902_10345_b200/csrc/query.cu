@@ -564,7 +564,7 @@ auto query_tma_kernel_for(int op) {
 #define SDFGB_Q_PIECE_MB 64
 #endif
 #ifndef SDFGB_Q_MINB
-#define SDFGB_Q_MINB 2
+#define SDFGB_Q_MINB 1
 #endif
 constexpr int64_t kPieceBytes = (int64_t)SDFGB_Q_PIECE_MB << 20;  // upper bound; pieces are equalised
 
