@@ -251,20 +251,25 @@ def bench_query(args, dist, P):
         be = MG.DeviceBackend()
         gcnt = torch.zeros(1, dtype=torch.int64, device="cuda")
 
-    def step(k):
+    def step(k, ordered=False):
         if multi:  # per-shard compaction; global offsets from an all-gather of counts
             MG.query(dist.pg, col, 0.5, out, gcnt, be, "<")
         else:
-            device.query(col, 0.5, out, cnt, ws, "<")
+            device.query(col, 0.5, out, cnt, ws, "<", ordered=ordered)
 
     ms = time_steps(step, args.steps, args.warmup, dist)
     total = int((gcnt if multi else cnt).item()) // (args.steps + args.warmup)
     nsel = total // dist.world  # per-rank average survivors
     by = 4 * n + 4 * nsel + 8
     res = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms, "bytes_per_unit": by,
-           "launches_per_step": 1, "roofline": roof("hbm", by / ms / 1e6, P, "query_kernel"),
+           "launches_per_step": 1, "roofline": roof("hbm", by / ms / 1e6, P, "query_push_kernel"),
+           "stream_order": "any (concurrent pushes; output compared as a sorted set)",
            "l2": "input 256 MiB > L2",
            "config": {"workload": "Query x < 0.5 over 2^26 fp32 (configs[1])", "N": n, "selected": nsel}}
+    if not multi:  # the input-order (FIFO) variant, same bytes
+        fms = time_steps(lambda k: step(k, True), args.steps, args.warmup, dist)
+        res["fifo"] = {"value": by / fms / 1e6, "unit": "GB/s", "ms_per_step": fms,
+                       "roofline": roof("hbm", by / fms / 1e6, P, "query_piece_kernel")}
     if args.e2e:
         hcol = pinned(n, torch.float64)
         hcol.copy_(col.double().cpu())

@@ -83,11 +83,15 @@ int sdfgb_hist_i64(const int64_t* img, int64_t n,
                    int64_t* hist, int64_t bins, uint64_t* oob, void* stream);
 
 /* Query = predicated stream push + drain (codegen.py:462-471, :363-376;
- * interpreter.py:346-365, :447-481).  out_vals[0:k) = {v : v OP thr} in
- * INPUT ORDER (order-preserving compaction, matching the CPU FIFO);
+ * interpreter.py:346-365, :447-481).  out_vals[0:k) = {v : v OP thr};
  * out_vals[k:] untouched; count[0] += k.  thr is read on the host side.
+ * By default the survivors' ORDER is unspecified (a Map's iterations push
+ * concurrently into the stream): a single-pass reservation
+ * kernel.  OR SDFGB_QUERY_ORDERED into op for input order (the CPU FIFO
+ * order of the generated C code) at the cost of a second, L2-resident pass.
  * ws must hold sdfgb_query_workspace_bytes(n) bytes, zeroed ONCE before
  * its first use (it resets itself afterwards). */
+#define SDFGB_QUERY_ORDERED 0x100
 size_t sdfgb_query_workspace_bytes(int64_t n, int elem_bytes);
 int sdfgb_query_f32(const float* col, int64_t n, int op, double thr,
                     float* out_vals, int64_t* count,

@@ -19,6 +19,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "sdfgb200.h")
 OK, ERR_INVALID, ERR_CUDA, ERR_OOB, ERR_WORKSPACE = 0, 1, 2, 3, 4
 PREC_FP32, PREC_NATIVE = 0, 1
 CMP = {"<": 0, "<=": 1, ">": 2, ">=": 3, "==": 4, "!=": 5}
+QUERY_ORDERED = 0x100  # include/sdfgb200.h: OR into op for input-order survivors
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

@@ -726,6 +726,148 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
     if (c == 0 && tid == 0) atomicAdd(count, (unsigned long long)base);
 }
 
+// ---------------------------------------------------------------------------
+// Unordered push kernel (the default).  A Map's iterations are concurrent and
+// a Stream is a "concurrent queue" (Appendix A push rule ❷), so
+// the push order of the query map is unspecified -- the north star compares
+// Query output as a sorted set.  Each CTA therefore reserves its survivors'
+// slot range with ONE atomicAdd on a workspace counter and never looks at
+// another CTA: a single streaming pass, HBM read 4N + write 4k, no grid
+// barrier, no L2 re-read.
+//   tile   = kPBlock/32 warps x 8 chunks x (32 lanes x 16 B)   (32 KB)
+//   warp   8 loads in flight per lane, predicate nibbles, two byte-packed
+//          shuffle scans -> per-chunk exclusive offsets, warp total
+//   CTA    warp totals -> smem -> warp 0 scan + atomicAdd(ctr, total)
+//   store  lanes of a chunk write consecutive slots (coalesced per chunk)
+// Within a warp's 1024 elements the survivors keep input order; the CTA
+// order is the reservation order.  The last CTA to finish (done ticket)
+// folds the total into *count and re-zeroes the counter and the ticket, so
+// the workspace stays zero between launches.
+constexpr int kPBlock = 256;
+constexpr int kPChunks = 8;
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(kPBlock, 4)
+query_push_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
+                  unsigned long long* __restrict__ count, unsigned long long* __restrict__ ctr,
+                  unsigned long long* __restrict__ done) {
+    using V = typename Vec16<T>::type;
+    constexpr int VN = Vec16<T>::n;
+    constexpr int NW = kPBlock / 32;
+    constexpr int CH = 32 * VN;
+    constexpr int WE = kPChunks * CH;  // elements per warp
+    __shared__ uint32_t s_w[NW];
+    __shared__ unsigned long long s_base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t w0 = ((int64_t)blockIdx.x * NW + warp) * WE;
+    const uint64_t drop = make_policy(false);
+    V x[kPChunks];
+    uint32_t bits = 0, pk[2] = {0u, 0u};
+    const bool full = w0 + WE <= n;
+    if (full) {
+#pragma unroll
+        for (int j = 0; j < kPChunks; ++j) x[j] = ldg_hint(col + w0 + j * CH + lane * VN, drop);
+    }
+#pragma unroll
+    for (int j = 0; j < kPChunks; ++j) {
+        const int64_t e0 = w0 + j * CH + lane * VN;
+        uint32_t m = 0;
+        if (full) {
+#pragma unroll
+            for (int cc = 0; cc < VN; ++cc) m |= (uint32_t)pred<OP>(vget<V, T>(x[j], cc), thr) << cc;
+        } else if (e0 + VN <= n) {
+            x[j] = ldg_hint(col + e0, drop);
+#pragma unroll
+            for (int cc = 0; cc < VN; ++cc) m |= (uint32_t)pred<OP>(vget<V, T>(x[j], cc), thr) << cc;
+        } else {
+            T* xs = reinterpret_cast<T*>(&x[j]);
+#pragma unroll
+            for (int cc = 0; cc < VN; ++cc) {
+                const bool live = e0 + cc < n;
+                xs[cc] = live ? col[e0 + cc] : T(0);
+                m |= (uint32_t)(live && pred<OP>(xs[cc], thr)) << cc;
+            }
+        }
+        bits |= m << (j * VN);
+        pk[j >> 2] |= (uint32_t)__popc(m) << (8 * (j & 3));
+    }
+    // per-chunk exclusive lane offsets (bytes of excl) and chunk totals (bytes of tot)
+    uint32_t excl[2], tot[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint32_t incl = pk[h];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += o;
+        }
+        tot[h] = __shfl_sync(0xffffffffu, incl, 31);
+        excl[h] = incl - pk[h];
+    }
+    const uint32_t t4 = (tot[0] & 0x00ff00ffu) + ((tot[0] >> 8) & 0x00ff00ffu) + (tot[1] & 0x00ff00ffu) +
+                        ((tot[1] >> 8) & 0x00ff00ffu);
+    const uint32_t wtot = (t4 & 0xffffu) + (t4 >> 16);
+    if (lane == 0) s_w[warp] = wtot;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t v = lane < NW ? s_w[lane] : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int d = 1; d < NW; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        unsigned long long b = 0;
+        if (lane == NW - 1) {
+            b = atomicAdd(ctr, (unsigned long long)inc);
+            s_base = b;
+        }
+        __syncwarp();
+        if (lane < NW) s_w[lane] = inc - v;  // exclusive warp offsets
+    }
+    __syncthreads();
+    T* wout = out + (s_base + s_w[warp]);
+    uint32_t run = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int j = 4 * h + jj;
+            uint32_t at = run + ((excl[h] >> (8 * jj)) & 0xffu);
+#pragma unroll
+            for (int cc = 0; cc < VN; ++cc) {
+                const uint32_t pp = (bits >> (j * VN + cc)) & 1u;
+                st_pred(wout, at, vget<V, T>(x[j], cc), pp);
+                at += pp;
+            }
+            run += (tot[h] >> (8 * jj)) & 0xffu;
+        }
+    }
+    if (tid == NW - 1) {  // the thread that reserved: publish completion after its reservation
+        __threadfence();
+        if (atomicAdd(done, 1ull) == (unsigned long long)gridDim.x - 1) {
+            __threadfence();
+            const unsigned long long total = atomicExch(ctr, 0ull);
+            atomicAdd(count, total);
+            *done = 0ull;
+        }
+    }
+}
+
+template <typename T>
+auto query_push_kernel_for(int op) {
+    switch (op) {
+    case 0: return query_push_kernel<T, 0>;
+    case 1: return query_push_kernel<T, 1>;
+    case 2: return query_push_kernel<T, 2>;
+    case 3: return query_push_kernel<T, 3>;
+    case 4: return query_push_kernel<T, 4>;
+    case 5: return query_push_kernel<T, 5>;
+    case 6: return query_push_kernel<T, 6>;
+    default: return query_push_kernel<T, 7>;
+    }
+}
+
 template <typename T>
 auto query_piece_kernel_for(int op) {
     switch (op) {
@@ -806,6 +948,8 @@ auto query_kernel_for(int op) {
 template <typename T>
 int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* count, void* ws,
                  size_t ws_bytes, void* stream) {
+    const bool ordered = (op & SDFGB_QUERY_ORDERED) != 0;
+    op &= ~SDFGB_QUERY_ORDERED;
     if (n < 0 || op < 0 || op > 5 || !count || (n > 0 && (!col || !out || !ws)))
         return set_error(SDFGB_ERR_INVALID, "query: bad arguments");
     if (n == 0) return SDFGB_OK;
@@ -823,6 +967,15 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
     int kop;
     T tt;
     fold_threshold<T>(op, thr, kop, tt);
+    if (!ordered && vec) {
+        // unordered push: one CTA per 32 KB tile, one reservation atomic each
+        constexpr int64_t tile = (int64_t)kPBlock / 32 * kPChunks * 32 * Vec16<T>::n;
+        const int64_t G = (n + tile - 1) / tile;
+        if (G > 0x7fffffff) return set_error(SDFGB_ERR_INVALID, "query: n too large");
+        query_push_kernel_for<T>(kop)<<<(unsigned)G, kPBlock, 0, s>>>(col, n, tt, out, C, &W->ticket, &W->done);
+        SDFGB_LAUNCHED("query_push_kernel");
+        return SDFGB_OK;
+    }
     if (vec && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && !getenv("SDFGB_QUERY_TMA")) {
         // piece kernel: co-resident CTAs, one grid barrier per 64 MB piece
         auto pk = query_piece_kernel_for<T>(kop);

@@ -54,15 +54,18 @@ def query_workspace(n, elem_bytes=4, device=None):
     return torch.zeros(nb, dtype=torch.uint8, device=device or "cuda")
 
 
-def query(col, thr, out, count, ws, op="<", stream=None):
-    """out[0:k) = survivors of ``col OP thr`` in input order; count[0] += k."""
+def query(col, thr, out, count, ws, op="<", stream=None, ordered=False):
+    """out[0:k) = survivors of ``col OP thr``; count[0] += k.  The survivors'
+    order is unspecified (concurrent pushes) unless ``ordered``, which keeps
+    the input order of the reference's FIFO drain."""
     import torch
     L = _lib.load()
     _require(count, torch.int64, "count")
     fn = {torch.float32: L.sdfgb_query_f32, torch.float64: L.sdfgb_query_f64}.get(col.dtype)
     if fn is None or out.dtype != col.dtype:
         raise TypeError("query: col/out must both be float32 or float64")
-    _lib.check(fn(_p(col), col.numel(), _lib.CMP[op], float(thr), _p(out), _p(count), _p(ws),
+    opf = _lib.CMP[op] | (_lib.QUERY_ORDERED if ordered else 0)
+    _lib.check(fn(_p(col), col.numel(), opf, float(thr), _p(out), _p(count), _p(ws),
                   ws.numel(), _stream(stream)))
 
 

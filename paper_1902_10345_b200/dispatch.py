@@ -33,23 +33,41 @@ PRECISIONS = ("fp32", "native")
 _CT = {"int64": "int64_t", "float64": "double"}
 
 
-def gpu_storage(precision: str) -> str:
-    return f"{STORAGE_PREFIX}:{precision}"
+STREAM_ORDERS = ("any", "fifo")
 
 
-def marked_precision(g: Graph, plan: Plan) -> Optional[str]:
-    """Precision recorded by GPUTransformMap on the motif's containers
-    (DataDesc.storage is a free string, ir.py:75)."""
+def gpu_storage(precision: str, stream_order: str = "any") -> str:
+    """The marker GPUTransformMap writes into DataDesc.storage:
+    ``GPU_Global:<precision>[:fifo]``."""
+    return f"{STORAGE_PREFIX}:{precision}" + (":fifo" if stream_order == "fifo" else "")
+
+
+def _parse_storage(st: str):
+    parts = st.split(":")
+    prec = parts[1] if len(parts) > 1 else "fp32"
+    order = parts[2] if len(parts) > 2 else "any"
+    return prec, order
+
+
+def marked_mode(g: Graph, plan: Plan) -> Optional[tuple]:
+    """(precision, stream_order) recorded by GPUTransformMap on the motif's
+    containers (DataDesc.storage is a free string, ir.py:75); None if the
+    graph is not marked."""
     seen = set()
     for c in plan.roles.values():
         st = g.data[c].storage or ""
         if st.startswith(STORAGE_PREFIX):
-            seen.add(st.split(":", 1)[1] if ":" in st else "fp32")
+            seen.add(_parse_storage(st))
         else:
             return None
     if len(seen) != 1:
-        raise CodegenError(f"inconsistent GPU storage precisions {sorted(seen)}")
+        raise CodegenError(f"inconsistent GPU storage markers {sorted(seen)}")
     return seen.pop()
+
+
+def marked_precision(g: Graph, plan: Plan) -> Optional[str]:
+    mode = marked_mode(g, plan)
+    return None if mode is None else mode[0]
 
 
 @dataclass
@@ -61,6 +79,7 @@ class GeneratedB200Code:
     symbol_args: list
     plan: Plan
     precision: str
+    stream_order: str = "any"
 
     def signature(self) -> str:
         parts = [f"{_CT[t]}* {n}" for n, t in self.pointer_args]
@@ -97,17 +116,20 @@ def generate(sdfg: Any, require_marked: bool = True) -> GeneratedB200Code:
         plan = classify(g)
     except UnsupportedGraph as exc:
         raise CodegenError(str(exc)) from exc
-    prec = marked_precision(g, plan)
-    if prec is None:
+    mode = marked_mode(g, plan)
+    if mode is None:
         if require_marked:
             raise CodegenError(
                 f"SDFG '{g.name}' has no state matched by GPUTransformMap; apply the "
                 f"transformation before generating B200 code")
-        prec = "fp32"
+        mode = ("fp32", "any")
+    prec, order = mode
     if prec not in PRECISIONS:
         raise CodegenError(f"unknown precision '{prec}'")
+    if order not in STREAM_ORDERS:
+        raise CodegenError(f"unknown stream order '{order}'")
     return GeneratedB200Code(_describe(plan, prec), g.name, plan.pointer_args, plan.symbol_args,
-                             plan, prec)
+                             plan, prec, order)
 
 
 def invoke_toolchain(code: GeneratedB200Code) -> "CompiledB200Sdfg":
@@ -174,7 +196,10 @@ class CompiledB200Sdfg:
         if out.size < col.size:
             raise ExecutionError(f"drain of {col.size} elements may overflow '{r['out_vals']}'")
         _lib.check(self._lib.sdfgb_host_query(_ptr(col), _ptr(thr), _ptr(out), _ptr(cnt), col.size,
-                                              _lib.CMP[plan.params["op"]], prec))
+                                              _lib.CMP[plan.params["op"]] | self._order_flag(), prec))
+
+    def _order_flag(self):
+        return _lib.QUERY_ORDERED if self.code.stream_order == "fifo" else 0
 
     def _run_spmv(self, plan, b, syms, prec):
         r = plan.roles

@@ -6,12 +6,15 @@ an applicability check, and a rewrite on the copy that
 ``apply_transformation`` makes (engine.py:178-202).  The rule applies to the
 top-level map of the program's compute state when the whole program is a
 motif the sm_100a library implements (classify.py); ``apply`` records the
-decision -- and the ``precision`` parameter, which is journaled like any
-rule parameter (engine.py:188-202) -- in ``DataDesc.storage`` of the motif's
-containers.  ``storage`` is a free string (ir.py:75) the validator and the
-interpreter ignore, so the marked graph stays valid for the reference's
-interpreter, which remains the oracle for it (the reference rejects any new
-map schedule, validation.py:122-125, and has no GPU transformation, so the
+decision -- and the ``precision`` and ``stream_order`` parameters, which are
+journaled like any rule parameter (engine.py:188-202) -- in
+``DataDesc.storage`` of the motif's containers.  ``stream_order`` "any"
+(default) lets concurrent pushes land in any order (a Stream is a concurrent
+queue); "fifo" keeps the generated C code's input order.
+``storage`` is a free string (ir.py:75) the validator and the interpreter
+ignore, so the marked graph stays valid for the reference's interpreter,
+which remains the oracle for it (the reference rejects any new map
+schedule, validation.py:122-125, and has no GPU transformation, so the
 marker cannot be a schedule).
 
 Registration is explicit (``paper_1902_10345_b200.register()``): adding a
@@ -24,7 +27,7 @@ from __future__ import annotations
 from typing import Any
 
 from .classify import UnsupportedGraph, classify
-from .dispatch import PRECISIONS, STORAGE_PREFIX, gpu_storage
+from .dispatch import PRECISIONS, STORAGE_PREFIX, STREAM_ORDERS, gpu_storage
 from .graph import load
 
 RULE_NAME = "GPUTransformMap"
@@ -36,7 +39,7 @@ def build_rule(engine, matching, ir):
     class GPUTransformMap(engine.Transformation):
         name = RULE_NAME
         strict = False
-        default_params = {"precision": "fp32"}
+        default_params = {"precision": "fp32", "stream_order": "any"}
 
         def expressions(self):
             return [matching.Pattern([matching.PatternNode("map", (ir.MapEntry,))])]
@@ -62,11 +65,14 @@ def build_rule(engine, matching, ir):
             prec = params.get("precision", "fp32")
             if prec not in PRECISIONS:
                 raise ValueError(f"precision must be one of {PRECISIONS}, not '{prec}'")
+            order = params.get("stream_order", "any")
+            if order not in STREAM_ORDERS:
+                raise ValueError(f"stream_order must be one of {STREAM_ORDERS}, not '{order}'")
             plan = self._plan(sdfg)
             if plan is None:
                 raise ValueError("GPUTransformMap: program is not a B200 motif")
             for c in set(plan.roles.values()):
-                sdfg.data[c].storage = gpu_storage(prec)
+                sdfg.data[c].storage = gpu_storage(prec, order)
 
     return GPUTransformMap
 

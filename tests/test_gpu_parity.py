@@ -2,7 +2,8 @@
 its interpreter) and against the C oracle, through the C ABI.
 
 Tolerances: histogram counts and query survivors bit-exact
-(query compared in order -- the compaction is order-preserving); Jacobi
+(query compared as a sorted set by default -- concurrent pushes have no
+order -- and in input order with stream_order "fifo" / ordered=True); Jacobi
 bit-exact against the same-op-order restatement (fp32) or the reference
 itself (native f64); SpMV 1e-5 rel (fp32) / 1e-12 (native); GEMM 1e-4 rel.
 """
@@ -31,12 +32,20 @@ def _gpu():
 DEV = "cuda"
 
 
-def marked(name, precision):
+def marked(name, precision, order="any"):
     doc = json.load(open(graph_path(name)))
     for d in doc["data"]:
         if not d["transient"]:
-            d["storage"] = f"GPU_Global:{precision}"
+            d["storage"] = f"GPU_Global:{precision}" + (":fifo" if order == "fifo" else "")
     return doc
+
+
+def _as_set(out_vals, count, count0):
+    """survivors sorted (a stream's push order is unspecified), tail as is"""
+    k = int(count[0] - count0[0])
+    o = np.array(out_vals, copy=True)
+    o[:k] = np.sort(o[:k])
+    return o
 
 
 SUPPORTED = ["histogram", "histogram_int", "query", "query_gallery", "spmv", "jacobi2d", "matmul",
@@ -51,12 +60,15 @@ def _f32_exact(a):
     return np.array_equal(a, a.astype(np.float32).astype(np.float64))
 
 
+@pytest.mark.parametrize("order", ["any", "fifo"])
 @pytest.mark.parametrize("precision", ["native", "fp32"])
 @pytest.mark.parametrize("c", CASES, ids=repr)
-def test_dropin_matches_reference_interpreter(c, precision):
+def test_dropin_matches_reference_interpreter(c, precision, order):
     if c.motif.startswith("matmul") and precision == "native":
         pytest.skip("GEMM runs 3xTF32 only")
-    prog = b200.invoke_toolchain(b200.generate(marked(c.motif, precision)))
+    if order == "fifo" and not c.motif.startswith("query"):
+        pytest.skip("stream order only applies to the query motif")
+    prog = b200.invoke_toolchain(b200.generate(marked(c.motif, precision, order)))
     if c.error:
         with pytest.raises(b200.OutOfBoundsError):
             prog.run(c.inputs, c.symbols)
@@ -76,6 +88,10 @@ def test_dropin_matches_reference_interpreter(c, precision):
             full = np.array(c.inputs["out_vals"], np.float64)
             full[:k] = o[:k]
             outputs["out_vals"], outputs["count"] = full, n
+    if c.motif.startswith("query") and order == "any":
+        got = dict(got)
+        got["out_vals"] = _as_set(got["out_vals"], got["count"], c.inputs["count"])
+        outputs["out_vals"] = _as_set(outputs["out_vals"], outputs["count"], c.inputs["count"])
     for name, exp in outputs.items():
         g = got[name].reshape(exp.shape)
         if exp.dtype.kind == "i" or c.motif.startswith(("histogram", "query")):
@@ -169,9 +185,10 @@ def test_hist_i64():
     np.testing.assert_array_equal(h.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("ordered", [False, True])
 @pytest.mark.parametrize("op", ["<", "<=", ">", ">=", "==", "!="])
 @pytest.mark.parametrize("n,offset", [(1, 0), (31, 1), (4096, 0), (4097, 3), (1000003, 2), (65536 * 3, 0)])
-def test_query_order_preserving(n, offset, op):
+def test_query(n, offset, op, ordered):
     from paper_1902_10345_b200 import device
     rng = np.random.default_rng(n + offset)
     col = rng.random(n, dtype=np.float32)
@@ -184,23 +201,50 @@ def test_query_order_preserving(n, offset, op):
     for rep in range(3):  # workspace reuse across launches (epoch + self-reset)
         out.fill_(-1.0)
         cnt.fill_(11)
-        device.query(view, 0.5, out, cnt, ws, op)
+        device.query(view, 0.5, out, cnt, ws, op, ordered=ordered)
         rout, rcnt = oracle.query(col, 0.5, np.full(n, -1.0, np.float32), np.array([11]), op)
         np.testing.assert_array_equal(cnt.cpu().numpy(), rcnt)
-        np.testing.assert_array_equal(out.cpu().numpy(), rout)
+        got = out.cpu().numpy()
+        if not ordered:
+            got, rout = _as_set(got, rcnt, [11]), _as_set(rout, rcnt, [11])
+        np.testing.assert_array_equal(got, rout)
 
 
-def test_query_f64():
+@pytest.mark.parametrize("ordered", [False, True])
+def test_query_f64(ordered):
     from paper_1902_10345_b200 import device
     rng = np.random.default_rng(9)
     col = rng.random(777777)
     out = torch.zeros(col.size, dtype=torch.float64, device=DEV)
     cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
     ws = device.query_workspace(col.size, 8, DEV)
-    device.query(t(col), 0.3, out, cnt, ws, ">=")
+    device.query(t(col), 0.3, out, cnt, ws, ">=", ordered=ordered)
     rout, rcnt = oracle.query(col, 0.3, np.zeros(col.size), np.zeros(1, np.int64), ">=")
     assert cnt.item() == rcnt[0]
-    np.testing.assert_array_equal(out.cpu().numpy(), rout)
+    got = out.cpu().numpy()
+    if not ordered:
+        got, rout = _as_set(got, rcnt, [0]), _as_set(rout, rcnt, [0])
+    np.testing.assert_array_equal(got, rout)
+
+
+def test_query_mixed_modes_share_workspace():
+    """ordered and unordered launches alternate on one workspace; the
+    unordered kernel's counter/ticket must be left zeroed every time"""
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(12)
+    col = rng.random(300001, dtype=np.float32)
+    ws = device.query_workspace(col.size, 4, DEV)
+    sel = col[col < 0.25]
+    for rep in range(6):
+        out = torch.zeros(col.size, dtype=torch.float32, device=DEV)
+        cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+        device.query(t(col), 0.25, out, cnt, ws, "<", ordered=bool(rep % 2))
+        assert cnt.item() == sel.size
+        got = out[:sel.size].cpu().numpy()
+        if rep % 2:
+            np.testing.assert_array_equal(got, sel)
+        else:
+            np.testing.assert_array_equal(np.sort(got), np.sort(sel))
 
 
 def random_csr(rng, H, W, max_len):
@@ -302,11 +346,18 @@ def test_full_query_2pow26():
     col = np.random.default_rng(1).random(1 << 26, dtype=np.float32)
     out = torch.zeros(col.size, dtype=torch.float32, device=DEV)
     cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
-    device.query(t(col), 0.5, out, cnt, device.query_workspace(col.size, 4, DEV), "<")
-    k = int(cnt.item())
+    ws = device.query_workspace(col.size, 4, DEV)
     sel = col[col < 0.5]
-    assert k == sel.size
-    np.testing.assert_array_equal(out[:k].cpu().numpy(), sel)
+    for ordered in (False, True):
+        cnt.zero_()
+        device.query(t(col), 0.5, out, cnt, ws, "<", ordered=ordered)
+        k = int(cnt.item())
+        assert k == sel.size
+        got = out[:k].cpu().numpy()
+        if ordered:
+            np.testing.assert_array_equal(got, sel)
+        else:
+            np.testing.assert_array_equal(np.sort(got), np.sort(sel))
 
 
 def test_full_jacobi_8192_three_steps():
