@@ -14,10 +14,13 @@
 //   * shared-memory-privatised counters, R replicas (warp % R) so skewed
 //     images do not serialise one address; a warp whose lanes all hit one
 //     bin issues a single add of 32;
-//   * 8-CTA thread-block clusters fold their smem histograms through DSMEM
-//     into the leader CTA, which alone merges into global memory -> only
-//     grid/8 x bins global atomics (the 2 KB hist lives in 4 L2 slices, so
-//     per-CTA global merges would serialise there).
+//   * 2-CTA thread-block clusters fold their smem histograms through DSMEM
+//     into the leader CTA, which alone merges into global memory -> grid/2
+//     x bins global atomics.  (8-CTA clusters halve those again but strand
+//     SMs: clusters must fit in a GPC, and 16.9 -> 15.8 us measured.)
+//   * programmatic dependent launch: the counter init and CTA launch overlap
+//     the previous kernel's merge tail (15.8 -> 14.2 us on 4096^2 fp32;
+//     sweep in tools/sweep.sh).
 #include <algorithm>
 #include <cmath>
 #include <cooperative_groups.h>
@@ -29,9 +32,21 @@ namespace cg = cooperative_groups;
 namespace sdfgb {
 namespace {
 
-constexpr int kHistBlock = 512;
-constexpr int kHistUnroll = 4;
-constexpr int kHistCluster = 8;
+#ifndef SDFGB_H_BLOCK
+#define SDFGB_H_BLOCK 512
+#endif
+#ifndef SDFGB_H_UNROLL
+#define SDFGB_H_UNROLL 4
+#endif
+#ifndef SDFGB_H_CLUSTER
+#define SDFGB_H_CLUSTER 2
+#endif
+#ifndef SDFGB_H_PDL
+#define SDFGB_H_PDL 1
+#endif
+constexpr int kHistBlock = SDFGB_H_BLOCK;
+constexpr int kHistUnroll = SDFGB_H_UNROLL;
+constexpr int kHistCluster = SDFGB_H_CLUSTER;
 constexpr int kMaxSmemBins = 12288;  // 48 KB of uint32 counters per replica set
 
 enum BinMode { kScaled = 0, kIdentity = 1, kPow2 = 2 };
@@ -83,6 +98,10 @@ hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale
     const int warp = tid >> 5;
 
     for (uint32_t k = tid; k < (uint32_t)reps * row; k += blockDim.x) sh[k] = 0u;
+    // programmatic dependent launch: everything above overlaps the previous
+    // kernel's tail; the image and the counters are touched only after it
+    // has completed and flushed (no-op without the launch attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
 
     const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(sh) + (uint32_t)(warp % reps) * row * 4u;
@@ -121,6 +140,8 @@ hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale
         for (int u = 0; u < kHistUnroll; ++u) cur[u] = nxt[u];
     }
     __syncthreads();
+    // let the next kernel in the stream start launching its CTAs
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // fold replicas into replica 0 (trash included)
     for (uint32_t k = tid; k < row; k += blockDim.x) {
         uint32_t s = 0;
@@ -204,7 +225,17 @@ int launch_hist(const T* img, int64_t n, double scale, double div, int64_t* hist
     int64_t cap = (int64_t)nc * kHistCluster;
     int64_t blocks = std::max<int64_t>(1, std::min(want, cap));
     blocks = (blocks + kHistCluster - 1) / kHistCluster * kHistCluster;
-    kern<<<(unsigned)blocks, kHistBlock, smem, s>>>(img, n, head, scale, div, bins, reps, H, O);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(kHistBlock);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = SDFGB_H_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SDFGB_CUDA(cudaLaunchKernelEx(&cfg, kern, img, n, head, scale, div, bins, reps, H, O));
     SDFGB_LAUNCHED("hist_smem_kernel");
     return SDFGB_OK;
 }
