@@ -148,20 +148,39 @@ class Dist:
 
 # ---------------------------------------------------------------- timing
 
-def time_steps(step, steps, warmup, dist, stream=None):
+def time_steps(step, steps, warmup, dist, stream=None, graph=False):
     """W untimed steps, then K steps between CUDA events on the launching
-    stream, barrier + synchronize on both sides; max over ranks."""
+    stream, barrier + synchronize on both sides; max over ranks.  With
+    ``graph`` the K steps are captured once into a CUDA graph and the timed
+    region is one replay (the same kernels with the host launch cost
+    removed: a ~15 us histogram step is otherwise launch-bound)."""
     import torch
     s = stream or torch.cuda.current_stream()
     for k in range(warmup):
         step(k)
     torch.cuda.synchronize()
+    g = None
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g, stream=cs):
+                for k in range(steps):
+                    step(warmup + k)
+        torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # ~1 ms device spin queued ahead of the start event: the host enqueues the
+    # K steps while it runs, so host submission latency is not timed
+    torch.cuda._sleep(2_000_000)
     a.record(s)
-    for k in range(steps):
-        step(warmup + k)
+    if g is not None:
+        g.replay()
+    else:
+        for k in range(steps):
+            step(warmup + k)
     b.record(s)
     b.synchronize()
     torch.cuda.synchronize()
@@ -211,7 +230,7 @@ def bench_histogram(args, dist, P):
         else:
             device.hist(imgs[k % nbuf], hist, oob)
 
-    ms = time_steps(step, args.steps, args.warmup, dist)
+    ms = time_steps(step, args.steps, args.warmup, dist, graph=not multi)
     assert oob.item() == 0
     by = 4 * H * W + 2 * 256 * 8
     out = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms,
@@ -257,7 +276,7 @@ def bench_query(args, dist, P):
         else:
             device.query(col, 0.5, out, cnt, ws, "<", ordered=ordered)
 
-    ms = time_steps(step, args.steps, args.warmup, dist)
+    ms = time_steps(step, args.steps, args.warmup, dist, graph=not multi)
     total = int((gcnt if multi else cnt).item()) // (args.steps + args.warmup)
     nsel = total // dist.world  # per-rank average survivors
     by = 4 * n + 4 * nsel + 8
@@ -267,7 +286,7 @@ def bench_query(args, dist, P):
            "l2": "input 256 MiB > L2",
            "config": {"workload": "Query x < 0.5 over 2^26 fp32 (configs[1])", "N": n, "selected": nsel}}
     if not multi:  # the input-order (FIFO) variant, same bytes
-        fms = time_steps(lambda k: step(k, True), args.steps, args.warmup, dist)
+        fms = time_steps(lambda k: step(k, True), args.steps, args.warmup, dist, graph=True)
         res["fifo"] = {"value": by / fms / 1e6, "unit": "GB/s", "ms_per_step": fms,
                        "roofline": roof("hbm", by / fms / 1e6, P, "query_piece_kernel")}
     if args.e2e:
