@@ -316,18 +316,25 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
                     if (!rowb && !colb[j]) op[j] = o[j];
             }
         };
+        // three rows per iteration with the window's names rotating
+        // (n4, c4, s4) -> (c4, s4, n4) -> (s4, n4, c4): every load lands in a
+        // register whose old row is dead, so the loop carries no moves
+        // (the two-row version spent ~12 MOVs per row on the rotation)
         int r = rb;
-        for (; r + 1 < re; r += 2) {  // two rows per iteration: 2x ILP, no register rotation moves
-            const float4 sa = *reinterpret_cast<const float4*>(in + (r + 1) * kTbRX + 4 * lane);
-            const float4 sb = *reinterpret_cast<const float4*>(in + (r + 2) * kTbRX + 4 * lane);
-            row(r, n4, c4, sa);
-            row(r + 1, c4, sa, sb);
-            n4 = sa;
-            c4 = sb;
+        float4 s4;
+        auto ld = [&](int rr) { return *reinterpret_cast<const float4*>(in + rr * kTbRX + 4 * lane); };
+        for (; r + 2 < re; r += 3) {
+            s4 = ld(r + 1);
+            row(r, n4, c4, s4);
+            n4 = ld(r + 2);
+            row(r + 1, c4, s4, n4);
+            c4 = ld(r + 3);
+            row(r + 2, s4, n4, c4);  // the window for row r+3 is (n4, c4) again
         }
         if (r < re) {
-            const float4 sa = *reinterpret_cast<const float4*>(in + (r + 1) * kTbRX + 4 * lane);
-            row(r, n4, c4, sa);
+            s4 = ld(r + 1);
+            row(r, n4, c4, s4);
+            if (r + 1 < re) row(r + 1, c4, s4, ld(r + 2));
         }
         __syncthreads();
     }

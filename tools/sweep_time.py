@@ -54,3 +54,11 @@ elif motif == "query":
     ws = device.query_workspace(n, 4)
     us = timed(lambda k: device.query(col, 0.5, out, cnt, ws, "<"))
     print(f"{name:28s} query  {us:7.1f} us {(6 * n) / us / 1e3:6.0f} GB/s")
+elif motif == "jacobi2d":
+    N, T = 8192, 141
+    A = torch.zeros(2, N, N, device="cuda")
+    A[0, 1:-1, 1:-1] = torch.rand(N - 2, N - 2, device="cuda")
+    A[1] = A[0]
+    us = timed(lambda k: device.jacobi2d(A, T), reps=3)
+    per = 4 * N * N + 4 * (N - 2) * (N - 2)
+    print(f"{name:28s} jacobi {us / T:7.2f} us/step {per * T / us / 1e3:6.0f} GB/s")
