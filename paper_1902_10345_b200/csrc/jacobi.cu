@@ -265,11 +265,20 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
     }
     // does the region touch the global border (or beyond)?  CTA-uniform
     const bool edge = gx0 <= 0 || gy0 <= 0 || gx0 + kTbRX - 1 >= N - 1 || gy0 + RY - 1 >= N - 1;
-    if (edge) {  // buffer 1 carries plane p^1's border
-        for (int q = threadIdx.x; q < kTbRX * RY; q += kTbThreads) {
-            const int gy = gy0 + q / kTbRX, gx = gx0 + q % kTbRX;
-            if (gy >= 0 && gy < N && gx >= 0 && gx < N && (gy == 0 || gy == N - 1 || gx == 0 || gx == N - 1))
-                buf1[q] = dst_in[(int64_t)gy * N + gx];
+    if (edge) {  // buffer 1 carries plane p^1's border: copy just the border lines in the region
+        for (int q = threadIdx.x; q < 2 * kTbRX + 2 * RY; q += kTbThreads) {
+            int ry, rx;  // region coordinates of candidate q
+            if (q < 2 * kTbRX) {  // border rows 0 and N-1
+                ry = (q < kTbRX ? 0 : N - 1) - gy0;
+                rx = q % kTbRX;
+            } else {  // border columns 0 and N-1
+                const int k = q - 2 * kTbRX;
+                ry = k % RY;
+                rx = (k < RY ? 0 : N - 1) - gx0;
+            }
+            const int gy = gy0 + ry, gx = gx0 + rx;
+            if (ry >= 0 && ry < RY && rx >= 0 && rx < kTbRX && gy >= 0 && gy < N && gx >= 0 && gx < N)
+                buf1[ry * kTbRX + rx] = dst_in[(int64_t)gy * N + gx];
         }
     }
     __syncthreads();
@@ -282,33 +291,51 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
 #pragma unroll
     for (int j = 0; j < 4; ++j) colb[j] = gx + j <= 0 || gx + j >= N - 1;
 
-    for (int st = 0; st < steps; ++st) {
-        const float* in = (st & 1) ? buf1 : buf0;
-        float* out = (st & 1) ? buf0 : buf1;
-        float4 n4 = *reinterpret_cast<const float4*>(in + (rb - 1) * kTbRX + 4 * lane);
-        float4 c4 = *reinterpret_cast<const float4*>(in + rb * kTbRX + 4 * lane);
-        // one output row from its north/centre/south float4s
-        auto row = [&](int r, const float4& nq, const float4& cq, const float4& sq) {
-            const float lft = __shfl_up_sync(0xffffffffu, cq.w, 1);   // lane 0: region edge, unused
-            const float rgt = __shfl_down_sync(0xffffffffu, cq.x, 1); // lane 31: region edge, unused
-            const float cc[4] = {cq.x, cq.y, cq.z, cq.w};
-            const float nn[4] = {nq.x, nq.y, nq.z, nq.w};
-            const float ss[4] = {sq.x, sq.y, sq.z, sq.w};
-            const float ww[4] = {lft, cq.x, cq.y, cq.z};
-            const float ee[4] = {cq.y, cq.z, cq.w, rgt};
-            float o[4];
+    // one stencil row from its north/centre/south float4s, reference order
+    auto calc = [&](const float4& nq, const float4& cq, const float4& sq) -> float4 {
+        const float lft = __shfl_up_sync(0xffffffffu, cq.w, 1);   // lane 0: region edge, unused
+        const float rgt = __shfl_down_sync(0xffffffffu, cq.x, 1); // lane 31: region edge, unused
+        const float cc[4] = {cq.x, cq.y, cq.z, cq.w};
+        const float nn[4] = {nq.x, nq.y, nq.z, nq.w};
+        const float ss[4] = {sq.x, sq.y, sq.z, sq.w};
+        const float ww[4] = {lft, cq.x, cq.y, cq.z};
+        const float ee[4] = {cq.y, cq.z, cq.w, rgt};
+        float o[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float acc = __fadd_rn(cc[j], nn[j]);
-                acc = __fadd_rn(acc, ss[j]);
-                acc = __fadd_rn(acc, ww[j]);
-                acc = __fadd_rn(acc, ee[j]);
-                o[j] = __fmul_rn(coef, acc);
-            }
+        for (int j = 0; j < 4; ++j) {
+            float acc = __fadd_rn(cc[j], nn[j]);
+            acc = __fadd_rn(acc, ss[j]);
+            acc = __fadd_rn(acc, ww[j]);
+            acc = __fadd_rn(acc, ee[j]);
+            o[j] = __fmul_rn(coef, acc);
+        }
+        return make_float4(o[0], o[1], o[2], o[3]);
+    };
+    auto ldrow = [&](const float* in, int rr) {
+        rr = rr < 0 ? 0 : (rr > RY - 1 ? RY - 1 : rr);  // beyond the region: halo garbage, never kept
+        return *reinterpret_cast<const float4*>(in + rr * kTbRX + 4 * lane);
+    };
+
+    const float* cur = buf0;
+    float* oth = buf1;
+    auto flip = [&]() {
+        const float* t = cur;
+        cur = oth;
+        oth = const_cast<float*>(t);
+    };
+    // one step cur -> oth, one smem row load + store per output row
+    auto single_step = [&]() {
+        const float* in = cur;
+        float* out = oth;
+        float4 n4 = ldrow(in, rb - 1);
+        float4 c4 = ldrow(in, rb);
+        auto row = [&](int r, const float4& nq, const float4& cq, const float4& sq) {
+            const float4 o4 = calc(nq, cq, sq);
             float* op = out + r * kTbRX + 4 * lane;
             if (!edge) {
-                *reinterpret_cast<float4*>(op) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4*>(op) = o4;
             } else {
+                const float o[4] = {o4.x, o4.y, o4.z, o4.w};
                 const int gy = gy0 + r;
                 const bool rowb = gy <= 0 || gy >= N - 1;
 #pragma unroll
@@ -337,9 +364,74 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
             if (r + 1 < re) row(r + 1, c4, s4, ld(r + 2));
         }
         __syncthreads();
+        flip();
+    };
+
+    if (!edge) {
+        // Interior regions (no global border inside): the odd step first,
+        // then two steps per sweep.  The intermediate state never touches
+        // smem -- each warp recomputes it for its band plus one row on each
+        // side -- so shared-memory traffic and barriers per step are halved
+        // (the single-step sweep is bound by LDS/STS/SHFL bandwidth).
+        // Intermediate values outside the band's cone are garbage exactly
+        // like the halo of the one-step path: the valid area still shrinks
+        // one row/column per step.  The last pair stores the tile centre
+        // straight from registers to HBM (no smem write-back pass).
+        int st = 0;
+        if (steps & 1) {
+            single_step();
+            st = 1;
+        }
+        for (; st + 1 < steps; st += 2) {
+            const bool last = st + 2 == steps;
+            // entry for intermediate row i: X1 = s(i-1), X2 = s(i); M1 = m(i-2), M2 = m(i-1)
+            float4 X1, X2, X3, M1, M2, M3;
+            {
+                const float4 t0 = ldrow(cur, rb - 2), t1 = ldrow(cur, rb - 1);
+                X1 = ldrow(cur, rb);
+                X2 = ldrow(cur, rb + 1);
+                M1 = calc(t0, t1, X1);
+                M2 = calc(t1, X1, X2);
+            }
+            auto put = [&](int r, const float4& v) {
+                if (!last) {
+                    *reinterpret_cast<float4*>(oth + r * kTbRX + 4 * lane) = v;
+                } else if (r >= KT && r < KT + kTbY && lane >= kTbPad / 4 && lane < (kTbPad + kTbX) / 4) {
+                    *reinterpret_cast<float4*>(dst + (int64_t)(gy0 + r) * N + gx) = v;
+                }
+            };
+            int i = rb + 1;  // output row i-1
+            for (; i + 2 <= re; i += 3) {
+                X3 = ldrow(cur, i + 1);
+                M3 = calc(X1, X2, X3);
+                put(i - 1, calc(M1, M2, M3));
+                X1 = ldrow(cur, i + 2);
+                M1 = calc(X2, X3, X1);
+                put(i, calc(M2, M3, M1));
+                X2 = ldrow(cur, i + 3);
+                M2 = calc(X3, X1, X2);
+                put(i + 1, calc(M3, M1, M2));
+            }
+            if (i <= re) {
+                X3 = ldrow(cur, i + 1);
+                M3 = calc(X1, X2, X3);
+                put(i - 1, calc(M1, M2, M3));
+                if (i + 1 <= re) {
+                    X1 = ldrow(cur, i + 2);
+                    M1 = calc(X2, X3, X1);
+                    put(i, calc(M2, M3, M1));
+                }
+            }
+            if (last) return;  // the centre is already in HBM
+            __syncthreads();
+            flip();
+        }
+        // only a one-step launch gets here: its result is in smem
+    } else {
+        for (int st = 0; st < steps; ++st) single_step();
     }
     // write the tile centre (global interior only)
-    const float* fin = (steps & 1) ? buf1 : buf0;
+    const float* fin = cur;
     constexpr int CG = kTbX / 4;
     for (int it = threadIdx.x; it < kTbY * CG; it += kTbThreads) {
         const int r = it / CG, g = it % CG;

@@ -372,6 +372,18 @@ def test_full_jacobi_8192_three_steps():
     np.testing.assert_array_equal(At.cpu().numpy(), ref)
 
 
+def test_full_jacobi_8192_nine_steps_temporal_blocking():
+    """BASELINE size through the temporal-blocking path (one 7-step launch
+    with fused two-step sweeps, a 1-step launch, then the final step)"""
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(5)
+    A = rng.random((2, 8192, 8192), dtype=np.float32)
+    ref = oracle.jacobi2d(A, 9, fp32=True)
+    At = t(A)
+    device.jacobi2d(At, 9)
+    np.testing.assert_array_equal(At.cpu().numpy(), ref)
+
+
 def test_full_spmv_2pow22_rows_sampled():
     from paper_1902_10345_b200 import device
     H = W = 1 << 22
