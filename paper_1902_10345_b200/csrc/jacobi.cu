@@ -20,6 +20,7 @@
 //   * the canonical c,n,s,w,e order is a compile-time fast path; any other
 //     order of up to 9 neighbours runs the same kernel through a select chain.
 #include <algorithm>
+#include <type_traits>
 
 #include "tma.cuh"
 
@@ -238,7 +239,9 @@ int launch_step(const T* src, T* dst, int64_t N, int64_t rows, int64_t g0, int64
 constexpr int kTbRX = 128, kTbPad = 8, kTbX = kTbRX - 2 * kTbPad, kTbY = 96, kTbThreads = 256;
 
 __host__ __device__ constexpr int tb_rows(int k) { return kTbY + 2 * k; }
-__host__ __device__ constexpr size_t tb_smem(int k) { return (size_t)2 * kTbRX * tb_rows(k) * 4 + 128 + 64; }
+// two region buffers + one pad row (the fused sweep may read row RY of a
+// buffer: halo garbage, but it must be inside the allocation) + mbarrier
+__host__ __device__ constexpr size_t tb_smem(int k) { return (size_t)(2 * tb_rows(k) + 1) * kTbRX * 4 + 128 + 64; }
 
 template <int KT>
 __global__ void __launch_bounds__(kTbThreads, 2)
@@ -251,7 +254,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
     extern __shared__ __align__(1024) float tb_smem_f[];
     float* buf0 = tb_smem_f;
     float* buf1 = tb_smem_f + kTbRX * RY;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(tb_smem_f + 2 * kTbRX * RY);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tb_smem_f + (2 * RY + 1) * kTbRX);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int x0 = blockIdx.x * kTbX, y0 = blockIdx.y * kTbY;
@@ -382,49 +385,59 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
             single_step();
             st = 1;
         }
-        for (; st + 1 < steps; st += 2) {
-            const bool last = st + 2 == steps;
+        // one fused pair cur -> oth (LAST: the tile centre -> HBM instead)
+        auto pair = [&](auto last_tag) {
+            constexpr bool LAST = decltype(last_tag)::value;
+            auto ld = [&](int rr) { return *reinterpret_cast<const float4*>(cur + rr * kTbRX + 4 * lane); };
+            auto put = [&](int r, const float4& v) {
+                if constexpr (!LAST) {
+                    *reinterpret_cast<float4*>(oth + r * kTbRX + 4 * lane) = v;
+                } else {
+                    if (r >= KT && r < KT + kTbY && lane >= kTbPad / 4 && lane < (kTbPad + kTbX) / 4)
+                        *reinterpret_cast<float4*>(dst + (int64_t)(gy0 + r) * N + gx) = v;
+                }
+            };
             // entry for intermediate row i: X1 = s(i-1), X2 = s(i); M1 = m(i-2), M2 = m(i-1)
             float4 X1, X2, X3, M1, M2, M3;
             {
                 const float4 t0 = ldrow(cur, rb - 2), t1 = ldrow(cur, rb - 1);
-                X1 = ldrow(cur, rb);
-                X2 = ldrow(cur, rb + 1);
+                X1 = ld(rb);
+                X2 = ld(rb + 1);
                 M1 = calc(t0, t1, X1);
                 M2 = calc(t1, X1, X2);
             }
-            auto put = [&](int r, const float4& v) {
-                if (!last) {
-                    *reinterpret_cast<float4*>(oth + r * kTbRX + 4 * lane) = v;
-                } else if (r >= KT && r < KT + kTbY && lane >= kTbPad / 4 && lane < (kTbPad + kTbX) / 4) {
-                    *reinterpret_cast<float4*>(dst + (int64_t)(gy0 + r) * N + gx) = v;
-                }
-            };
+            // rows read below reach re + 1 <= RY (the pad row): no clamps
             int i = rb + 1;  // output row i-1
             for (; i + 2 <= re; i += 3) {
-                X3 = ldrow(cur, i + 1);
+                X3 = ld(i + 1);
                 M3 = calc(X1, X2, X3);
                 put(i - 1, calc(M1, M2, M3));
-                X1 = ldrow(cur, i + 2);
+                X1 = ld(i + 2);
                 M1 = calc(X2, X3, X1);
                 put(i, calc(M2, M3, M1));
-                X2 = ldrow(cur, i + 3);
+                X2 = ld(i + 3);
                 M2 = calc(X3, X1, X2);
                 put(i + 1, calc(M3, M1, M2));
             }
             if (i <= re) {
-                X3 = ldrow(cur, i + 1);
+                X3 = ld(i + 1);
                 M3 = calc(X1, X2, X3);
                 put(i - 1, calc(M1, M2, M3));
                 if (i + 1 <= re) {
-                    X1 = ldrow(cur, i + 2);
+                    X1 = ld(i + 2);
                     M1 = calc(X2, X3, X1);
                     put(i, calc(M2, M3, M1));
                 }
             }
-            if (last) return;  // the centre is already in HBM
+        };
+        for (; st + 2 < steps; st += 2) {
+            pair(std::false_type{});
             __syncthreads();
             flip();
+        }
+        if (st + 2 == steps) {
+            pair(std::true_type{});
+            return;  // the centre is already in HBM
         }
         // only a one-step launch gets here: its result is in smem
     } else {
