@@ -239,9 +239,16 @@ int launch_step(const T* src, T* dst, int64_t N, int64_t rows, int64_t g0, int64
 constexpr int kTbRX = 128, kTbPad = 8, kTbX = kTbRX - 2 * kTbPad, kTbY = 96, kTbThreads = 256;
 
 __host__ __device__ constexpr int tb_rows(int k) { return kTbY + 2 * k; }
-// two region buffers + one pad row (the fused sweep may read row RY of a
-// buffer: halo garbage, but it must be inside the allocation) + mbarrier
-__host__ __device__ constexpr size_t tb_smem(int k) { return (size_t)(2 * tb_rows(k) + 1) * kTbRX * 4 + 128 + 64; }
+// two region buffers + kTbPadRows pad rows (a fused sweep of F steps may
+// read rows up to RY+F-2 of a buffer: halo garbage, but it must be inside
+// the allocation) + mbarrier
+constexpr int kTbPadRows = 2;
+#ifndef SDFGB_J_F3
+#define SDFGB_J_F3 1  // odd step counts start with a 3-step sweep (else a 1-step one)
+#endif
+__host__ __device__ constexpr size_t tb_smem(int k) {
+    return (size_t)(2 * tb_rows(k) + kTbPadRows) * kTbRX * 4 + 128 + 64;
+}
 
 template <int KT>
 __global__ void __launch_bounds__(kTbThreads, 2)
@@ -254,7 +261,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
     extern __shared__ __align__(1024) float tb_smem_f[];
     float* buf0 = tb_smem_f;
     float* buf1 = tb_smem_f + kTbRX * RY;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(tb_smem_f + (2 * RY + 1) * kTbRX);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tb_smem_f + (2 * RY + kTbPadRows) * kTbRX);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int x0 = blockIdx.x * kTbX, y0 = blockIdx.y * kTbY;
@@ -371,24 +378,22 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
     };
 
     if (!edge) {
-        // Interior regions (no global border inside): the odd step first,
-        // then two steps per sweep.  The intermediate state never touches
-        // smem -- each warp recomputes it for its band plus one row on each
-        // side -- so shared-memory traffic and barriers per step are halved
-        // (the single-step sweep is bound by LDS/STS/SHFL bandwidth).
-        // Intermediate values outside the band's cone are garbage exactly
-        // like the halo of the one-step path: the valid area still shrinks
-        // one row/column per step.  The last pair stores the tile centre
-        // straight from registers to HBM (no smem write-back pass).
-        int st = 0;
-        if (steps & 1) {
-            single_step();
-            st = 1;
-        }
-        // one fused pair cur -> oth (LAST: the tile centre -> HBM instead)
-        auto pair = [&](auto last_tag) {
+        // Interior regions (no global border inside): F steps per sweep.
+        // The intermediate states never touch smem -- each warp recomputes
+        // them for its band plus a shrinking margin -- so shared-memory
+        // traffic and barriers per step drop F-fold (the one-step sweep is
+        // bound by LDS/STS/SHFL bandwidth).  Intermediate values outside
+        // the band's cone are garbage exactly like the halo of the one-step
+        // path: the valid area still shrinks one row/column per step.  The
+        // last sweep stores the tile centre straight from registers to HBM.
+        //
+        // Level k (0 = the sweep's input state) keeps a 3-row window; row r
+        // of level k lives in slot (r + k - base) mod 3, so every sub-step
+        // writes the same slot at every level and the unrolled loop needs no
+        // register moves.  Streaming input row j computes level k row j - k.
+        auto sweep = [&](auto f_tag, auto last_tag) {
+            constexpr int F = decltype(f_tag)::value;
             constexpr bool LAST = decltype(last_tag)::value;
-            auto ld = [&](int rr) { return *reinterpret_cast<const float4*>(cur + rr * kTbRX + 4 * lane); };
             auto put = [&](int r, const float4& v) {
                 if constexpr (!LAST) {
                     *reinterpret_cast<float4*>(oth + r * kTbRX + 4 * lane) = v;
@@ -397,46 +402,62 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
                         *reinterpret_cast<float4*>(dst + (int64_t)(gy0 + r) * N + gx) = v;
                 }
             };
-            // entry for intermediate row i: X1 = s(i-1), X2 = s(i); M1 = m(i-2), M2 = m(i-1)
-            float4 X1, X2, X3, M1, M2, M3;
-            {
-                const float4 t0 = ldrow(cur, rb - 2), t1 = ldrow(cur, rb - 1);
-                X1 = ld(rb);
-                X2 = ld(rb + 1);
-                M1 = calc(t0, t1, X1);
-                M2 = calc(t1, X1, X2);
+            float4 w[F][3];
+            const int j0 = rb - F;  // first input row of the cone
+            // prologue: input rows j0 .. j0+2F-1 fill the windows; level k
+            // row j-k is valid (and computed) once j >= j0 + 2k
+#pragma unroll
+            for (int p = 0; p < 2 * F; ++p) {
+                const int sl = ((p - 2 * F + 1) % 3 + 3) % 3;
+                const int sn = (sl + 1) % 3, sc = (sl + 2) % 3;  // north / centre slots of the level below
+                w[0][sl] = ldrow(cur, j0 + p);
+#pragma unroll
+                for (int k = 1; k < F; ++k)
+                    if (p >= 2 * k) w[k][sl] = calc(w[k - 1][sn], w[k - 1][sc], w[k - 1][sl]);
             }
-            // rows read below reach re + 1 <= RY (the pad row): no clamps
-            int i = rb + 1;  // output row i-1
-            for (; i + 2 <= re; i += 3) {
-                X3 = ld(i + 1);
-                M3 = calc(X1, X2, X3);
-                put(i - 1, calc(M1, M2, M3));
-                X1 = ld(i + 2);
-                M1 = calc(X2, X3, X1);
-                put(i, calc(M2, M3, M1));
-                X2 = ld(i + 3);
-                M2 = calc(X3, X1, X2);
-                put(i + 1, calc(M3, M1, M2));
+            // main stream: input row j = i + 1 + u produces output row j - F
+            auto sub = [&](int i, int u) {
+                const int sl = (1 + u) % 3, sn = (u + 2) % 3, sc = u % 3;  // south (new) / north / centre
+                w[0][sl] = *reinterpret_cast<const float4*>(cur + (i + 1 + u) * kTbRX + 4 * lane);
+#pragma unroll
+                for (int k = 1; k < F; ++k) w[k][sl] = calc(w[k - 1][sn], w[k - 1][sc], w[k - 1][sl]);
+                put(i + 1 + u - F, calc(w[F - 1][sn], w[F - 1][sc], w[F - 1][sl]));
+            };
+            int i = j0 + 2 * F - 1;  // rows read below reach re-1+F <= RY-2+F: the pad rows
+            for (; i + 3 - F <= re - 1; i += 3) {
+                sub(i, 0);
+                sub(i, 1);
+                sub(i, 2);
             }
-            if (i <= re) {
-                X3 = ld(i + 1);
-                M3 = calc(X1, X2, X3);
-                put(i - 1, calc(M1, M2, M3));
-                if (i + 1 <= re) {
-                    X1 = ld(i + 2);
-                    M1 = calc(X2, X3, X1);
-                    put(i, calc(M2, M3, M1));
+            if (i + 1 - F <= re - 1) sub(i, 0);
+            if (i + 2 - F <= re - 1) sub(i, 1);
+        };
+        int st = 0;
+        auto run = [&](auto f_tag) {
+            constexpr int F = decltype(f_tag)::value;
+            if (st + F == steps) {
+                sweep(f_tag, std::true_type{});
+            } else {
+                sweep(f_tag, std::false_type{});
+                __syncthreads();
+                flip();
+            }
+            st += F;
+        };
+        // KT = 7 -> 3 + 2 + 2;  5 -> 3 + 2;  3 -> 3
+        if (steps == 1) {
+            single_step();
+            st = 1;
+        } else {
+            if (steps & 1) {
+                if (SDFGB_J_F3) {
+                    run(std::integral_constant<int, 3>{});
+                } else {
+                    single_step();
+                    st = 1;
                 }
             }
-        };
-        for (; st + 2 < steps; st += 2) {
-            pair(std::false_type{});
-            __syncthreads();
-            flip();
-        }
-        if (st + 2 == steps) {
-            pair(std::true_type{});
+            while (st < steps) run(std::integral_constant<int, 2>{});
             return;  // the centre is already in HBM
         }
         // only a one-step launch gets here: its result is in smem
