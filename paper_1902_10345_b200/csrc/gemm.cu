@@ -90,6 +90,9 @@ constexpr int GEMM_THREADS = 256;
 #ifndef SDFGB_GEMM_NACC
 #define SDFGB_GEMM_NACC 4
 #endif
+#ifndef SDFGB_GEMM_GROUP
+#define SDFGB_GEMM_GROUP 16
+#endif
 #ifndef SDFGB_GEMM_TMEM_COLS
 #define SDFGB_GEMM_TMEM_COLS (BN * SDFGB_GEMM_NACC)
 #endif
@@ -109,7 +112,20 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_consta
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    // grouped rasterisation: consecutive CTAs cover SDFGB_GEMM_GROUP tile rows
+    // x a few tile columns, so a wave of co-resident CTAs shares ~26 operand
+    // panels instead of ~5 A + 148 B panels (row-major order re-read every B
+    // panel from DRAM once per tile row: ~280 GB at 16384^3)
+    int m0, n0;
+    {
+        const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+        const int pid = blockIdx.x, group = SDFGB_GEMM_GROUP * tiles_n;
+        const int first_m = (pid / group) * SDFGB_GEMM_GROUP;
+        const int gm = min(tiles_m - first_m, SDFGB_GEMM_GROUP);
+        const int in_group = pid % group;
+        m0 = (first_m + in_group % gm) * BM;
+        n0 = (in_group / gm) * BN;
+    }
     const int KB = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
@@ -305,7 +321,7 @@ extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t 
         attr_err = cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
     });
     SDFGB_CUDA(attr_err);
-    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+    dim3 grid((unsigned)(((N + BN - 1) / BN) * ((M + BM - 1) / BM)));
     gemm_3xtf32_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, s>>>(mAhi, mAlo, mBhi, mBlo, C, (int)M, (int)N, (int)K);
     SDFGB_LAUNCHED("gemm_3xtf32_kernel");
     return SDFGB_OK;

@@ -62,3 +62,12 @@ elif motif == "jacobi2d":
     us = timed(lambda k: device.jacobi2d(A, T), reps=3)
     per = 4 * N * N + 4 * (N - 2) * (N - 2)
     print(f"{name:28s} jacobi {us / T:7.2f} us/step {per * T / us / 1e3:6.0f} GB/s")
+elif motif == "gemm":
+    for n in (4096, 16384):
+        A = torch.rand(n, n, device="cuda")
+        B = torch.rand(n, n, device="cuda")
+        C = torch.empty(n, n, device="cuda")
+        ws = device.gemm_workspace(n, n, n, "cuda")
+        us = timed(lambda k: device.gemm(A, B, C, ws), reps=10 if n == 4096 else 2)
+        print(f"{name:28s} gemm{n:<6d} {us:9.1f} us {2 * n ** 3 / us / 1e6:6.1f} TF/s")
+        del A, B, C, ws
