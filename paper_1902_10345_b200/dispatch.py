@@ -72,14 +72,18 @@ def marked_precision(g: Graph, plan: Plan) -> Optional[str]:
 
 @dataclass
 class GeneratedB200Code:
-    """Counterpart of ``GeneratedCode`` (codegen.py:146-156)."""
+    """Counterpart of ``GeneratedCode`` (codegen.py:146-156).  ``plan`` is
+    the motif binding; graphs outside the five motifs carry ``lowered``
+    (the generic Map/tasklet -> CUDA translation unit, lower.py) instead."""
     source: str
     name: str
     pointer_args: list
     symbol_args: list
-    plan: Plan
+    plan: Optional[Plan]
     precision: str
     stream_order: str = "any"
+    lowered: Any = None
+    graph: Any = None
 
     def signature(self) -> str:
         parts = [f"{_CT[t]}* {n}" for n, t in self.pointer_args]
@@ -115,7 +119,7 @@ def generate(sdfg: Any, require_marked: bool = True) -> GeneratedB200Code:
     try:
         plan = classify(g)
     except UnsupportedGraph as exc:
-        raise CodegenError(str(exc)) from exc
+        return _generate_generic(g, require_marked, exc)
     mode = marked_mode(g, plan)
     if mode is None:
         if require_marked:
@@ -132,9 +136,48 @@ def generate(sdfg: Any, require_marked: bool = True) -> GeneratedB200Code:
                              plan, prec, order)
 
 
+def generic_marked(g: Graph) -> Optional[tuple]:
+    """(precision, stream_order) from the non-transient containers of a
+    graph outside the motifs; None when any of them is unmarked."""
+    seen = set()
+    for d in g.data.values():
+        if d.transient:
+            continue
+        st = d.storage or ""
+        if not st.startswith(STORAGE_PREFIX):
+            return None
+        seen.add(_parse_storage(st))
+    if len(seen) > 1:
+        raise CodegenError(f"inconsistent GPU storage markers {sorted(seen)}")
+    return seen.pop() if seen else None
+
+
+def _generate_generic(g: Graph, require_marked: bool, why: Exception) -> GeneratedB200Code:
+    """Graphs that are none of the five motifs go through the generic
+    Map/tasklet lowering (lower.py).  It computes in the
+    reference's basetypes (float64/int64) whatever precision was marked."""
+    from .lower import LoweringError, lower
+    mode = generic_marked(g)
+    if mode is None and require_marked:
+        raise CodegenError(
+            f"SDFG '{g.name}' has no state matched by GPUTransformMap; apply the "
+            f"transformation before generating B200 code")
+    try:
+        lw = lower(g)
+    except LoweringError as exc:
+        raise CodegenError(f"SDFG '{g.name}': not a motif ({why}) and not lowerable: {exc}") from exc
+    order = mode[1] if mode else "any"
+    return GeneratedB200Code(lw.source, g.name, lw.pointer_args, lw.symbol_args, None, "native", order,
+                             lowered=lw, graph=g)
+
+
 def invoke_toolchain(code: GeneratedB200Code) -> "CompiledB200Sdfg":
     """Load the prebuilt sm_100a library (the reference compiles with cc
-    here, codegen.py:890-913; our kernels are built once by build())."""
+    here, codegen.py:890-913; our kernels are built once by build()).
+    Generic programs are compiled with nvcc for sm_100a (generic.py)."""
+    if code.lowered is not None:
+        from .generic import GenericProgram, build
+        return GenericProgram(code.graph, code.lowered, build(code.lowered))
     try:
         lib = _lib.load()
     except _lib.BackendUnavailable as exc:

@@ -1,0 +1,137 @@
+"""Compile and run SDFGs through the generic Map/tasklet -> CUDA lowering
+(lower.py): the B200 counterpart of the reference's ``generate`` +
+``invoke_toolchain`` + ``CompiledSdfg.run`` (codegen.py:802-913) for graphs
+that are not one of the five motif kernels.
+
+The generated translation unit is compiled with nvcc for sm_100a into an
+in-tree cache (``_gen/``, keyed by the source digest), loaded with ctypes,
+and called with device pointers; containers keep the reference's basetypes
+(float64/int64).  ``run`` has ``CompiledSdfg.run``'s contract: every
+non-transient array is copied into a contiguous buffer of its declared
+type, the program executes on the GPU, and the buffers come back.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import shutil
+import subprocess
+import threading
+from typing import Any, Mapping
+
+import numpy as np
+
+from . import expr as X
+from .errors import CodegenError, ExecutionError, OutOfBoundsError, ToolchainError
+from .graph import Graph, load
+from .lower import Lowered, lower
+
+GEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_gen")
+_LOCK = threading.Lock()
+_STATUS = {1: (OutOfBoundsError, "subscript write out of bounds"),
+           2: (ExecutionError, "subscript read out of bounds"),
+           3: (ExecutionError, "stream overflow"),
+           4: (OutOfBoundsError, "stream drain overflows its target array")}
+
+
+def nvcc() -> str:
+    for c in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if c and os.path.exists(c):
+            return c
+    raise ToolchainError("nvcc not found (the generic lowering compiles with nvcc for sm_100a)")
+
+
+def build(lowered: Lowered) -> str:
+    """nvcc -> _gen/<name>_<digest>.so (reused when present)."""
+    os.makedirs(GEN_DIR, exist_ok=True)
+    # -fmad=false: no a*b+c contraction, so float64 results match the
+    # reference's gcc -O2 build and its interpreter bit for bit
+    flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
+             "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared"]
+    key = hashlib.sha256((lowered.source + " ".join(flags)).encode()).hexdigest()[:16]
+    base = os.path.join(GEN_DIR, f"{lowered.name}_{key}")
+    so = base + ".so"
+    with _LOCK:
+        if os.path.exists(so):
+            return so
+        cu = base + ".cu"
+        with open(cu, "w") as f:
+            f.write(lowered.source)
+        tmp = f"{so}.{os.getpid()}.tmp"
+        cmd = [nvcc()] + flags + ["-o", tmp, cu, "-lcudart"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise ToolchainError(f"nvcc failed for '{lowered.name}':\n{r.stderr}")
+        os.replace(tmp, so)
+    return so
+
+
+class GenericProgram:
+    """A lowered, compiled SDFG; ``run`` mirrors CompiledSdfg.run."""
+
+    def __init__(self, g: Graph, lowered: Lowered, so_path: str):
+        self.graph = g
+        self.lowered = lowered
+        self.path = so_path
+        self._lib = ctypes.CDLL(so_path)
+        self._fn = getattr(self._lib, lowered.entry)
+        self._fn.restype = ctypes.c_int
+        self._fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
+
+    @property
+    def pointer_args(self):
+        return self.lowered.pointer_args
+
+    @property
+    def symbol_args(self):
+        return self.lowered.symbol_args
+
+    def run(self, arrays: Mapping[str, Any], symbols: Mapping[str, int]) -> dict:
+        import torch
+        if not torch.cuda.is_available():
+            raise ExecutionError("the generic B200 path needs a CUDA device")
+        g = self.graph
+        syms = {k: int(v) for k, v in symbols.items()}
+        missing = [s for s in self.symbol_args if s not in syms]
+        if missing:
+            raise ExecutionError(f"unbound symbols: {sorted(missing)}")
+        bufs, dev = {}, []
+        for name, bt in self.pointer_args:
+            if name not in arrays:
+                raise ExecutionError(f"missing input container '{name}'")
+            dt = np.int64 if bt == "int64" else np.float64
+            buf = np.ascontiguousarray(np.asarray(arrays[name], dtype=dt)).copy()
+            want = 1
+            for d in g.data[name].dims:
+                want *= int(X.evaluate(d, syms))
+            if buf.size != want:
+                raise ExecutionError(f"input '{name}' has {buf.size} elements; container expects {want}")
+            bufs[name] = buf
+            t = torch.from_numpy(buf.reshape(-1)).to("cuda") if buf.size else \
+                torch.empty(1, dtype=torch.float64 if bt == "float64" else torch.int64, device="cuda")
+            dev.append(t)
+        ptrs = (ctypes.c_void_p * max(1, len(dev)))(*[t.data_ptr() for t in dev])
+        svals = (ctypes.c_int64 * max(1, len(self.symbol_args)))(*[syms[s] for s in self.symbol_args])
+        status = ctypes.c_int(0)
+        stream = torch.cuda.current_stream().cuda_stream
+        rc = self._fn(ctypes.cast(ptrs, ctypes.c_void_p), ctypes.cast(svals, ctypes.c_void_p),
+                      ctypes.c_void_p(stream), ctypes.byref(status))
+        if rc != 0:
+            raise ExecutionError(f"generic program '{g.name}' failed on the device (cuda status {-status.value})")
+        if status.value:
+            exc, msg = _STATUS.get(status.value, (ExecutionError, f"device error {status.value}"))
+            raise exc(f"{msg} in '{g.name}'")
+        for (name, _), t in zip(self.pointer_args, dev):
+            if bufs[name].size:
+                bufs[name].reshape(-1)[:] = t.cpu().numpy()
+        return bufs
+
+
+def compile_generic(sdfg: Any) -> GenericProgram:
+    """Lower + nvcc + load.  CodegenError for constructs the lowering does
+    not cover (consume scopes, custom WCR, vector memlets)."""
+    g = load(sdfg)
+    lw = lower(g)
+    return GenericProgram(g, lw, build(lw))

@@ -50,12 +50,34 @@ def build_rule(engine, matching, ir):
             except (UnsupportedGraph, ValueError, KeyError):
                 return None
 
+        def _generic(self, sdfg):
+            """A graph outside the motifs the generic lowering accepts: the
+            rule matches its first top-level map (state order, node order)."""
+            from .lower import LoweringError, lower
+            try:
+                g = load(sdfg)
+                lower(g)
+            except (LoweringError, ValueError, KeyError):
+                return None
+            for st in g.states:
+                parent = st.scope_parent()
+                for n in st.nodes:
+                    if n.kind == "map_entry" and parent[n.id] is None:
+                        return g, st.name, n.id
+            return None
+
         def can_be_applied(self, sdfg, state, match, strict=False):
             plan = self._plan(sdfg)
-            if plan is None or plan.main_state != state.name:
+            entry = match.nodes["map"]
+            if plan is None:
+                gen = self._generic(sdfg)
+                if gen is None or gen[1] != state.name or sorted(state.nodes).index(entry) != gen[2]:
+                    return False
+                return not all((d.storage or "").startswith(STORAGE_PREFIX)
+                               for d in sdfg.data.values() if not d.transient)
+            if plan.main_state != state.name:
                 return False
             # to_json renumbers node ids densely in id order (serialization.py:113-116)
-            entry = match.nodes["map"]
             if sorted(state.nodes).index(entry) != plan.main_map:
                 return False
             return not all((sdfg.data[c].storage or "").startswith(STORAGE_PREFIX)
@@ -69,10 +91,15 @@ def build_rule(engine, matching, ir):
             if order not in STREAM_ORDERS:
                 raise ValueError(f"stream_order must be one of {STREAM_ORDERS}, not '{order}'")
             plan = self._plan(sdfg)
-            if plan is None:
-                raise ValueError("GPUTransformMap: program is not a B200 motif")
-            for c in set(plan.roles.values()):
-                sdfg.data[c].storage = gpu_storage(prec, order)
+            if plan is not None:
+                for c in set(plan.roles.values()):
+                    sdfg.data[c].storage = gpu_storage(prec, order)
+                return
+            if self._generic(sdfg) is None:
+                raise ValueError("GPUTransformMap: program is neither a B200 motif nor lowerable")
+            for name, d in sdfg.data.items():
+                if not d.transient:
+                    d.storage = gpu_storage(prec, order)
 
     return GPUTransformMap
 

@@ -230,7 +230,40 @@ def matmul_cases():
                    "C": np.zeros((6, 9))}, {"M": 6, "N": 9, "K": 5})
 
 
+def gallery_cases():
+    """The reference gallery (gallery.py:55-545) for the generic lowering:
+    graphs gal_<name>, inputs from each fixture's own make_inputs plus a
+    few larger / edge cases, outputs from the interpreter."""
+    from sdfg import gallery
+    for name in gallery.fixture_names():
+        fx = gallery.fixture(name)
+        save_graph(f"gal_{name}", fx.sdfg)
+        for seed in (0, 1, 2):
+            arrays, symbols = fx.make_inputs(np.random.default_rng(100 + seed))
+            save_case(f"gal_{name}", f"seed{seed}", fx.sdfg, arrays, symbols)
+    rng = np.random.default_rng(7)
+    g = gallery.fixture("laplace").sdfg
+    save_case("gal_laplace", "n300_t9", g, {"A": rng.random((2, 300))}, {"N": 300, "T": 9})
+    g = gallery.fixture("mandelbrot").sdfg
+    save_case("gal_mandelbrot", "12x9_k40", g,
+              {"CR": rng.uniform(-2, 0.5, 12), "CI": rng.uniform(-1.2, 1.2, 9),
+               "IT": np.zeros((9, 12), dtype=np.int64)}, {"W": 12, "H": 9, "K": 40})
+    g = gallery.fixture("indirection").sdfg
+    save_case("gal_indirection", "w50_m200", g,
+              {"x": rng.random(50), "ind": rng.integers(0, 50, 200), "y": np.zeros(200)}, {"W": 50, "M": 200})
+    save_case("gal_indirection", "oob", g,
+              {"x": rng.random(5), "ind": np.array([0, 7, 2]), "y": np.zeros(3)}, {"W": 5, "M": 3})
+    g = gallery.fixture("histogram").sdfg
+    fx = gallery.fixture("histogram")
+    arrays, symbols = fx.make_inputs(np.random.default_rng(11))
+    save_case("gal_histogram", "again", g, arrays, symbols)
+    for a in (0, 3, -1):
+        save_case("gal_branching", f"a{a}".replace("-", "m"), gallery.fixture("branching").sdfg,
+                  {"a": np.array([a], dtype=np.int64), "out": np.zeros(1, dtype=np.int64)}, {})
+
+
 if __name__ == "__main__":
+    gallery_cases()
     histogram_cases()
     query_cases()
     spmv_cases()
