@@ -115,11 +115,13 @@ def test_classified_parameters():
     assert s.pointer_args[0] == ("A_row", "int64") and s.symbol_args == ["H", "W", "nnz"]
 
 
-def test_unsupported_program_raises_codegen_error():
+def test_non_motif_programs_take_the_generic_lowering():
     with pytest.raises(UnsupportedGraph):
-        classify(load(graph_path("laplace1d")))  # 1-D 'l - 2*c + r' stencil: no kernel
-    with pytest.raises(b200.CodegenError):
-        b200.generate(graph_path("laplace1d"), require_marked=False)
+        classify(load(graph_path("laplace1d")))  # 1-D 'l - 2*c + r' stencil: no motif kernel
+    code = b200.generate(graph_path("laplace1d"), require_marked=False)
+    assert code.plan is None and code.lowered is not None
+    with pytest.raises(b200.CodegenError):  # consume scopes: neither motif nor lowerable
+        b200.generate(graph_path("gal_fibonacci"), require_marked=False)
 
 
 def test_mutated_programs_are_rejected():
