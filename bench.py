@@ -37,7 +37,7 @@ sys.path.insert(0, REPO)
 
 METRIC = "per-motif GB/s (hist/query/SpMV/Jacobi), MM TFLOP/s vs roofline, 1/2/4/8 GPU"
 HEADLINE = "query"
-ALL = ["histogram", "query", "spmv", "jacobi2d", "gemm4096", "gemm16384"]
+ALL = ["histogram", "query", "spmv", "jacobi2d", "gemm4096", "gemm16384", "generic_laplace", "generic_mandelbrot"]
 
 
 def peaks():
@@ -412,6 +412,55 @@ def bench_jacobi(args, dist, P):
     return res
 
 
+def _gallery_program(name):
+    from paper_1902_10345_b200.generic import compile_generic
+    return compile_generic(os.path.join(REPO, "tests", "golden", "graphs", f"gal_{name}.sdfg.json"))
+
+
+def bench_generic_laplace(args, dist, P):
+    """Reference gallery 'laplace' (gallery.py:60-105: 3-point stencil in a
+    guard loop over A[2, N]) through the generic Map -> CUDA lowering:
+    float64 as the reference declares it, one kernel per time step."""
+    import torch
+    N, T = 1 << 24, 20
+    prog = _gallery_program("laplace")
+    g = torch.Generator(device="cuda").manual_seed(5 + dist.rank)
+    A = torch.rand(2, N, device="cuda", dtype=torch.float64, generator=g)
+
+    def step(k):
+        prog.run_device([A], {"N": N, "T": T})
+    ms = time_steps(step, max(1, min(args.steps, 5)), args.warmup, dist)
+    per = 8 * N + 8 * (N - 2)
+    kern = [k for k in prog.lowered.source.split() if k.startswith("gen_laplace_k")][0].split("(")[0]
+    return {"value": dist.world * per * T / ms / 1e6, "unit": "GB/s", "ms_per_step": ms, "bytes_per_unit": per * T,
+            "launches_per_step": T + 0, "roofline": roof("hbm", per * T / ms / 1e6, P, kern),
+            "l2": "2 x 128 MiB planes > L2", "path": "generic lowering (lower.py), nvcc -fmad=false",
+            "config": {"workload": "gallery laplace, A[2, 2^24] float64, T=20 (generic path)", "N": N, "T": T}}
+
+
+def bench_generic_mandelbrot(args, dist, P):
+    """Reference gallery 'mandelbrot' (gallery.py:461-545: a nested per-pixel
+    convergence loop under a 2-D map) through the generic lowering: the
+    nested graph is a __device__ state machine per map iteration."""
+    import torch
+    W, H, K = 2048, 2048, 256
+    prog = _gallery_program("mandelbrot")
+    CR = torch.linspace(-2.0, 0.5, W, device="cuda", dtype=torch.float64)
+    CI = torch.linspace(-1.2, 1.2, H, device="cuda", dtype=torch.float64)
+    IT = torch.zeros(H, W, device="cuda", dtype=torch.int64)
+
+    def step(k):
+        prog.run_device([CR, CI, IT], {"W": W, "H": H, "K": K})
+    ms = time_steps(step, max(1, min(args.steps, 5)), args.warmup, dist)
+    iters = int(IT.sum().item())
+    return {"value": dist.world * iters / ms / 1e6, "unit": "Giter/s", "ms_per_step": ms,
+            "bytes_per_unit": None, "launches_per_step": 1,
+            "roofline": {"bound": "fp64", "achieved": None, "peak": None, "frac": None,
+                         "note": "data-dependent trip counts; compared with the reference CPU only"},
+            "iterations": iters, "path": "generic lowering (lower.py), nvcc -fmad=false",
+            "config": {"workload": "gallery mandelbrot 2048x2048, K=256 (generic path)", "W": W, "H": H, "K": K}}
+
+
 def bench_gemm(n, args, dist, P):
     import torch
     from paper_1902_10345_b200 import device, _lib
@@ -659,8 +708,38 @@ def cpu_gemm(n, rows):
                       f"(paper §5.2), {T} threads x row blocks", "seconds": best}
 
 
+def cpu_generic_laplace(steps=4):
+    """The reference's generated C for gallery laplace, cpu_parallel schedule
+    (-fopenmp, all host cores), on the bench's N for a few of its steps."""
+    fn = ref_lib("gal_laplace_omp")
+    if fn is None:
+        return {"error": "oracle/_ref not built"}
+    N = 1 << 24
+    A = np.random.default_rng(5).random((2, N))
+    best = _best(lambda: fn(_P(A), _I(N), _I(steps)), 1)
+    per = 8 * N + 8 * (N - 2)
+    return {"value": per * steps / best / 1e9, "unit": "GB/s", "cores": _threads(), "kind": "reference",
+            "sample": f"gal_laplace_omp (cpu_parallel, -fopenmp, {_threads()} threads), {steps} of 20 steps",
+            "seconds": best}
+
+
+def cpu_generic_mandelbrot():
+    fn = ref_lib("gal_mandelbrot_omp")
+    if fn is None:
+        return {"error": "oracle/_ref not built"}
+    W, H, K = 2048, 256, 256  # 256 of the 2048 rows
+    CR = np.linspace(-2.0, 0.5, W)
+    CI = np.linspace(-1.2, 1.2, 2048)[896:896 + H].copy()
+    IT = np.zeros((H, W), np.int64)
+    best = _best(lambda: fn(_P(CR), _P(CI), _P(IT), _I(W), _I(H), _I(K)), 1)
+    return {"value": int(IT.sum()) / best / 1e9, "unit": "Giter/s", "cores": _threads(), "kind": "reference",
+            "sample": f"gal_mandelbrot_omp (cpu_parallel, {_threads()} threads), rows 896..1151 of 2048",
+            "seconds": best}
+
+
 CPU = {"histogram": cpu_histogram, "query": cpu_query, "spmv": cpu_spmv, "jacobi2d": cpu_jacobi,
-       "gemm4096": lambda: cpu_gemm(4096, 2 * _threads()), "gemm16384": lambda: cpu_gemm(16384, _threads())}
+       "gemm4096": lambda: cpu_gemm(4096, 2 * _threads()), "gemm16384": lambda: cpu_gemm(16384, _threads()),
+       "generic_laplace": cpu_generic_laplace, "generic_mandelbrot": cpu_generic_mandelbrot}
 
 
 # ---------------------------------------------------------------- main
@@ -724,6 +803,10 @@ def main():
                 results[m] = bench_jacobi(args, dist, P)
             elif m.startswith("gemm"):
                 results[m] = bench_gemm(int(m[4:]), args, dist, P)
+            elif m == "generic_laplace":
+                results[m] = bench_generic_laplace(args, dist, P)
+            elif m == "generic_mandelbrot":
+                results[m] = bench_generic_mandelbrot(args, dist, P)
             torch.cuda.empty_cache()
     clocks = clk.summary()
     h = results[HEADLINE]
@@ -743,6 +826,7 @@ def main():
             except Exception as exc:  # a CPU sample must not sink the GPU line
                 results[m]["cpu_baseline"] = {"error": str(exc)[:200]}
         line["cpu_baseline"] = results[HEADLINE]["cpu_baseline"]
+        line["motifs"] = {k: dict(v) for k, v in results.items()}
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
     dist.close()

@@ -53,6 +53,19 @@ def main() -> int:
             if isinstance(n, MapEntry):
                 n.schedule = "cpu_parallel"
     graphs["jacobi2d_omp"] = jp
+    # generic-lowering workloads (reference gallery, gallery.py:60-105, :498-545)
+    from sdfg import gallery  # noqa: E402
+    for name in ("laplace", "mandelbrot"):
+        g = gallery.fixture(name).sdfg
+        g.name = f"gal_{name}"
+        graphs[f"gal_{name}"] = g
+        go = gallery.fixture(name).sdfg
+        go.name = f"gal_{name}_omp"
+        for st in go.states:
+            for n in st.nodes.values():
+                if isinstance(n, MapEntry):
+                    n.schedule = "cpu_parallel"
+        graphs[f"gal_{name}_omp"] = go
 
     manifest = {}
     for key, g in graphs.items():

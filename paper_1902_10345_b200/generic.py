@@ -129,6 +129,31 @@ class GenericProgram:
         return bufs
 
 
+    def run_device(self, tensors: list, symbols: Mapping[str, int], stream=None) -> None:
+        """Execute on device-resident containers (torch tensors in
+        pointer_args order, contiguous, float64/int64): the timed path."""
+        import torch
+        syms = {k: int(v) for k, v in symbols.items()}
+        if len(tensors) != len(self.pointer_args):
+            raise ExecutionError(f"expected {len(self.pointer_args)} containers, got {len(tensors)}")
+        for (name, bt), t in zip(self.pointer_args, tensors):
+            want = torch.float64 if bt == "float64" else torch.int64
+            if t.dtype != want or not t.is_cuda or not t.is_contiguous():
+                raise ExecutionError(f"container '{name}' must be a contiguous CUDA {want} tensor")
+        ptrs = (ctypes.c_void_p * max(1, len(tensors)))(*[t.data_ptr() for t in tensors])
+        svals = (ctypes.c_int64 * max(1, len(self.symbol_args)))(*[syms[s] for s in self.symbol_args])
+        status = ctypes.c_int(0)
+        st = stream if stream is not None else torch.cuda.current_stream()
+        rc = self._fn(ctypes.cast(ptrs, ctypes.c_void_p), ctypes.cast(svals, ctypes.c_void_p),
+                      ctypes.c_void_p(st.cuda_stream), ctypes.byref(status))
+        if rc != 0:
+            raise ExecutionError(f"generic program '{self.graph.name}' failed on the device "
+                                 f"(cuda status {-status.value})")
+        if status.value:
+            exc, msg = _STATUS.get(status.value, (ExecutionError, f"device error {status.value}"))
+            raise exc(f"{msg} in '{self.graph.name}'")
+
+
 def compile_generic(sdfg: Any) -> GenericProgram:
     """Lower + nvcc + load.  CodegenError for constructs the lowering does
     not cover (consume scopes, custom WCR, vector memlets)."""
