@@ -33,7 +33,8 @@ _LOCK = threading.Lock()
 _STATUS = {1: (OutOfBoundsError, "subscript write out of bounds"),
            2: (ExecutionError, "subscript read out of bounds"),
            3: (ExecutionError, "stream overflow"),
-           4: (OutOfBoundsError, "stream drain overflows its target array")}
+           4: (OutOfBoundsError, "stream drain overflows its target array"),
+           5: (ExecutionError, "consume scope made no progress (watchdog)")}
 
 
 def nvcc() -> str:

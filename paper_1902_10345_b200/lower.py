@@ -39,8 +39,12 @@ for a GPU (not translated from them):
 * the top-level state machine runs on the host: conditions over symbols are
   host arithmetic, conditions over size-1 containers read them back.
 
-Not lowered (CodegenError): consume scopes, custom WCR functions,
-vectorised (tile > 1) memlets, stream pops inside tasklets.
+* a consume scope draining its stream (``size(S) > 0``) is a persistent
+  work-queue kernel: tickets, per-item ready flags, and quiescence when every
+  pushed item has finished (codegen.py:526-543 runs P sequential workers).
+
+Not lowered (CodegenError): other consume conditions, custom WCR functions,
+vectorised (tile > 1) memlets, stream pops outside consume scopes.
 """
 
 from __future__ import annotations
@@ -56,6 +60,7 @@ from .graph import Graph, State, from_json
 
 CT = {"int64": "int64_t", "float64": "double"}
 MAX_PRIVATE = 4096  # elements of a per-iteration private transient
+QUEUE_ITEMS = int(__import__("os").environ.get("SDFGB_GEN_QUEUE", 1 << 22))  # work-queue stream capacity
 
 
 class LoweringError(CodegenError):
@@ -126,13 +131,47 @@ template <typename T> GEN_HD void pwcr_min(T* p, T v) { *p = v < *p ? v : *p; }
 template <typename T> GEN_HD void pwcr_max(T* p, T v) { *p = v > *p ? v : *p; }
 
 // first error wins: 1 = out-of-bounds subscript write, 2 = out-of-bounds
-// subscript read, 3 = stream overflow, 4 = drain overflows its target
+// subscript read, 3 = stream overflow, 4 = drain overflows its target,
+// 5 = a consume worker waited past its watchdog
 GEN_DEV void gen_fail(int* err, int code) { atomicCAS(err, 0, code); }
 
 template <typename T>
 GEN_DEV void stream_push(T* buf, unsigned long long* cnt, int64_t cap, T v, int* err) {
     const unsigned long long i = atomicAdd(cnt, 1ull);
     if ((int64_t)i < cap) buf[i] = v; else gen_fail(err, 3);
+}
+
+// work-queue streams (consumed by a consume scope): items carry a ready
+// flag; q[0] = next ticket, q[1] = items finished (pushes of an item happen
+// before it counts as finished, so finished == pushed means quiescence)
+GEN_DEV unsigned ld_acq_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+GEN_DEV unsigned long long ld_acq_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+template <typename T>
+GEN_DEV void stream_push_q(T* buf, unsigned long long* cnt, int64_t cap, unsigned* ready,
+                           unsigned long long* q, T v, int* err) {
+    const unsigned long long i = atomicAdd(cnt, 1ull);
+    if ((int64_t)i < cap) {
+        buf[i] = v;
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + i), "r"(1u) : "memory");
+    } else {
+        gen_fail(err, 3);
+        atomicAdd(q + 1, 1ull);  // the lost item counts as finished: quiescence stays reachable
+    }
+}
+__global__ void gen_queue_reset(unsigned* ready, unsigned long long* cnt, unsigned long long* q, int64_t cap) {
+    const unsigned long long n = *cnt;
+    const int64_t m = (int64_t)n < cap ? (int64_t)n : cap;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        ready[i] = 0u;
 }
 
 template <typename T>
@@ -444,6 +483,14 @@ class Lowering:
         self.kcount = 0
         self.tcount = 0
         self.private = self._find_private()
+        self.consumed = set()
+        for st in g.states:
+            for n in st.nodes:
+                if n.kind == "consume_entry":
+                    for e in st.in_edges(n.id):
+                        if e.dst_conn == "IN_stream" and not e.memlet.is_empty:
+                            self.consumed.add(e.memlet.data)
+        self.pop_vars: dict = {}  # stream -> C variable of the element a consume worker popped
 
     # -- containers ---------------------------------------------------------
 
@@ -512,6 +559,8 @@ class Lowering:
             if d.kind == "stream":
                 ps += [f"{CT[d.basetype]}* {self.cname(name)}", f"unsigned long long* n_{_ident(name)}",
                        f"int64_t cap_{_ident(name)}"]
+                if name in self.consumed:
+                    ps += [f"unsigned* r_{_ident(name)}", f"unsigned long long* q_{_ident(name)}"]
             else:
                 ps.append(f"{CT[d.basetype]}* {self.cname(name)}")
         ps += [f"int64_t s_{_ident(s)}" for s in self.sym_names]
@@ -525,6 +574,8 @@ class Lowering:
                 continue
             if d.kind == "stream":
                 a += [self.cname(name), f"n_{_ident(name)}", f"cap_{_ident(name)}"]
+                if name in self.consumed:
+                    a += [f"r_{_ident(name)}", f"q_{_ident(name)}"]
             else:
                 a.append(self.cname(name))
         a += [f"s_{_ident(s)}" for s in self.sym_names]
@@ -564,7 +615,7 @@ class Lowering:
                 self.emit_access_device(st, n, env, ind, out)
             elif n.kind == "nested":
                 self.emit_nested_call(st, n, env, ind, out)
-            elif n.kind in ("map_exit",):
+            elif n.kind in ("map_exit", "consume_exit"):
                 continue
             else:
                 raise LoweringError(f"'{n.kind}' nodes are not lowered inside a map scope")
@@ -657,7 +708,12 @@ class Lowering:
             d = self.g.data[m.data]
             types[c] = d.basetype
             if d.kind == "stream":
-                raise LoweringError("stream pops inside tasklets are not lowered (consume scopes)")
+                if st.nodes[e.src].kind == "consume_entry" and m.data in self.pop_vars:
+                    v = f"k{t}_{_ident(c)}"
+                    out.append(f"{ind2}const {CT[d.basetype]} {v} = {self.pop_vars[m.data]};")
+                    names[c] = v
+                    continue
+                raise LoweringError("stream pops outside a consume scope are not lowered")
             if any(not _is_one(r.tile) for r in m.subset):
                 raise LoweringError("vectorised memlets are not lowered")
             v = f"k{t}_{_ident(c)}"
@@ -711,7 +767,11 @@ class Lowering:
                 guard = f"if ({v}__set) " if m.is_dynamic else ""
                 if td.kind == "stream":
                     s = _ident(target.data)
-                    out.append(f"{ind2}{guard}stream_push({self.cname(target.data)}, n_{s}, cap_{s}, {v}, g_err);")
+                    if target.data in self.consumed:
+                        out.append(f"{ind2}{guard}stream_push_q({self.cname(target.data)}, n_{s}, cap_{s}, r_{s}, "
+                                   f"q_{s}, {v}, g_err);")
+                    else:
+                        out.append(f"{ind2}{guard}stream_push({self.cname(target.data)}, n_{s}, cap_{s}, {v}, g_err);")
                     continue
                 sub = m.subset if m.data == target.data or m.reindex is None else m.reindex
                 pt = [env.emit(r.begin) for r in sub]
@@ -849,6 +909,55 @@ class Lowering:
         out.append(f"      if (tot > 0) {{ {k}<<<gen_blocks(tot), 256, 0, st>>>({self.kargs()}); "
                    f"GEN_CHECK(); }} }}")
 
+    def top_consume(self, st: State, parent: dict, n, out: list) -> None:
+        """A consume scope (codegen.py:526-543: P workers popping until the
+        quiescence condition fails) as a persistent work-queue kernel.
+        Every resident thread is a worker: it takes a ticket, waits for that
+        item or for quiescence (every pushed item finished and nothing left
+        to pop), runs the scope body on the item, and counts it finished
+        after the body's pushes.  Only ``size(S) > 0`` conditions -- run
+        until the stream is drained -- are lowered."""
+        se = next((e for e in st.in_edges(n.id) if e.dst_conn == "IN_stream"), None)
+        if se is None or se.memlet.is_empty:
+            raise LoweringError("consume entry without a stream")
+        S = se.memlet.data
+        cond = X.parse_expr(n.doc["condition"])
+        ok = (isinstance(cond, X.Cmp) and isinstance(cond.left, X.Call) and cond.left.fn == "size"
+              and cond.left.args[0] == X.Sym(S) and
+              ((cond.op == ">" and cond.right == X.Num(0)) or (cond.op == ">=" and cond.right == X.Num(1))))
+        if not ok:
+            raise LoweringError(f"consume condition '{n.doc['condition']}' is not 'size({S}) > 0'")
+        s = _ident(S)
+        bt = CT[self.g.data[S].basetype]
+        denv = Env(self, {}, host=False)
+        self.pop_vars[S] = "elem"
+        body = ["    const int64_t wid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;",
+                "    for (;;) {",
+                f"        const unsigned long long h = atomicAdd(&q_{s}[0], 1ull);",
+                "        bool got = false;",
+                "        for (long long spin = 0;; ++spin) {",
+                f"            if ((int64_t)h < cap_{s} && ld_acq_u32(r_{s} + h)) {{ got = true; break; }}",
+                f"            const unsigned long long F = ld_acq_u64(&q_{s}[1]);",
+                f"            const unsigned long long T = ld_acq_u64(n_{s});",
+                "            if (F == T && h >= T) break;",
+                "            if (*(volatile int*)g_err) return;",
+                "            if (spin > (1LL << 26)) { gen_fail(g_err, 5); return; }  // watchdog (~seconds)",
+                "            __nanosleep(64);",
+                "        }",
+                "        if (!got) return;",
+                f"        const {bt} elem = {self.cname(S)}[h];"]
+        penv = denv.child({n.doc["param"]: f"(wid % g_imax(1LL, {denv.emit(X.parse_expr(n.doc['num_pes']))}))"})
+        inner: list = []
+        self.emit_scope(st, parent, n.id, penv, "        ", inner, True)
+        body += inner
+        body += ["        __threadfence();", f"        atomicAdd(&q_{s}[1], 1ull);", "    }"]
+        del self.pop_vars[S]
+        k = self.new_kernel(body, f"{st.name}_consume{n.id}")
+        out.append(f"    {k}<<<148 * 4, 128, 0, st>>>({self.kargs()}); GEN_CHECK();")
+        out.append(f"    gen_queue_reset<<<gen_blocks(cap_{s}), 256, 0, st>>>(r_{s}, n_{s}, q_{s}, cap_{s}); "
+                   f"GEN_CHECK();")
+        out.append(f"    cudaMemsetAsync(n_{s}, 0, 8, st); cudaMemsetAsync(q_{s}, 0, 16, st); ub_{s} = 0;")
+
     def _owned_by(self, name: str, st: State, parent: dict, entry: int) -> bool:
         for n in st.nodes:
             if n.kind == "access" and n.data == name:
@@ -874,7 +983,7 @@ class Lowering:
         d = self.g.data[n.data]
         for e in sorted(st.in_edges(n.id), key=lambda e: e.id):
             src = st.nodes[e.src]
-            if e.memlet.is_empty or src.kind in ("tasklet", "map_exit", "nested", "reduce"):
+            if e.memlet.is_empty or src.kind in ("tasklet", "map_exit", "consume_exit", "nested", "reduce"):
                 continue
             m = e.memlet
             sdata = src.data if src.kind == "access" else m.data
@@ -990,10 +1099,6 @@ class Lowering:
 
     def program(self) -> Lowered:
         g = self.g
-        for st in g.states:
-            for n in st.nodes:
-                if n.kind in ("consume_entry", "consume_exit"):
-                    raise LoweringError("consume scopes are not lowered")
         henv = Env(self, {}, host=True)
         ptr_args = g.pointer_args()
         lines = ["extern \"C\" int " + self.prefix + "_run(void** ptrs, const int64_t* syms, void* stream_, "
@@ -1019,6 +1124,8 @@ class Lowering:
             lines += [f"    {CT[d.basetype]}* {self.cname(name)} = nullptr;",
                       f"    unsigned long long* n_{s} = nullptr;",
                       f"    int64_t cap_{s} = 0, ub_{s} = 0;"]
+            if name in self.consumed:
+                lines += [f"    unsigned* r_{s} = nullptr;", f"    unsigned long long* q_{s} = nullptr;"]
         lines.append("    if (cudaMallocAsync((void**)&g_err, 16, st) != cudaSuccess) return 2;")
         lines.append("    cudaMemsetAsync(g_err, 0, 16, st);")
         for name, d in trans:
@@ -1026,14 +1133,24 @@ class Lowering:
             lines.append(f"      if (cudaMallocAsync((void**)&{self.cname(name)}, nb ? nb : 8, st) != cudaSuccess) "
                          f"goto gen_fail; cudaMemsetAsync({self.cname(name)}, 0, nb, st); }}")
         for name, d in streams:
-            lines.append(f"    if (cudaMallocAsync((void**)&n_{_ident(name)}, 8, st) != cudaSuccess) goto gen_fail;")
-            lines.append(f"    cudaMemsetAsync(n_{_ident(name)}, 0, 8, st);")
+            s = _ident(name)
+            lines.append(f"    if (cudaMallocAsync((void**)&n_{s}, 8, st) != cudaSuccess) goto gen_fail;")
+            lines.append(f"    cudaMemsetAsync(n_{s}, 0, 8, st);")
+            if name in self.consumed:
+                bt = CT[d.basetype]
+                lines.append(f"    cap_{s} = {QUEUE_ITEMS}LL;")
+                lines.append(f"    if (cudaMallocAsync((void**)&{self.cname(name)}, (size_t)cap_{s} * sizeof({bt}), st) "
+                             f"!= cudaSuccess || cudaMallocAsync((void**)&r_{s}, (size_t)cap_{s} * 4, st) != cudaSuccess "
+                             f"|| cudaMallocAsync((void**)&q_{s}, 16, st) != cudaSuccess) goto gen_fail;")
+                lines.append(f"    cudaMemsetAsync(r_{s}, 0, (size_t)cap_{s} * 4, st); cudaMemsetAsync(q_{s}, 0, 16, st);")
         lines.append(f"    goto st_{_ident(g.start_state)};")
         for st in g.states:
             parent = st.scope_parent()
             lines.append(f"st_{_ident(st.name)}:;")
             lines.append("    {")
             for sname, trips in self.stream_pushes(st, parent, henv).items():
+                if sname in self.consumed:
+                    continue  # fixed-capacity work queue
                 s = _ident(sname)
                 bt = CT[g.data[sname].basetype]
                 lines.append(f"    {{ const int64_t need = ub_{s} + {' + '.join(f'({t})' for t in trips)};")
@@ -1058,7 +1175,9 @@ class Lowering:
                     self.top_access(st, n, henv, lines)
                 elif n.kind == "reduce":
                     self.top_reduce(st, n, henv, lines)
-                elif n.kind == "map_exit":
+                elif n.kind == "consume_entry":
+                    self.top_consume(st, parent, n, lines)
+                elif n.kind in ("map_exit", "consume_exit"):
                     continue
                 else:
                     raise LoweringError(f"'{n.kind}' nodes are not lowered")
@@ -1075,6 +1194,9 @@ class Lowering:
         for name, _ in streams:
             free += [f"    if ({self.cname(name)}) cudaFreeAsync({self.cname(name)}, st);",
                      f"    if (n_{_ident(name)}) cudaFreeAsync(n_{_ident(name)}, st);"]
+            if name in self.consumed:
+                free += [f"    if (r_{_ident(name)}) cudaFreeAsync(r_{_ident(name)}, st);",
+                         f"    if (q_{_ident(name)}) cudaFreeAsync(q_{_ident(name)}, st);"]
         lines += free
         lines.append("    cudaFreeAsync(g_err, st);")
         lines.append("    return cudaStreamSynchronize(st) == cudaSuccess ? 0 : 2;")

@@ -257,6 +257,8 @@ def gallery_cases():
     fx = gallery.fixture("histogram")
     arrays, symbols = fx.make_inputs(np.random.default_rng(11))
     save_case("gal_histogram", "again", g, arrays, symbols)
+    save_case("gal_fibonacci", "n20_p4", gallery.fixture("fibonacci").sdfg,
+              {"n_in": np.array([20], dtype=np.int64), "out": np.zeros(1, dtype=np.int64)}, {"P": 4})
     for a in (0, 3, -1):
         save_case("gal_branching", f"a{a}".replace("-", "m"), gallery.fixture("branching").sdfg,
                   {"a": np.array([a], dtype=np.int64), "out": np.zeros(1, dtype=np.int64)}, {})

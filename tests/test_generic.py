@@ -20,7 +20,8 @@ from paper_1902_10345_b200 import CodegenError, ExecutionError
 from paper_1902_10345_b200.graph import load
 from paper_1902_10345_b200.lower import LoweringError, lower
 
-GALLERY = ["branching", "histogram", "indirection", "laplace", "mandelbrot", "matmul", "query", "spmv"]
+GALLERY = ["branching", "fibonacci", "histogram", "indirection", "laplace", "mandelbrot", "matmul", "query",
+           "spmv"]
 MOTIF_GRAPHS = ["histogram", "histogram_int", "query", "query_gallery", "spmv", "jacobi2d", "laplace1d",
                 "matmul", "matmul_raw", "matmul_tiled", "matmul_chain"]
 # outputs assembled by atomics from several threads: order-free comparison
@@ -42,9 +43,19 @@ def test_lowers(name):
     assert "__global__" in lw.source or "__device__" in lw.source
 
 
-def test_consume_scopes_are_refused():
+def test_consume_scope_is_a_work_queue_kernel():
+    src = lower(load(_doc("gal_fibonacci"))).source
+    assert "stream_push_q" in src and "gen_queue_reset" in src
+
+
+def test_other_consume_conditions_are_refused():
+    doc = _doc("gal_fibonacci")
+    for st in doc["states"]:
+        for n in st["nodes"]:
+            if n["kind"] == "consume_entry":
+                n["condition"] = "size(S) > 3"
     with pytest.raises(LoweringError):
-        lower(load(_doc("gal_fibonacci")))
+        lower(load(doc))
 
 
 def test_generate_routes_non_motifs_to_the_lowering():
@@ -54,8 +65,7 @@ def test_generate_routes_non_motifs_to_the_lowering():
     assert "__device__ __noinline__ void" in code.source  # the nested pixel loop
     with pytest.raises(CodegenError):
         generate(_doc("gal_mandelbrot"))  # unmarked
-    with pytest.raises(CodegenError):
-        generate(_doc("gal_fibonacci"), require_marked=False)
+    assert generate(_doc("gal_fibonacci"), require_marked=False).lowered is not None
 
 
 def test_nvcc_builds_a_nested_program():

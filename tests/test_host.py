@@ -120,8 +120,13 @@ def test_non_motif_programs_take_the_generic_lowering():
         classify(load(graph_path("laplace1d")))  # 1-D 'l - 2*c + r' stencil: no motif kernel
     code = b200.generate(graph_path("laplace1d"), require_marked=False)
     assert code.plan is None and code.lowered is not None
-    with pytest.raises(b200.CodegenError):  # consume scopes: neither motif nor lowerable
-        b200.generate(graph_path("gal_fibonacci"), require_marked=False)
+    doc = json.load(open(graph_path("gal_fibonacci")))
+    for st in doc["states"]:
+        for n in st["nodes"]:
+            if n["kind"] == "consume_entry":
+                n["condition"] = "size(S) > 3"  # not a drain-until-empty consume: not lowerable
+    with pytest.raises(b200.CodegenError):
+        b200.generate(doc, require_marked=False)
 
 
 def test_mutated_programs_are_rejected():
