@@ -30,6 +30,7 @@ class Case:
         self.outputs = {k[5:]: z[k] for k in z.files if k.startswith("out__")}
         self.symbols = json.loads(str(z["symbols"]))
         self.error = str(z["error"])
+        self.states = json.loads(str(z["states"])) if "states" in z.files else None
 
     def __repr__(self):
         return f"{self.motif}__{self.case}"

@@ -53,6 +53,7 @@ def save_case(motif, case, g, arrays, symbols):
         rep = run(g, arrays, symbols)
         for k, v in rep.outputs.items():
             payload[f"out__{k}"] = v
+        payload["states"] = np.array(json.dumps(rep.states_visited))
         payload["error"] = np.array("")
     except Exception as exc:  # the reference's error class is part of the contract
         payload["error"] = np.array(type(exc).__name__)

@@ -1,0 +1,71 @@
+"""CLI (paper_1902_10345_b200/cli.py): the reference CLI's run/codegen shape
+for on-disk graphs.  CPU tests cover parsing, marking, codegen and the
+interstate simulation; the GPU test runs a graph end to end."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import graph_path, load_cases
+
+from paper_1902_10345_b200 import cli
+from paper_1902_10345_b200.graph import load
+
+
+def test_states_visited_follows_the_guard_loop():
+    g = load(graph_path("jacobi2d"))
+    sv = cli.states_visited(g, {"N": 6, "T": 3})
+    assert sv[0] == g.start_state and len(sv) >= 2 + 2 * 3
+
+
+def test_states_visited_is_none_for_data_dependent_control_flow():
+    assert cli.states_visited(load(graph_path("gal_branching")), {}) is None
+
+
+def test_codegen_writes_cuda_for_generic_graphs(tmp_path):
+    rc = cli.main(["--format", "json", "codegen", graph_path("gal_mandelbrot"), "--out", str(tmp_path)])
+    assert rc == 0
+    cu = [f for f in os.listdir(tmp_path) if f.endswith(".cu")]
+    assert cu and "__global__" in open(tmp_path / cu[0]).read()
+    assert os.access(tmp_path / "build.sh", os.X_OK)
+
+
+def test_codegen_describes_motif_bindings(tmp_path):
+    assert cli.main(["codegen", graph_path("histogram"), "--out", str(tmp_path)]) == 0
+    txt = [f for f in os.listdir(tmp_path) if f.endswith(".b200.txt")]
+    assert txt and "sdfgb_host_histogram" in open(tmp_path / txt[0]).read()
+
+
+def test_usage_errors_exit_2(tmp_path, capsys):
+    assert cli.main(["run", str(tmp_path / "missing.sdfg.json")]) == 2
+
+
+@pytest.mark.gpu
+def test_run_end_to_end(tmp_path, capsys, cuda_ok):
+    case = [c for c in load_cases("gal_laplace") if c.case == "seed0"][0]
+    inp = tmp_path / "in.json"
+    inp.write_text(json.dumps({"arrays": {k: v.tolist() for k, v in case.inputs.items()},
+                               "symbols": case.symbols}))
+    assert cli.main(["--format", "json", "run", graph_path("gal_laplace"), "--input", str(inp)]) == 0
+    rep = json.loads(capsys.readouterr().out)
+    assert rep["path"] == "generic"
+    np.testing.assert_array_equal(np.array(rep["outputs"]["A"]), case.outputs["A"].reshape(2, -1))
+    assert rep["states_visited"][0] == "init"
+
+
+def test_states_visited_matches_the_reference_interpreter():
+    """interstate simulation == interpreter's states_visited on every golden
+    case whose control flow reads symbols only"""
+    n = 0
+    for c in load_cases():
+        if c.states is None or c.error:
+            continue
+        name = c.motif
+        sv = cli.states_visited(load(graph_path(name)), c.symbols)
+        if sv is None:
+            continue
+        assert sv == c.states, repr(c)
+        n += 1
+    assert n > 20
