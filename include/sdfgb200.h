@@ -124,6 +124,18 @@ int sdfgb_jacobi2d_step_f32(const float* src, float* dst, int64_t N, int64_t row
                             int64_t g0, int64_t r0, int64_t r1, double coef,
                             const int32_t* di, const int32_t* dj, int nterms, void* stream);
 
+/* The same time loop on rectangular planes A[2, M, N] (fp32): the border is
+ * the plane's edge.  The multi-GPU slab decomposition puts ghost rows at the
+ * slab edges and global rows 0 / Ng-1 at the first / last rank's edge. */
+int sdfgb_jacobi2d_rect_f32(float* A, int64_t M, int64_t N, int64_t T, double coef,
+                            const int32_t* di, const int32_t* dj, int nterms, void* stream);
+/* One temporal-blocking launch (canonical 5-point order): k in {1, 3, 5, 7}
+ * steps from plane src (state t) to plane dst (state t+k), both [M, N],
+ * N % 4 == 0, 16 B aligned.  Rows/columns within k of the plane edge are
+ * halo: exact only where the edge is the true border. */
+int sdfgb_jacobi2d_block_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k,
+                             double coef, void* stream);
+
 /* GEMM after MapReduceFusion (library.py:461-554): C = A(MxK) * B(KxN),
  * row-major fp32, fp32-accurate through 3xTF32 on tcgen05 tensor cores.
  * ws must hold sdfgb_gemm_workspace_bytes(M, N, K) bytes. */

@@ -253,7 +253,10 @@ __host__ __device__ constexpr size_t tb_smem(int k) {
 template <int KT>
 __global__ void __launch_bounds__(kTbThreads, 2)
 jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restrict__ dst_in,
-                 float* __restrict__ dst, int N, float coef, int steps) {
+                 float* __restrict__ dst, int M, int N, float coef, int steps) {
+    // planes are M rows x N columns; the border is the plane's edge (rows 0
+    // and M-1, columns 0 and N-1) -- the reference's square case is M == N,
+    // a multi-GPU slab puts ghost rows there (multigpu.jacobi)
     constexpr int RY = tb_rows(KT);
     // dynamic smem starts at the CTA window base (no static smem here), so it
     // is 1 KB-aligned for TMA; indexing the extern array directly keeps the
@@ -274,12 +277,12 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
         tma_load_2d(buf0, &src, bar, gx0, gy0);
     }
     // does the region touch the global border (or beyond)?  CTA-uniform
-    const bool edge = gx0 <= 0 || gy0 <= 0 || gx0 + kTbRX - 1 >= N - 1 || gy0 + RY - 1 >= N - 1;
+    const bool edge = gx0 <= 0 || gy0 <= 0 || gx0 + kTbRX - 1 >= N - 1 || gy0 + RY - 1 >= M - 1;
     if (edge) {  // buffer 1 carries plane p^1's border: copy just the border lines in the region
         for (int q = threadIdx.x; q < 2 * kTbRX + 2 * RY; q += kTbThreads) {
             int ry, rx;  // region coordinates of candidate q
             if (q < 2 * kTbRX) {  // border rows 0 and N-1
-                ry = (q < kTbRX ? 0 : N - 1) - gy0;
+                ry = (q < kTbRX ? 0 : M - 1) - gy0;
                 rx = q % kTbRX;
             } else {  // border columns 0 and N-1
                 const int k = q - 2 * kTbRX;
@@ -287,7 +290,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
                 rx = (k < RY ? 0 : N - 1) - gx0;
             }
             const int gy = gy0 + ry, gx = gx0 + rx;
-            if (ry >= 0 && ry < RY && rx >= 0 && rx < kTbRX && gy >= 0 && gy < N && gx >= 0 && gx < N)
+            if (ry >= 0 && ry < RY && rx >= 0 && rx < kTbRX && gy >= 0 && gy < M && gx >= 0 && gx < N)
                 buf1[ry * kTbRX + rx] = dst_in[(int64_t)gy * N + gx];
         }
     }
@@ -347,7 +350,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
             } else {
                 const float o[4] = {o4.x, o4.y, o4.z, o4.w};
                 const int gy = gy0 + r;
-                const bool rowb = gy <= 0 || gy >= N - 1;
+                const bool rowb = gy <= 0 || gy >= M - 1;
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                     if (!rowb && !colb[j]) op[j] = o[j];
@@ -470,7 +473,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
     for (int it = threadIdx.x; it < kTbY * CG; it += kTbThreads) {
         const int r = it / CG, g = it % CG;
         const int gy = y0 + r, gxx = x0 + 4 * g;
-        if (gy < 1 || gy > N - 2) continue;
+        if (gy < 1 || gy > M - 2) continue;
         const float4 v = *reinterpret_cast<const float4*>(fin + (KT + r) * kTbRX + kTbPad + 4 * g);
         float* d = dst + (int64_t)gy * N + gxx;
         if (gxx >= 1 && gxx + 3 <= N - 2) {
@@ -485,7 +488,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
 }
 
 template <int KT>
-int launch_tb(const float* src_plane, float* dst, int64_t N, float coef, cudaStream_t s) {
+int launch_tb(const float* src_plane, float* dst, int64_t M, int64_t N, float coef, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         SDFGB_CUDA(cudaFuncSetAttribute(jacobi_tb_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -493,38 +496,40 @@ int launch_tb(const float* src_plane, float* dst, int64_t N, float coef, cudaStr
         attr = true;
     }
     CUtensorMap map;
-    SDFGB_TRY(encode_tiled_2d(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, src_plane, N, N, kTbRX, tb_rows(KT),
+    SDFGB_TRY(encode_tiled_2d(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, src_plane, M, N, kTbRX, tb_rows(KT),
                               CU_TENSOR_MAP_SWIZZLE_NONE));
-    dim3 grid((unsigned)((N + kTbX - 1) / kTbX), (unsigned)((N + kTbY - 1) / kTbY));
-    jacobi_tb_kernel<KT><<<grid, kTbThreads, tb_smem(KT), s>>>(map, dst, dst, (int)N, coef, KT);
+    dim3 grid((unsigned)((N + kTbX - 1) / kTbX), (unsigned)((M + kTbY - 1) / kTbY));
+    jacobi_tb_kernel<KT><<<grid, kTbThreads, tb_smem(KT), s>>>(map, dst, dst, (int)M, (int)N, coef, KT);
     SDFGB_LAUNCHED("jacobi_tb_kernel");
     return SDFGB_OK;
 }
 
-// T steps on A[2, N, N] in fp32 with temporal blocking.  Launches advance an
+int launch_block(const float* src, float* dst, int64_t M, int64_t N, int64_t k, float coef, const Terms& terms,
+                 cudaStream_t s) {
+    if (k == 7) return launch_tb<7>(src, dst, M, N, coef, s);
+    if (k == 5) return launch_tb<5>(src, dst, M, N, coef, s);
+    if (k == 3) return launch_tb<3>(src, dst, M, N, coef, s);
+    if (k == 1) return launch_step<float>(src, dst, N, M, 0, 1, M - 1, coef, terms, true, s);
+    return set_error(SDFGB_ERR_INVALID, "jacobi2d block: k must be 1, 3, 5 or 7 (got %lld)", (long long)k);
+}
+
+// T steps on A[2, M, N] in fp32 with temporal blocking.  Launches advance an
 // odd number of steps each (so state s stays in plane s % 2, as in the
 // reference), and the last step is a one-step launch so the other plane ends
 // holding state T-1 exactly like A[(T+1) % 2] of the reference.
-int jacobi_f32_blocked(float* A, int64_t N, int64_t T_, float coef, const Terms& terms, cudaStream_t s) {
-    float* P[2] = {A, A + N * N};
+int jacobi_f32_blocked(float* A, int64_t M, int64_t N, int64_t T_, float coef, const Terms& terms,
+                       cudaStream_t s) {
+    float* P[2] = {A, A + M * N};
     int64_t t = 0;
     while (T_ - t > 1) {
         int64_t k = std::min<int64_t>(7, T_ - 1 - t);
         if ((k & 1) == 0) k -= 1;
         const int p = (int)(t & 1);
-        if (k == 7)
-            SDFGB_TRY(launch_tb<7>(P[p], P[p ^ 1], N, coef, s));
-        else if (k == 5)
-            SDFGB_TRY(launch_tb<5>(P[p], P[p ^ 1], N, coef, s));
-        else if (k == 3)
-            SDFGB_TRY(launch_tb<3>(P[p], P[p ^ 1], N, coef, s));
-        else
-            SDFGB_TRY(launch_step<float>(P[p], P[p ^ 1], N, N, 0, 1, N - 1, coef, terms, true, s));
+        SDFGB_TRY(launch_block(P[p], P[p ^ 1], M, N, k, coef, terms, s));
         t += k;
     }
     const int p = (int)(t & 1);
-    SDFGB_TRY(launch_step<float>(P[p], P[p ^ 1], N, N, 0, 1, N - 1, coef, terms, true, s));
-    return SDFGB_OK;
+    return launch_block(P[p], P[p ^ 1], M, N, 1, coef, terms, s);
 }
 
 template <typename T>
@@ -540,7 +545,7 @@ int launch_jacobi(T* A, int64_t N, int64_t T_, double coef, const int32_t* di, c
     if constexpr (sizeof(T) == 4) {
         // temporal blocking needs 16 B rows (TMA) and enough steps to pay off
         if (canon && (N % 4) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && T_ >= 4 && N >= 16)
-            return jacobi_f32_blocked(reinterpret_cast<float*>(A), N, T_, (float)coef, terms, s);
+            return jacobi_f32_blocked(reinterpret_cast<float*>(A), N, N, T_, (float)coef, terms, s);
     }
     T* P[2] = {A, A + N * N};
     for (int64_t t = 0; t < T_; ++t)
@@ -570,4 +575,33 @@ extern "C" int sdfgb_jacobi2d_step_f32(const float* src, float* dst, int64_t N, 
     (void)g0;
     return sdfgb::launch_step<float>(src, dst, N, rows, g0, r0, r1, (float)coef, terms, canon,
                                      sdfgb::as_stream(stream));
+}
+
+extern "C" int sdfgb_jacobi2d_rect_f32(float* A, int64_t M, int64_t N, int64_t T, double coef, const int32_t* di,
+                                       const int32_t* dj, int nterms, void* stream) {
+    sdfgb::Terms terms;
+    bool canon;
+    if (M < 0 || N < 0 || T < 0 || ((M > 0 && N > 0) && !A) || !sdfgb::parse_terms(di, dj, nterms, terms, canon))
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_rect: bad arguments");
+    if (M < 3 || N < 3 || T == 0) return SDFGB_OK;
+    cudaStream_t s = sdfgb::as_stream(stream);
+    if (canon && (N % 4) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && T >= 4 && N >= 16 && M >= 16)
+        return sdfgb::jacobi_f32_blocked(A, M, N, T, (float)coef, terms, s);
+    float* P[2] = {A, A + M * N};
+    for (int64_t t = 0; t < T; ++t)
+        SDFGB_TRY(sdfgb::launch_step<float>(P[t & 1], P[(t + 1) & 1], N, M, 0, 1, M - 1, (float)coef, terms, canon,
+                                            s));
+    return SDFGB_OK;
+}
+extern "C" int sdfgb_jacobi2d_block_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k, double coef,
+                                        void* stream) {
+    if (M < 3 || N < 16 || (N % 4) != 0 || !src || !dst || (reinterpret_cast<uintptr_t>(src) & 15) != 0 ||
+        (reinterpret_cast<uintptr_t>(dst) & 15) != 0 || (k > 1 && M < 16))
+        return sdfgb::set_error(SDFGB_ERR_INVALID,
+                                "jacobi2d_block: needs M >= 16, N >= 16, N %% 4 == 0 and 16 B aligned planes");
+    sdfgb::Terms terms;
+    bool canon;
+    const int32_t di[5] = {0, -1, 1, 0, 0}, dj[5] = {0, 0, 0, -1, 1};
+    sdfgb::parse_terms(di, dj, 5, terms, canon);
+    return sdfgb::launch_block(src, dst, M, N, k, (float)coef, terms, sdfgb::as_stream(stream));
 }

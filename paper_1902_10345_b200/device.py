@@ -104,6 +104,22 @@ def jacobi2d(A, T, coef=0.2, terms=JACOBI5, stream=None):
     _lib.check(fn(_p(A), N, int(T), float(coef), di, dj, len(terms), _stream(stream)))
 
 
+def jacobi2d_rect(A, T, coef=0.2, terms=JACOBI5, stream=None):
+    """T steps on fp32 A[2, M, N] whose border is the plane edge."""
+    L = _lib.load()
+    M, N = A.shape[-2], A.shape[-1]
+    di, dj = _terms(terms)
+    _lib.check(L.sdfgb_jacobi2d_rect_f32(_p(A), M, N, int(T), float(coef), di, dj, len(terms), _stream(stream)))
+
+
+def jacobi2d_block(src, dst, k, coef=0.2, stream=None):
+    """One temporal-blocking launch: k in {1,3,5,7} steps, plane src (state
+    t) -> plane dst (state t+k), canonical 5-point order."""
+    L = _lib.load()
+    M, N = src.shape[-2], src.shape[-1]
+    _lib.check(L.sdfgb_jacobi2d_block_f32(_p(src), _p(dst), M, N, int(k), float(coef), _stream(stream)))
+
+
 def jacobi2d_step(src, dst, N, rows, g0, r0, r1, coef=0.2, terms=JACOBI5, stream=None):
     L = _lib.load()
     di, dj = _terms(terms)

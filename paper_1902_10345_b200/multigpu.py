@@ -14,7 +14,8 @@ The exchange steps are the ones the north star names:
   query      per-shard compaction -> all_gather of counts -> global offsets
              (output stays sharded at its global offset; gather is optional)
   spmv       row blocks, x sharded -> all_gather(x) -> row kernel
-  jacobi     row blocks with 1-row halos -> per-step send/recv of halo rows
+  jacobi     row blocks with 7-row ghost zones -> one send/recv of ghost
+             rows per temporal block (up to 7 steps)
   gemm       2-D process grid -> all_gather of A row panels / B column panels
 """
 
@@ -47,6 +48,9 @@ class DeviceBackend:
 
     def jacobi_step(self, src, dst, N, rows, r0, r1, coef, terms):
         self.d.jacobi2d_step(src, dst, N, rows, 0, r0, r1, coef, terms)
+
+    def jacobi_block(self, src, dst, k, coef):
+        self.d.jacobi2d_block(src, dst, k, coef)
 
     def gemm(self, A, B, C):
         M, K = A.shape
@@ -119,52 +123,84 @@ def spmv(pg, rowptr_local, col, val, x_shard, b_local, backend):
 
 # -------------------------------------------------------------------- jacobi
 
+GHOST = 7  # ghost rows per neighbour = the deepest temporal block
+
+
 @dataclass
 class JacobiSlab:
-    """This rank's rows of the global [2, Ng, N] array plus one halo row on
-    each side: planes [2, rows + 2, N]; local row l <-> global row g0 + l - 1."""
+    """This rank's rows of the global [2, Ng, N] array plus ``top``/``bot``
+    ghost rows towards its neighbours: planes [2, top + rows + bot, N].
+    Local row l <-> global row g0 + l - top.  The first rank has no rows
+    above it, so its plane's top edge IS the global border row 0 (and the
+    last rank's bottom edge is row Ng-1): the kernels' plane-edge border
+    is the reference's border exactly there."""
     A: object
     g0: int
     rows: int
     Ng: int
+    top: int = 1
+    bot: int = 1
 
 
-def jacobi_slab(A_global_rows, g0, Ng):
-    """Build a slab from this rank's interior rows [2, rows, N] (a copy)."""
+def jacobi_slab(A_global_rows, g0, Ng, ghost=GHOST):
+    """Build a slab from this rank's rows [2, rows, N] (a copy)."""
     import torch
     two, rows, N = A_global_rows.shape
-    A = torch.zeros((2, rows + 2, N), dtype=A_global_rows.dtype, device=A_global_rows.device)
-    A[:, 1:rows + 1] = A_global_rows
-    return JacobiSlab(A, g0, rows, Ng)
+    top = ghost if g0 > 0 else 0
+    bot = ghost if g0 + rows < Ng else 0
+    if (top or bot) and rows < ghost:
+        raise ValueError(f"slab of {rows} rows is thinner than the {ghost} ghost rows")
+    A = torch.zeros((2, top + rows + bot, N), dtype=A_global_rows.dtype, device=A_global_rows.device)
+    A[:, top:top + rows] = A_global_rows
+    return JacobiSlab(A, g0, rows, Ng, top, bot)
 
 
 def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1))):
-    """T steps of the guard loop (loops.py:31-61) over row blocks.  Before each
-    step the source plane's boundary rows are exchanged with the neighbours
-    (send/recv, the 'row-block halo exchange'); global rows 0 and Ng-1 are
-    the border and never written, exactly like the reference."""
+    """T steps of the guard loop (loops.py:31-61) over row blocks with
+    ghost zones: the single-GPU temporal-blocking schedule (odd blocks of
+    7/5/3 steps, then one final step so the other plane ends at state T-1)
+    with, before every launch, one exchange of the source plane's ghost
+    rows with each neighbour (GHOST rows of 2 x N fp32 per block of up to
+    GHOST steps, instead of a halo per step).  Every owned row sits at least
+    GHOST rows from a ghost edge, so after k <= GHOST steps it is exact;
+    the ghost rows themselves are refreshed before they are read again.
+    Non-canonical stencil orders take one step per exchange."""
     rank, world = _rank_world(pg)
-    A, rows, N = slab.A, slab.rows, slab.A.shape[-1]
-    first_global = slab.g0
-    last_global = slab.g0 + rows - 1
-    # local interior rows to compute: skip the global border rows
-    r0 = 1 + (1 if first_global == 0 else 0)
-    r1 = rows + 1 - (1 if last_global == slab.Ng - 1 else 0)
-    for t in range(T):
+    A = slab.A
+    canon = tuple(map(tuple, terms)) == ((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1))
+    # both planes' ghost rows once: the border columns of the ghost rows are
+    # border values of their own plane, read by intermediate states of the
+    # other parity and never exchanged again
+    _ghost_exchange(pg, A[1], slab, rank, world)
+    t = 0
+    while t < T:
+        if not canon:
+            k = 1
+        elif T - t > 1:
+            k = min(GHOST, T - 1 - t)
+            k -= (k % 2 == 0)
+        else:
+            k = 1
         src, dst = A[t % 2], A[(t + 1) % 2]
-        _halo_exchange(pg, src, rows, rank, world)
-        if r1 > r0:
-            backend.jacobi_step(src, dst, N, rows + 2, r0, r1, coef, terms)
+        _ghost_exchange(pg, src, slab, rank, world)
+        if canon:
+            backend.jacobi_block(src, dst, k, coef)
+        else:
+            M = A.shape[1]
+            backend.jacobi_step(src, dst, A.shape[-1], M, 1, M - 1, coef, terms)
+        t += k
 
 
-def _halo_exchange(pg, plane, rows, rank, world):
+def _ghost_exchange(pg, plane, slab: JacobiSlab, rank, world):
+    """Owned edge rows -> the neighbours' ghost rows (batched send/recv)."""
     ops = []
-    if rank > 0:
-        ops.append(pg.P2POp(pg.isend, plane[1].contiguous(), rank - 1))
-        ops.append(pg.P2POp(pg.irecv, plane[0], rank - 1))
-    if rank < world - 1:
-        ops.append(pg.P2POp(pg.isend, plane[rows].contiguous(), rank + 1))
-        ops.append(pg.P2POp(pg.irecv, plane[rows + 1], rank + 1))
+    top, rows, bot = slab.top, slab.rows, slab.bot
+    if rank > 0 and top:
+        ops.append(pg.P2POp(pg.isend, plane[top:2 * top].contiguous(), rank - 1))
+        ops.append(pg.P2POp(pg.irecv, plane[0:top], rank - 1))
+    if rank < world - 1 and bot:
+        ops.append(pg.P2POp(pg.isend, plane[top + rows - bot:top + rows].contiguous(), rank + 1))
+        ops.append(pg.P2POp(pg.irecv, plane[top + rows:top + rows + bot], rank + 1))
     if ops:
         for r in pg.batch_isend_irecv(ops):
             r.wait()

@@ -384,6 +384,62 @@ def test_full_jacobi_8192_nine_steps_temporal_blocking():
     np.testing.assert_array_equal(At.cpu().numpy(), ref)
 
 
+def _jacobi_rect_ref(A, T):
+    ref = A.copy()
+    for t in range(T):
+        s, d = ref[t % 2], ref[(t + 1) % 2]
+        acc = s[1:-1, 1:-1] + s[0:-2, 1:-1]
+        acc = acc + s[2:, 1:-1]
+        acc = acc + s[1:-1, 0:-2]
+        acc = acc + s[1:-1, 2:]
+        d[1:-1, 1:-1] = np.float32(0.2) * acc
+    return ref
+
+
+@pytest.mark.parametrize("M,N,T", [(16, 132, 9), (300, 144, 15), (1000, 256, 11), (129, 512, 8)])
+def test_jacobi_rect_temporal_blocking_bit_exact(M, N, T):
+    from paper_1902_10345_b200 import device
+    A = np.random.default_rng(M + N).random((2, M, N), dtype=np.float32)
+    At = t(A)
+    device.jacobi2d_rect(At, T)
+    np.testing.assert_array_equal(At.cpu().numpy(), _jacobi_rect_ref(A, T))
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_jacobi_ghost_zone_slabs_on_one_device(ranks):
+    """The multi-GPU decomposition (multigpu.jacobi: 7-row ghost zones, one
+    exchange per temporal block) with its device kernels, ranks run one after
+    another on this GPU with the exchanges done by copies: equals the
+    single-domain restatement bit for bit."""
+    from paper_1902_10345_b200 import multigpu as MG
+    from paper_1902_10345_b200 import device
+    rows, N, T = 300, 256, 23
+    Ng = rows * ranks
+    A = np.random.default_rng(ranks).random((2, Ng, N), dtype=np.float32)
+    ref = _jacobi_rect_ref(A, T)
+    slabs = [MG.jacobi_slab(t(A[:, r * rows:(r + 1) * rows].copy()), r * rows, Ng) for r in range(ranks)]
+
+    def exchange(p):
+        for r in range(ranks - 1):
+            lo, hi = slabs[r], slabs[r + 1]
+            hi.A[p, 0:hi.top] = lo.A[p, lo.top + rows - lo.bot:lo.top + rows]
+            lo.A[p, lo.top + rows:lo.top + rows + lo.bot] = hi.A[p, hi.top:2 * hi.top]
+    exchange(1)
+    step = 0
+    while step < T:
+        k = 1 if T - step <= 1 else min(MG.GHOST, T - 1 - step)
+        if T - step > 1 and k % 2 == 0:
+            k -= 1
+        p = step % 2
+        exchange(p)
+        for sl in slabs:
+            device.jacobi2d_block(sl.A[p], sl.A[1 - p], k)
+        step += k
+    for r, sl in enumerate(slabs):
+        np.testing.assert_array_equal(sl.A[:, sl.top:sl.top + rows].cpu().numpy(),
+                                      ref[:, r * rows:(r + 1) * rows])
+
+
 def test_full_spmv_2pow22_rows_sampled():
     from paper_1902_10345_b200 import device
     H = W = 1 << 22

@@ -44,6 +44,21 @@ class OracleBackend:
                 acc = acc + s[i + di, 1 + dj:N - 1 + dj]
             d[i, 1:N - 1] = c32 * acc
 
+    def jacobi_block(self, src, dst, k, coef):
+        """k steps from plane src to plane dst with the kernels' semantics:
+        intermediate states alternate between the two planes' borders
+        (plane edges), only dst is written (state t+k)."""
+        P = [src.numpy().copy(), dst.numpy().copy()]
+        c32 = np.float32(coef)
+        for i in range(k):
+            s_, d_ = P[i % 2], P[(i + 1) % 2]
+            acc = s_[1:-1, 1:-1] + s_[0:-2, 1:-1]
+            acc = acc + s_[2:, 1:-1]
+            acc = acc + s_[1:-1, 0:-2]
+            acc = acc + s_[1:-1, 2:]
+            d_[1:-1, 1:-1] = c32 * acc
+        dst.copy_(torch.from_numpy(P[k % 2]))
+
     def gemm(self, A, B, C):
         C.copy_(torch.from_numpy(oracle.matmul(A.numpy(), B.numpy()).astype(np.float32)))
 
@@ -144,23 +159,29 @@ def _case_spmv(rank, world):
 
 def _case_jacobi(rank, world):
     rng = np.random.default_rng(3)
-    rows, N, T = 9, 12, 5
+    rows, N, T = 9, 12, 17  # two 7-step blocks, a 1-step block, the final step
     Ng = rows * world
     A = rng.random((2, Ng, N), dtype=np.float32)  # distinct planes, non-zero borders
-    # reference: the whole domain is square in the oracle, so embed it: run a
-    # non-square restatement with the same op order instead
-    ref = A.copy()
-    for t in range(T):
-        s, d = ref[t % 2], ref[(t + 1) % 2]
-        acc = s[1:-1, 1:-1] + s[0:-2, 1:-1]
-        acc = acc + s[2:, 1:-1]
-        acc = acc + s[1:-1, 0:-2]
-        acc = acc + s[1:-1, 2:]
-        d[1:-1, 1:-1] = np.float32(0.2) * acc
-    slab = MG.jacobi_slab(torch.from_numpy(A[:, rank * rows:(rank + 1) * rows].copy()), rank * rows, Ng)
-    MG.jacobi(dist, slab, T, OracleBackend())
-    got = slab.A[:, 1:rows + 1].numpy()
-    return bool(np.array_equal(got, ref[:, rank * rows:(rank + 1) * rows]))
+
+    def restated(terms):
+        # the whole domain is not square, so a non-square restatement with
+        # the kernels' op order is the reference here
+        ref = A.copy()
+        for t in range(T):
+            s, d = ref[t % 2], ref[(t + 1) % 2]
+            acc = s[1 + terms[0][0]:Ng - 1 + terms[0][0], 1 + terms[0][1]:N - 1 + terms[0][1]].copy()
+            for di, dj in terms[1:]:
+                acc = acc + s[1 + di:Ng - 1 + di, 1 + dj:N - 1 + dj]
+            d[1:-1, 1:-1] = np.float32(0.2) * acc
+        return ref
+    ok = True
+    for terms in (((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1)), ((0, 1), (0, 0), (1, 0), (-1, 0), (0, -1))):
+        ref = restated(terms)
+        slab = MG.jacobi_slab(torch.from_numpy(A[:, rank * rows:(rank + 1) * rows].copy()), rank * rows, Ng)
+        MG.jacobi(dist, slab, T, OracleBackend(), terms=terms)
+        got = slab.A[:, slab.top:slab.top + rows].numpy()
+        ok = ok and bool(np.array_equal(got, ref[:, rank * rows:(rank + 1) * rows]))
+    return ok
 
 
 def _case_gemm(rank, world):
