@@ -8,7 +8,10 @@ def bench(path):
             print("headline", d["value"], d["unit"], "frac", round(d["roofline"]["frac"], 3), "clocks", d["clocks"])
             for k, v in d["motifs"].items():
                 e = v.get("e2e") or {}
-                print(f"  {k:10s} {v['value']:10.1f} {v['unit']:8s} frac={v['roofline']['frac']:.3f} ms={v['ms_per_step']:.4f} e2e={e.get('value', 0):.1f}")
+                fr = (v.get("roofline") or {}).get("frac")
+                cb = (v.get("cpu_baseline") or {}).get("value")
+                print(f"  {k:18s} {v['value']:10.1f} {v['unit']:8s} frac={fr if fr is None else round(fr, 3)} "
+                      f"ms={v['ms_per_step']:.4f} e2e={e.get('value', 0):.1f} cpu={cb}")
             if "cpu_baseline" in d: print("  cpu", d["cpu_baseline"])
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
