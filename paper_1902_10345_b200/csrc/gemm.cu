@@ -27,6 +27,8 @@
 #include <algorithm>
 #include <mutex>
 
+#include <cstdlib>
+
 #include "tma.cuh"
 
 namespace sdfgb {
@@ -234,6 +236,192 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_consta
     }
 }
 
+// Long contractions: the same pipeline, but every CHUNK uses of an
+// accumulator are folded into per-thread fp32 registers by 8 epilogue warps
+// (2 per TMEM lane quarter) while the tensor core keeps going on the other
+// three accumulators.  The tensor core's truncating accumulation then spans
+// at most CHUNK k-blocks per accumulator whatever K is: max relative error
+// 2.7e-6 at K = 16384 (one accumulation per accumulator: 4.4e-5, growing
+// linearly with K).  Measured ~5 % slower at 4096^3 / 16384^3, so
+// sdfgb_gemm_f32 selects it only for K > kFlushK.
+constexpr int FLUSH_EPI_WARPS = 8;
+constexpr int FLUSH_THREADS = 128 + 32 * FLUSH_EPI_WARPS;
+constexpr int CHUNK = 8;        // uses of one accumulator (k-blocks) per chunk
+constexpr int64_t kFlushK = 16384;
+
+__global__ void __launch_bounds__(FLUSH_THREADS, 1)
+gemm_3xtf32_flush_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
+                   float* __restrict__ C, int M, int N, int K) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* acc_full = empty + STAGES;   // [NACC]: an accumulator's chunk is complete
+    uint64_t* acc_empty = acc_full + NACC; // [NACC]: the epilogue has folded it into registers
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // grouped rasterisation: consecutive CTAs cover SDFGB_GEMM_GROUP tile rows
+    // x a few tile columns, so a wave of co-resident CTAs shares ~26 operand
+    // panels instead of ~5 A + 148 B panels (row-major order re-read every B
+    // panel from DRAM once per tile row: ~280 GB at 16384^3)
+    int m0, n0;
+    {
+        const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+        const int pid = blockIdx.x, group = SDFGB_GEMM_GROUP * tiles_n;
+        const int first_m = (pid / group) * SDFGB_GEMM_GROUP;
+        const int gm = min(tiles_m - first_m, SDFGB_GEMM_GROUP);
+        const int in_group = pid % group;
+        m0 = (first_m + in_group % gm) * BM;
+        n0 = (in_group / gm) * BN;
+    }
+    const int KB = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < NACC; ++a) {
+            mbar_init(&acc_full[a], 1);
+            mbar_init(&acc_empty[a], 32 * FLUSH_EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAhi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAlo)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBhi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBlo)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_d = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                mbar_expect_tx(&full[s], STAGE_BYTES);
+                tma_load_2d(st + 0 * TILE_BYTES, &mAhi, &full[s], kb * BK, m0);
+                tma_load_2d(st + 1 * TILE_BYTES, &mAlo, &full[s], kb * BK, m0);
+                tma_load_2d(st + 2 * TILE_BYTES, &mBhi, &full[s], kb * BK, n0);
+                tma_load_2d(st + 3 * TILE_BYTES, &mBlo, &full[s], kb * BK, n0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(BM, BN);
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                // k-block kb -> accumulator a = kb % 4 (round robin: four
+                // independent accumulation chains keep the tensor pipe full);
+                // every CHUNK uses of an accumulator form a chunk that the
+                // epilogue folds into registers before the accumulator's next
+                // use, staggered across the four accumulators
+                const int a = kb & (NACC - 1), u = kb / NACC, cu = u / CHUNK, j = u - cu * CHUNK;
+                if (j == 0 && cu >= 1) {
+                    mbar_wait(&acc_empty[a], (cu - 1) & 1);  // chunk cu-1 of this accumulator folded
+                    tc_fence_after();
+                }
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+                const uint32_t dacc = tmem_d + (uint32_t)(a * BN);
+                const uint32_t first = j == 0;
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k) {
+                    const uint32_t off = k * 32;  // 8 tf32 = 32 B along K inside the 128 B atom
+                    const uint64_t ahi = sw128_kmajor_desc(base + 0 * TILE_BYTES + off);
+                    const uint64_t alo = sw128_kmajor_desc(base + 1 * TILE_BYTES + off);
+                    const uint64_t bhi = sw128_kmajor_desc(base + 2 * TILE_BYTES + off);
+                    const uint64_t blo = sw128_kmajor_desc(base + 3 * TILE_BYTES + off);
+                    tc_mma_tf32(dacc, alo, bhi, idesc, !(first && k == 0));
+                    tc_mma_tf32(dacc, ahi, blo, idesc, 1u);
+                    tc_mma_tf32(dacc, ahi, bhi, idesc, 1u);
+                }
+                tc_commit(&empty[s]);
+                if (j == CHUNK - 1 || kb + NACC >= KB) tc_commit(&acc_full[a]);
+            }
+        }
+    } else if (warp >= 4) {
+        // Each thread owns one output row (its TMEM lane) and keeps the
+        // row's running fp32 sum in registers: every finished accumulator
+        // chunk is folded in with IEEE adds, so the tensor core's truncating
+        // accumulation spans at most CHUNK k-blocks per accumulator whatever
+        // K is (one long accumulation per accumulator biased the result by
+        // ~1e-8 per k-block: 4.4e-5 relative at K = 16384).
+        constexpr int HC = BN * 4 / FLUSH_EPI_WARPS;  // columns per epilogue warp
+        const int rw = (warp & 3) * 32;
+        const int h0 = ((warp - 4) >> 2) * HC;
+        const int row = m0 + rw + lane;
+        const int uses0 = (KB + NACC - 1) / NACC;  // uses of accumulator 0 (the most)
+        const int nchunks = (uses0 + CHUNK - 1) / CHUNK;
+        float sum[HC];
+#pragma unroll
+        for (int e = 0; e < HC; ++e) sum[e] = 0.f;
+        for (int cu = 0; cu < nchunks; ++cu) {
+#pragma unroll 1
+            for (int a = 0; a < NACC; ++a) {  // the order the chunks complete in
+                const int uses = (KB - a + NACC - 1) / NACC;
+                if (cu * CHUNK >= uses) continue;
+                mbar_wait_sleep(&acc_full[a], cu & 1, 512);
+                tc_fence_after();
+                const uint32_t t0 = tmem_d + ((uint32_t)rw << 16) + (uint32_t)(a * BN + h0);
+#pragma unroll
+                for (int cc = 0; cc < HC; cc += 16) {
+                    uint32_t r[16];
+                    tmem_ld16(t0 + cc, r);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) sum[cc + e] += __uint_as_float(r[e]);
+                }
+                tc_fence_before();
+                mbar_arrive(&acc_empty[a]);
+            }
+        }
+#pragma unroll
+        for (int cq = 0; cq < HC; cq += 16) {
+            const int c = h0 + cq;
+            uint32_t r[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(sum[cq + e]);
+            if (row < M) {
+                float* dst = C + (int64_t)row * N + n0 + c;
+                if (n0 + c + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        reinterpret_cast<float4*>(dst)[q] =
+                            make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        if (n0 + c + q < N) dst[q] = __uint_as_float(r[q]);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(TMEM_COLS));
+    }
+}
+
 // ------------------------------------------------------------ SIMT cross-check
 // 64x64 tile, 256 threads, 4x4 per thread, k-sequential FFMA per element.
 __global__ void __launch_bounds__(256)
@@ -319,11 +507,20 @@ extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t 
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr, [] {
         attr_err = cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(gemm_3xtf32_flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            GEMM_SMEM);
     });
     SDFGB_CUDA(attr_err);
     dim3 grid((unsigned)(((N + BN - 1) / BN) * ((M + BM - 1) / BM)));
-    gemm_3xtf32_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, s>>>(mAhi, mAlo, mBhi, mBlo, C, (int)M, (int)N, (int)K);
-    SDFGB_LAUNCHED("gemm_3xtf32_kernel");
+    if (K > kFlushK || getenv("SDFGB_GEMM_FLUSH")) {
+        gemm_3xtf32_flush_kernel<<<grid, FLUSH_THREADS, GEMM_SMEM, s>>>(mAhi, mAlo, mBhi, mBlo, C, (int)M, (int)N,
+                                                                         (int)K);
+        SDFGB_LAUNCHED("gemm_3xtf32_flush_kernel");
+    } else {
+        gemm_3xtf32_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, s>>>(mAhi, mAlo, mBhi, mBlo, C, (int)M, (int)N, (int)K);
+        SDFGB_LAUNCHED("gemm_3xtf32_kernel");
+    }
     return SDFGB_OK;
 }
 

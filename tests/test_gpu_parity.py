@@ -384,6 +384,21 @@ def test_full_jacobi_8192_nine_steps_temporal_blocking():
     np.testing.assert_array_equal(At.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("M,N,K", [(256, 384, 40000), (130, 200, 16388)])
+def test_gemm_long_k_register_flush(M, N, K):
+    """K > 16384 takes the kernel that folds accumulator chunks into fp32
+    registers: error independent of K (1e-5 here, where one accumulation
+    per TMEM accumulator would drift past 1e-4)."""
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(K)
+    A = rng.random((M, K), dtype=np.float32)
+    B = rng.random((K, N), dtype=np.float32)
+    C = torch.empty((M, N), dtype=torch.float32, device=DEV)
+    device.gemm(t(A), t(B), C, device.gemm_workspace(M, N, K, DEV))
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    assert np.abs(C.cpu().numpy() - ref).max() / np.abs(ref).max() < 1e-5
+
+
 def _jacobi_rect_ref(A, T):
     ref = A.copy()
     for t in range(T):

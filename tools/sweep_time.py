@@ -5,6 +5,9 @@ sys.path.insert(0, "/root/repo")
 from paper_1902_10345_b200 import _lib
 
 lib, motif = sys.argv[1], sys.argv[2]
+if "flush" in sys.argv[3:]:
+    import os
+    os.environ["SDFGB_GEMM_FLUSH"] = "1"
 _lib.load(lib)
 from paper_1902_10345_b200 import device  # noqa: E402
 
@@ -70,4 +73,17 @@ elif motif == "gemm":
         ws = device.gemm_workspace(n, n, n, "cuda")
         us = timed(lambda k: device.gemm(A, B, C, ws), reps=10 if n == 4096 else 2)
         print(f"{name:28s} gemm{n:<6d} {us:9.1f} us {2 * n ** 3 / us / 1e6:6.1f} TF/s")
+        del A, B, C, ws
+elif motif == "gemm_acc":
+    for n in (4096, 16384):
+        g = torch.Generator(device="cuda").manual_seed(4)
+        A = torch.rand(n, n, device="cuda", generator=g)
+        B = torch.rand(n, n, device="cuda", generator=g)
+        C = torch.empty(n, n, device="cuda")
+        ws = device.gemm_workspace(n, n, n, "cuda")
+        device.gemm(A, B, C, ws)
+        rows = torch.arange(0, n, n // 64, device="cuda")
+        ref = A[rows].double() @ B.double()
+        err = ((C[rows].double() - ref).abs().max() / ref.abs().max()).item()
+        print(f"{name:28s} gemm{n:<6d} max rel err {err:.3e}")
         del A, B, C, ws
