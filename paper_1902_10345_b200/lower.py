@@ -589,6 +589,18 @@ class Lowering:
         the committed memlet is the tasklet-side one (codegen.py:286-302)."""
         dst = st.nodes[e.dst]
         if dst.kind == "access":
+            d = self.g.data.get(dst.data)
+            if d is not None and d.kind == "stream" and d.transient:
+                # a scope-local stream drained through the scope exit into an
+                # outer stream (LocalStream, library.py): its pushes are the
+                # outer stream's pushes -- the order is unspecified either way
+                fwd = [o for o in st.out_edges(dst.id)
+                       if st.nodes[o.dst].kind in ("map_exit", "consume_exit") and o.dst_conn]
+                if fwd:
+                    out = []
+                    for o in fwd:
+                        out += self.targets(st, type(e)(o.id, e.src, e.src_conn, o.dst, o.dst_conn, e.memlet))
+                    return out
             return [dst]
         if dst.kind in ("map_exit", "consume_exit"):
             conn = "OUT_" + e.dst_conn[3:]
@@ -870,11 +882,14 @@ class Lowering:
         return name
 
     def top_map(self, st: State, parent: dict, n, host_env: Env, out: list) -> None:
-        for e in st.in_edges(n.id):
-            if e.dst_conn and not e.dst_conn.startswith("IN_") and not e.memlet.is_empty:
-                raise LoweringError("data-dependent ranges on a top-level map are not lowered")
+        dynamic = any(e.dst_conn and not e.dst_conn.startswith("IN_") and not e.memlet.is_empty
+                      for e in st.in_edges(n.id))
         denv = Env(self, {}, host=False)
         body = []
+        if dynamic:
+            # data-dependent range (e.g. the SpMV row map after MapToForLoop):
+            # every thread reads the bounds from HBM, the grid is fixed
+            denv = self.dyn_range_locals(st, n, denv, "    ", body)
         lens, begins, strides = [], [], []
         for k, r in enumerate(n.ranges):
             body.append(f"    const int64_t b{k} = {denv.emit(r.begin)}, s{k} = {denv.emit(r.stride)}, "
@@ -902,6 +917,9 @@ class Lowering:
         body += inner
         body.append("    }")
         k = self.new_kernel(body, f"{st.name}_map{n.id}")
+        if dynamic:
+            out.append(f"    {k}<<<148, 256, 0, st>>>({self.kargs()}); GEN_CHECK();")
+            return
         # host: launch over the same flattened range
         tot = " * ".join(f"g_rlen({host_env.emit(r.begin)}, {host_env.emit(r.end)}, {host_env.emit(r.stride)})"
                          for r in n.ranges)

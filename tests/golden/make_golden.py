@@ -265,7 +265,46 @@ def gallery_cases():
                   {"a": np.array([a], dtype=np.int64), "out": np.zeros(1, dtype=np.int64)}, {})
 
 
+def transformed_cases():
+    """Each motif graph after each reference transformation that matches it
+    (the dispatcher must accept these unchanged in result):
+    graphs x_<motif>_<transformation>, interpreter outputs on small inputs."""
+    from sdfg.rewriting import apply_transformation, find_matches, registry
+    rng = np.random.default_rng(21)
+    col = f32(rng.random(300, dtype=F32))
+    inputs = {
+        "histogram": ({"img": f32(rng.random((12, 17), dtype=F32)), "hist": np.zeros(256, np.int64)},
+                      {"H": 12, "W": 17}),
+        "query": ({"col": col, "thr": np.array([0.5]), "out_vals": np.zeros(300),
+                   "count": np.array([4], np.int64)}, {"N": 300}),
+        "spmv": spmv_inputs(rng, 40, 60, 9),
+        "jacobi2d": ({"A": jacobi_inputs(rng, 19, border=True, distinct=True)}, {"N": 19, "T": 5}),
+        "matmul": ({"A": f32(rng.random((7, 11), dtype=F32)), "B": f32(rng.random((11, 6), dtype=F32)),
+                    "C": np.zeros((7, 6))}, {"M": 7, "N": 6, "K": 11}),
+    }
+    builders = {"histogram": M.histogram, "query": lambda: M.query("<"), "spmv": M.spmv,
+                "jacobi2d": M.jacobi2d, "matmul": M.matmul}
+    for motif, build in builders.items():
+        g = build()
+        for tname in sorted(registry):
+            try:
+                ms = find_matches(g, tname)
+            except Exception:
+                continue
+            if not ms:
+                continue
+            try:
+                g2, _ = apply_transformation(g, ms[0], {})
+            except Exception:
+                continue
+            name = f"x_{motif}_{tname}"
+            save_graph(name, g2)
+            arrays, symbols = inputs[motif]
+            save_case(name, "small", g2, {k: np.array(v, copy=True) for k, v in arrays.items()}, symbols)
+
+
 if __name__ == "__main__":
+    transformed_cases()
     gallery_cases()
     histogram_cases()
     query_cases()

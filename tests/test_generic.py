@@ -9,7 +9,9 @@ threads (atomics, unordered) within 1e-12 relative; stream outputs as a
 sorted set (a Stream is a concurrent queue).
 """
 
+import glob
 import json
+import os
 
 import numpy as np
 import pytest
@@ -24,10 +26,15 @@ GALLERY = ["branching", "fibonacci", "histogram", "indirection", "laplace", "man
            "spmv"]
 MOTIF_GRAPHS = ["histogram", "histogram_int", "query", "query_gallery", "spmv", "jacobi2d", "laplace1d",
                 "matmul", "matmul_raw", "matmul_tiled", "matmul_chain"]
+# every motif graph after every reference transformation that matches it
+TRANSFORMED = sorted(os.path.basename(p)[:-len(".sdfg.json")]
+                     for p in glob.glob(os.path.join(os.path.dirname(graph_path("x")), "x_*.sdfg.json")))
 # outputs assembled by atomics from several threads: order-free comparison
-UNORDERED_SUMS = {"matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "gal_matmul"}
+UNORDERED_SUMS = {"matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "gal_matmul", "x_matmul_MapExpansion",
+                  "x_matmul_MapTiling"}
 STREAM_OUT = {"gal_query": ("out_vals", "count"), "query": ("out_vals", "count"),
-              "query_gallery": ("out_vals", "count")}
+              "query_gallery": ("out_vals", "count"), "x_query_LocalStream": ("out_vals", "count"),
+              "x_query_MapTiling": ("out_vals", "count"), "x_query_RedundantArray": ("out_vals", "count")}
 
 
 def _doc(name):
@@ -107,6 +114,52 @@ def test_generic_matches_reference_interpreter(graph, case, cuda_ok):
             prog.run(case.inputs, case.symbols)
         return
     _compare(graph, case, prog.run(case.inputs, case.symbols))
+
+
+@pytest.mark.parametrize("name", TRANSFORMED)
+def test_transformed_motifs_dispatch(name):
+    """every transformed motif graph binds to a motif kernel or lowers"""
+    from paper_1902_10345_b200 import generate
+    code = generate(_doc(name), require_marked=False)
+    assert code.plan is not None or code.lowered is not None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", TRANSFORMED)
+def test_transformed_motifs_match_the_interpreter(name, cuda_ok):
+    """drop-in (native precision) on each transformed graph == the reference
+    interpreter on the same graph"""
+    import paper_1902_10345_b200 as b200
+    doc = _doc(name)
+    for d in doc["data"]:
+        if not d["transient"]:
+            d["storage"] = "GPU_Global:native"
+    case = load_cases(name)[0]
+    got = b200.invoke_toolchain(b200.generate(doc)).run(case.inputs, case.symbols)
+    if name == "x_query_RedundantArray":
+        # RedundantArray folds the stream away: every survivor writes
+        # out_vals[0] with no WCR.  The interpreter keeps the last one in
+        # iteration order; concurrent map iterations keep one of them (the
+        # same race the reference's cpu_parallel schedule has).
+        col, thr = case.inputs["col"], case.inputs["thr"][0]
+        assert got["count"][0] == case.outputs["count"][0]
+        assert got["out_vals"][0] in set(col[col < thr].tolist())
+        np.testing.assert_array_equal(got["out_vals"][1:], case.outputs["out_vals"][1:])
+        return
+    motif_tol = name.startswith("x_spmv")
+    gemm_tol = name.startswith("x_matmul")  # the motif kernel is 3xTF32 at any precision
+    for k, exp in case.outputs.items():
+        g = np.asarray(got[k]).reshape(exp.shape)
+        if name in STREAM_OUT and k == "out_vals":
+            kk = int(case.outputs["count"][0] - case.inputs["count"][0])
+            g, exp = g.copy(), exp.copy()
+            g[:kk], exp[:kk] = np.sort(g[:kk]), np.sort(exp[:kk])
+        if gemm_tol:
+            assert np.abs(g - exp).max() / (np.abs(exp).max() + 1e-300) < 1e-4, k
+        elif motif_tol and exp.dtype.kind == "f":
+            np.testing.assert_allclose(g, exp, rtol=1e-12, atol=1e-12 * (np.abs(exp).max() + 1e-300))
+        else:
+            np.testing.assert_array_equal(g, exp, err_msg=f"{name}: {k}")
 
 
 @pytest.mark.gpu
