@@ -71,33 +71,36 @@ def histogram(pg, img_shard, hist, oob, backend, scale=256.0, div=1.0):
     """hist += counts of the union of all ranks' shards (every rank ends with
     the same hist); oob likewise."""
     import torch
-    part = torch.zeros_like(hist)
-    pbad = torch.zeros_like(oob)
-    backend.hist(img_shard, part, pbad, scale, div)
-    pg.all_reduce(part)
-    pg.all_reduce(pbad)
-    hist += part
-    oob += pbad
+    nb = hist.numel()
+    part = torch.zeros(nb + 1, dtype=hist.dtype, device=hist.device)  # bins, then the out-of-range count
+    backend.hist(img_shard, part[:nb], part[nb:], scale, div)
+    pg.all_reduce(part)  # one collective for bins + oob
+    hist += part[:nb]
+    oob += part[nb:].to(oob.dtype)
 
 
 # --------------------------------------------------------------------- query
 
 def query(pg, col_shard, thr, out_shard, count, backend, op="<", gather=False):
-    """Per-shard compaction.  Returns (k_local, offset): this rank's survivors
-    are out_shard[0:k_local] and belong at global out_vals[offset:offset+k].
-    ``count`` (replicated) is advanced by the global survivor count.  With
-    ``gather`` rank 0 also returns the concatenated survivors."""
+    """Per-shard compaction.  Returns (k_local, offset, full): this rank's
+    survivors are out_shard[0:k_local] and belong at global
+    out_vals[offset:offset+k].  ``count`` (replicated) is advanced by the
+    global survivor count.  Without ``gather`` k_local and offset are device
+    tensors (nothing waits for the host); with it they are ints and rank 0
+    also receives the concatenated survivors."""
     import torch
     rank, world = _rank_world(pg)
     local = torch.zeros(1, dtype=torch.int64, device=col_shard.device)
     backend.query(col_shard, thr, out_shard, local, op)
     counts = torch.empty(world, dtype=torch.int64, device=col_shard.device)
     pg.all_gather_into_tensor(counts, local)
+    if not gather:
+        # device-side bookkeeping: no host round trip per call
+        count += counts.sum()
+        return counts[rank:rank + 1], counts[:rank].sum(), None
     cl = counts.tolist()
     offset = sum(cl[:rank])
     count += int(sum(cl))
-    if not gather:
-        return cl[rank], offset, None
     kmax = max(cl) if cl else 0
     pad = torch.zeros(max(kmax, 1), dtype=out_shard.dtype, device=out_shard.device)
     pad[:cl[rank]] = out_shard[:cl[rank]]

@@ -137,6 +137,10 @@ def _case_query(rank, world):
     ok = count.item() == 5 + ref.size and np.array_equal(out[:k].numpy(), ref[off:off + k])
     if rank == 0:
         ok = ok and np.array_equal(full.numpy(), ref)
+    # device-tensor bookkeeping without the gather
+    count2 = torch.full((1,), 5, dtype=torch.int64)
+    k2, off2, none = MG.query(dist, shard, 0.5, out, count2, OracleBackend(), "<")
+    ok = ok and none is None and int(k2) == k and int(off2) == off and count2.item() == count.item()
     return bool(ok)
 
 
