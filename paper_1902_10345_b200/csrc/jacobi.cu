@@ -236,7 +236,17 @@ int launch_step(const T* src, T* dst, int64_t N, int64_t rows, int64_t g0, int64
 // Work mapping: warp w owns a band of rows, lane l owns columns 4l..4l+3
 // (one float4); a north/centre register window slides down the band so each
 // step costs one LDS.128 + two shuffles per 4 points.
-constexpr int kTbRX = 128, kTbPad = 8, kTbX = kTbRX - 2 * kTbPad, kTbY = 96, kTbThreads = 256;
+#ifndef SDFGB_J_TY
+#define SDFGB_J_TY 96
+#endif
+#ifndef SDFGB_J_THREADS
+#define SDFGB_J_THREADS 256
+#endif
+#ifndef SDFGB_J_MINB
+#define SDFGB_J_MINB 2
+#endif
+constexpr int kTbRX = 128, kTbPad = 8, kTbX = kTbRX - 2 * kTbPad, kTbY = SDFGB_J_TY, kTbThreads = SDFGB_J_THREADS;
+constexpr int kTbWarps = kTbThreads / 32;
 
 __host__ __device__ constexpr int tb_rows(int k) { return kTbY + 2 * k; }
 // two region buffers + kTbPadRows pad rows (a fused sweep of F steps may
@@ -251,7 +261,7 @@ __host__ __device__ constexpr size_t tb_smem(int k) {
 }
 
 template <int KT>
-__global__ void __launch_bounds__(kTbThreads, 2)
+__global__ void __launch_bounds__(kTbThreads, SDFGB_J_MINB)
 jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restrict__ dst_in,
                  float* __restrict__ dst, int M, int N, float coef, int steps) {
     // planes are M rows x N columns; the border is the plane's edge (rows 0
@@ -298,7 +308,7 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
     mbar_wait(bar, 0);
 
     // this warp's row band inside [1, RY-2]
-    const int rb = 1 + (warp * (RY - 2)) / 8, re = 1 + ((warp + 1) * (RY - 2)) / 8;
+    const int rb = 1 + (warp * (RY - 2)) / kTbWarps, re = 1 + ((warp + 1) * (RY - 2)) / kTbWarps;
     const int gx = gx0 + 4 * lane;
     bool colb[4];
 #pragma unroll
