@@ -9,8 +9,9 @@ with the same exit codes (0 ok, 1 validation, 2 usage, 3 runtime) and
               [--stream-order any|fifo]
         marks the program for the GPU (GPUTransformMap's marker), dispatches it
         to a motif kernel or the generic lowering, runs it, and prints an
-        ExecutionReport-shaped document: outputs (value_cap 4096 like
-        interpreter.py:117-132), states_visited, the kernel path.
+        ExecutionReport-shaped document (interpreter.py:107-132): outputs
+        (value_cap 4096), states_visited, elements_moved of every statically
+        countable edge, tasklet_invocations, and the kernel path.
     codegen GRAPH --out DIR [--compile]
         writes the B200 program (the motif binding, or the generated CUDA
         translation unit) plus a build script; --compile builds it.
@@ -106,6 +107,145 @@ def states_visited(g: Graph, symbols: dict, cap: int = 1_000_000) -> Optional[li
     return seq
 
 
+def _visits(g: Graph, symbols: dict, cap: int = 100_000):
+    """(state, symbol env) per visit of the interstate machine, or None when
+    control flow reads data (then decided on the device)."""
+    env = {k: int(v) for k, v in symbols.items()}
+    out, cur = [], g.start_state
+    data = set(g.data)
+    while cur is not None and len(out) < cap:
+        out.append((cur, dict(env)))
+        nxt = None
+        for t in g.out_transitions(cur):
+            names = X.free_symbols(t.condition)
+            for _, v in t.assignments:
+                names |= X.free_symbols(v)
+            if names & data:
+                return None
+            try:
+                ok = X.evaluate(t.condition, env)
+            except X.ExprError:
+                return None
+            if ok:
+                for k, v in t.assignments:
+                    env[k] = X.evaluate(v, env)
+                nxt = t.dst
+                break
+        cur = nxt
+    return out
+
+
+def _instances(st, parent: dict, scope, env: dict, limit: int = 200_000, per_point=None):
+    """Points of the map nest ending at ``scope`` (inclusive ranges,
+    symbolic.py:579-618) -- or the sum of ``per_point(env)`` over them;
+    None when a range is data-dependent or the nest is too large to
+    enumerate."""
+    chain = []
+    p = scope
+    while p is not None:
+        chain.append(st.nodes[p])
+        p = parent[p]
+    chain.reverse()
+    for n in chain:
+        if n.kind != "map_entry" or any(e.dst_conn and not e.dst_conn.startswith("IN_") and not e.memlet.is_empty
+                                        for e in st.in_edges(n.id)):
+            return None
+    count = 0
+    total = 0
+
+    def rec(k, e):
+        nonlocal count, total
+        if count > limit:
+            return
+        if k == len(chain):
+            count += 1
+            total += 1 if per_point is None else per_point(e)
+            return
+        n = chain[k]
+
+        def dims(d, e2):
+            if d == len(n.params):
+                rec(k + 1, e2)
+                return
+            r = n.ranges[d]
+            b, en, sd = (int(X.evaluate(x, e2)) for x in (r.begin, r.end, r.stride))
+            for v in (range(b, en + 1, sd) if sd > 0 else range(b, en - 1, sd)):
+                if count > limit:
+                    return
+                e3 = dict(e2)
+                e3[n.params[d]] = v
+                dims(d + 1, e3)
+        dims(0, e)
+    try:
+        rec(0, dict(env))
+    except X.ExprError:
+        return None
+    return None if count > limit else total
+
+
+def execution_report(g: Graph, symbols: dict) -> dict:
+    """The static part of the interpreter's ExecutionReport
+    (interpreter.py:107-132): states_visited, elements_moved for every
+    memlet edge whose volume is static (accesses x points of its scope x
+    visits), and tasklet_invocations when every tasklet's scope can be
+    counted.  Dynamic memlets (stream pushes, data-dependent ranges) are
+    listed under ``dynamic_edges``: their volumes are data-dependent."""
+    visits = _visits(g, symbols)
+    if visits is None:
+        return {"states_visited": None}
+    moved, dynamic = {}, set()
+    tasklets = 0
+    for name, env in visits:
+        st = g.state(name)
+        parent = st.scope_parent()
+        for e in st.edges:
+            key = f"{name}:e{e.id}"
+            m = e.memlet
+            src = st.nodes[e.src]
+            if m.is_empty:
+                moved[key] = moved.get(key, 0)
+                continue
+            if g.data[m.data].kind == "stream" and src.kind == "map_entry":
+                moved[key] = moved.get(key, 0)  # stream handles move nothing (interpreter.py:527-530)
+                continue
+            if m.accesses is None or src.kind in ("consume_entry", "consume_exit"):
+                dynamic.add(key)
+                continue
+            scope = src.id if src.kind == "map_entry" else (
+                parent[src.doc["entry"]] if src.kind == "map_exit" else parent[src.id])
+            if src.kind == "map_entry":
+                # a scope instance reads the memlet's whole block (interpreter.py:531-533)
+                def vol(pe, sub=m.subset):
+                    v = 1
+                    for r in sub:
+                        v *= max(0, int(X.evaluate(r.end, pe)) - int(X.evaluate(r.begin, pe)) + 1)
+                    return v
+                cnt = _instances(st, parent, scope, env, per_point=vol)
+            else:
+                cnt = _instances(st, parent, scope, env, per_point=lambda pe, a=m.accesses: int(X.evaluate(a, pe)))
+            if cnt is None:
+                dynamic.add(key)
+                continue
+            moved[key] = moved.get(key, 0) + cnt
+        for n in st.nodes:
+            if n.kind == "nested":  # its own edges count under the nested graph's prefix
+                dynamic.add(f"{name}:nested{n.id}")
+            if tasklets is None:
+                continue
+            if n.kind in ("nested", "consume_entry"):
+                tasklets = None
+            elif n.kind == "tasklet":
+                pts = _instances(st, parent, parent[n.id], env)
+                tasklets = None if pts is None else tasklets + pts
+    for k in dynamic:
+        moved.pop(k, None)
+    rep = {"states_visited": [s for s, _ in visits], "elements_moved": dict(sorted(moved.items())),
+           "dynamic_edges": sorted(dynamic), "tasklet_invocations": tasklets}
+    if not dynamic:
+        rep["total_moved"] = sum(moved.values())
+    return rep
+
+
 def cmd_run(args) -> int:
     doc = _load_doc(args.graph)
     if args.journal:
@@ -128,9 +268,7 @@ def cmd_run(args) -> int:
         shape = [int(X.evaluate(d, symbols)) for d in g.data[name].dims]
         a = np.asarray(arr).reshape(shape)
         rep["outputs"][name] = a.tolist() if a.size <= 4096 else {"truncated": True, "size": int(a.size)}
-    sv = states_visited(g, symbols)
-    if sv is not None:
-        rep["states_visited"] = sv
+    rep.update({k: v for k, v in execution_report(g, symbols).items() if v is not None})
     print(json.dumps(rep, indent=2, sort_keys=True) if args.format == "json" else json.dumps(rep, sort_keys=True))
     return EXIT_OK
 

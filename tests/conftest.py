@@ -31,6 +31,8 @@ class Case:
         self.symbols = json.loads(str(z["symbols"]))
         self.error = str(z["error"])
         self.states = json.loads(str(z["states"])) if "states" in z.files else None
+        self.moved = json.loads(str(z["moved"])) if "moved" in z.files else None
+        self.tasklets = int(z["tasklets"]) if "tasklets" in z.files else None
 
     def __repr__(self):
         return f"{self.motif}__{self.case}"

@@ -54,6 +54,8 @@ def save_case(motif, case, g, arrays, symbols):
         for k, v in rep.outputs.items():
             payload[f"out__{k}"] = v
         payload["states"] = np.array(json.dumps(rep.states_visited))
+        payload["moved"] = np.array(json.dumps(rep.elements_moved))
+        payload["tasklets"] = np.array(int(rep.tasklet_invocations))
         payload["error"] = np.array("")
     except Exception as exc:  # the reference's error class is part of the contract
         payload["error"] = np.array(type(exc).__name__)

@@ -69,3 +69,25 @@ def test_states_visited_matches_the_reference_interpreter():
         assert sv == c.states, repr(c)
         n += 1
     assert n > 20
+
+
+def test_execution_report_matches_the_interpreter_on_static_edges():
+    """elements_moved of every statically countable edge and
+    tasklet_invocations == the reference interpreter's ExecutionReport"""
+    edges = cases = tl = 0
+    for c in load_cases():
+        if c.moved is None or c.error:
+            continue
+        rep = cli.execution_report(load(graph_path(c.motif)), c.symbols)
+        if rep.get("states_visited") is None:
+            continue
+        for k, v in rep["elements_moved"].items():
+            assert c.moved.get(k, 0) == v, f"{c}: {k}"
+            edges += 1
+        if not rep["dynamic_edges"]:
+            assert rep["total_moved"] == sum(c.moved.values()), repr(c)
+        if rep["tasklet_invocations"] is not None:
+            assert rep["tasklet_invocations"] == c.tasklets, repr(c)
+            tl += 1
+        cases += 1
+    assert cases > 40 and edges > 400 and tl > 20, (cases, edges, tl)
