@@ -192,6 +192,20 @@ static int gen_blocks(int64_t total) {
     if (b > 148 * 16) b = 148 * 16;
     return (int)b;
 }
+// Keep stream-ordered allocations cached between runs: with the default
+// release threshold (0) every synchronize hands the pool back to the driver
+// and the next cudaMallocAsync pays a real allocation (ms-scale, variable).
+static void gen_pool_keep() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done = true;
+}
 template <typename T>
 static T gen_read(const T* p, cudaStream_t s) {
     T v;
@@ -1122,6 +1136,7 @@ class Lowering:
         lines = ["extern \"C\" int " + self.prefix + "_run(void** ptrs, const int64_t* syms, void* stream_, "
                  "int* status) {",
                  "    cudaStream_t st = (cudaStream_t)stream_;",
+                 "    gen_pool_keep();",
                  "    cudaError_t gen_ce = cudaSuccess;",
                  "#define GEN_CHECK() do { gen_ce = cudaGetLastError(); if (gen_ce != cudaSuccess) goto gen_fail; } while (0)"]
         for i, (name, bt) in enumerate(ptr_args):
