@@ -299,31 +299,7 @@ query_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
     if (c == 0 && tid == 0) atomicAdd(count, (unsigned long long)base_off);
 }
 
-// ---------------------------------------------------------------------------
-// TMA-pipelined variant (the common case: 16 B-aligned column).  One CTA per
-// SM; each round r gives CTA c the segment r*G + c of kTSegBytes.  A single
-// thread streams segments into a 3-deep ring of smem buffers with
-// cp.async.bulk (TMA) and mbarriers, so HBM never waits for the warps:
-//   prologue  bulk-load rounds 0, 1, 2; count(0)
-//   round r   count(r+1) (smem, warp ballots) -> publish;  gather(r);
-//             write(r) from smem: each warp compacts its contiguous slice in
-//             order with ballots, starting at the CTA offset plus the lower
-//             warps' counts -- no block barrier inside;  bulk-load round r+3
-//             into the buffer round r just released.
-// The column is read from HBM exactly once and never re-read from L2.
-constexpr int kTSegBytes = 64 * 1024;
-constexpr int kTBlock = 1024;  // 32 warps: the write pass is latency-bound, so more warps
-constexpr int kTStages = 3;
-[[maybe_unused]] constexpr int kTVec = 3;  // 16 B vectors per thread per write sub-tile (12 floats / 6 doubles)
-
-template <typename T>
-__host__ __device__ constexpr int tseg_elems() { return kTSegBytes / (int)sizeof(T); }
-template <typename T>
-__host__ __device__ constexpr int tsub_elems() { return kQBlock * kTVec * Vec16<T>::n; }
-template <typename T>
-__host__ __device__ constexpr size_t tma_query_smem() {
-    return (size_t)kTStages * kTSegBytes + 64;
-}
+constexpr int kTBlock = 1024;  // upper bound on co-resident CTAs of the piece kernel (count slots per piece)
 
 // predicated store of v to base[idx] with a single 32x32+64 address op
 __device__ __forceinline__ void st_pred(float* base, uint32_t idx, float v, uint32_t p) {
@@ -339,217 +315,6 @@ __device__ __forceinline__ void st_pred(double* base, uint32_t idx, double v, ui
         : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(dst)),
-        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
-        : "memory");
-}
-
-template <typename T, int OP>
-__global__ void __launch_bounds__(kTBlock, 1)
-query_tma_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
-                 unsigned long long* __restrict__ count, QueryWs* __restrict__ ws, int64_t rounds,
-                 uint32_t epoch) {
-    using V = typename Vec16<T>::type;
-    constexpr int VN = Vec16<T>::n;
-    constexpr int SEG = tseg_elems<T>();
-    constexpr int NW = kTBlock / 32;
-    constexpr int WSEG = SEG / NW;        // contiguous elements per warp per segment
-    constexpr int CV = WSEG / (32 * VN);  // 16 B vectors per lane per segment (one per 32*VN chunk)
-    static_assert(WSEG % (32 * VN) == 0 && CV * VN <= 32 && CV <= 4, "segment geometry");
-
-    extern __shared__ __align__(1024) uint8_t q_smem[];
-    T* segs = reinterpret_cast<T*>(q_smem);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(q_smem + kTStages * kTSegBytes);
-    __shared__ uint32_t s_red[NW + 1], s_tot[NW + 1];
-    __shared__ uint32_t s_wcnt[2][NW];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t G = gridDim.x, c = blockIdx.x;
-    const int GW = (int)((G + 31) / 32);  // warps that gather the round's counts
-
-    auto seg_len = [&](int64_t r) -> int64_t {
-        const int64_t start = (r * G + c) * (int64_t)SEG;
-        return start >= n ? 0 : (n - start < SEG ? n - start : SEG);
-    };
-    auto issue = [&](int64_t r) {  // thread 0 only
-        const int b = (int)(r % kTStages);
-        const int64_t len = seg_len(r);
-        const uint32_t bytes = (uint32_t)((len * (int64_t)sizeof(T)) & ~int64_t(15));
-        mbar_expect_tx(&bars[b], bytes);
-        if (bytes) bulk_g2s(segs + (size_t)b * SEG, col + (r * G + c) * (int64_t)SEG, bytes, &bars[b]);
-    };
-    auto wait = [&](int64_t r) {
-        const int b = (int)(r % kTStages);
-        mbar_wait(&bars[b], (uint32_t)((r / kTStages) & 1));
-        T* buf = segs + (size_t)b * SEG;
-        const int64_t len = seg_len(r);
-        const int64_t done = ((len * (int64_t)sizeof(T)) & ~int64_t(15)) / (int64_t)sizeof(T);
-        if (done < len) {  // sub-16 B tail of the very last segment
-            if (tid < len - done) buf[done + tid] = col[(r * G + c) * (int64_t)SEG + done + tid];
-            __syncthreads();
-        }
-    };
-    // Count this warp's slice and keep, per lane, the predicate bits (bit
-    // q*VN + cc) and the per-chunk counts packed in bytes: the write pass
-    // reuses both instead of re-evaluating the predicate.
-    // valid elements of this warp's slice, clamped to [0, WSEG] (32-bit)
-    auto warp_len = [&](int64_t r) -> int {
-        const int64_t wl = seg_len(r) - (int64_t)warp * WSEG;
-        return wl <= 0 ? 0 : (wl >= WSEG ? WSEG : (int)wl);
-    };
-    auto count_seg = [&](int64_t r, uint32_t& bits, uint32_t& packed) {
-        const V* wv = reinterpret_cast<const V*>(segs + (size_t)(r % kTStages) * SEG + warp * WSEG) + lane;
-        const int wl = warp_len(r);
-        bits = 0;
-        packed = 0;
-        if (wl == WSEG) {
-#pragma unroll
-            for (int q = 0; q < CV; ++q) {
-                const V x = wv[q * 32];
-                uint32_t m = 0;
-#pragma unroll
-                for (int cc = 0; cc < VN; ++cc) m |= (uint32_t)pred<OP>(vget<V, T>(x, cc), thr) << cc;
-                bits |= m << (q * VN);
-                packed |= (uint32_t)__popc(m) << (8 * q);
-            }
-        } else {
-            for (int q = 0; q < CV; ++q) {
-                const V x = wv[q * 32];
-                uint32_t m = 0;
-#pragma unroll
-                for (int cc = 0; cc < VN; ++cc) {
-                    const int e = (q * 32 + lane) * VN + cc;
-                    m |= (uint32_t)(e < wl && pred<OP>(vget<V, T>(x, cc), thr)) << cc;
-                }
-                bits |= m << (q * VN);
-                packed |= (uint32_t)__popc(m) << (8 * q);
-            }
-        }
-        uint32_t cnt = 0;
-#pragma unroll
-        for (int q = 0; q < CV; ++q) cnt += (packed >> (8 * q)) & 0xffu;
-#pragma unroll
-        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-        if (lane == 0) s_wcnt[r & 1][warp] = cnt;
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t t = 0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) t += s_wcnt[r & 1][w];
-            st_relaxed(&ws->status[r * G + c], pack_status(epoch, kFlagAgg, t));
-        }
-    };
-
-    if (tid == 0) {
-        for (int b = 0; b < kTStages; ++b) mbar_init(&bars[b], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int64_t r = 0; r < kTStages && r < rounds; ++r) issue(r);
-    }
-    __syncthreads();
-    uint32_t nbits, npacked;
-    wait(0);
-    count_seg(0, nbits, npacked);
-
-    int64_t base_off = 0;
-    for (int64_t r = 0; r < rounds; ++r) {
-        const uint32_t bits = nbits, packed = npacked;
-        if (r + 1 < rounds) {
-            wait(r + 1);
-            count_seg(r + 1, nbits, npacked);
-        }
-        // ---- all-gather of round r's counts: warps [0, GW) read one word per
-        // lane (segment counts fit 32 bits), warp 0 folds
-        if (warp < GW) {
-            uint32_t val = 0;
-            if (tid < G) {
-                uint64_t w;
-                while (true) {
-                    w = ld_relaxed(&ws->status[r * G + tid]);
-                    if ((uint32_t)(w >> 44) == epoch && ((w >> kValueBits) & 3ull)) break;
-                    __nanosleep(16);
-                }
-                val = (uint32_t)(w & kValueMask);
-            }
-            uint32_t lower = tid < c ? val : 0u;
-#pragma unroll
-            for (int d = 16; d; d >>= 1) {
-                lower += __shfl_xor_sync(0xffffffffu, lower, d);
-                val += __shfl_xor_sync(0xffffffffu, val, d);
-            }
-            if (lane == 0) {
-                s_red[warp] = lower;
-                s_tot[warp] = val;
-            }
-        }
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t lo = lane < GW ? s_red[lane] : 0u, to = lane < GW ? s_tot[lane] : 0u;
-#pragma unroll
-            for (int d = 16; d; d >>= 1) {
-                lo += __shfl_xor_sync(0xffffffffu, lo, d);
-                to += __shfl_xor_sync(0xffffffffu, to, d);
-            }
-            if (lane == 0) {
-                s_red[NW] = lo;
-                s_tot[NW] = to;
-            }
-        }
-        __syncthreads();
-        // ---- write(r): each warp compacts its slice in order.  One 32-bit
-        // shuffle scan of the byte-packed per-chunk counts ranks all CV chunks.
-        uint32_t wc = lane < warp ? s_wcnt[r & 1][lane] : 0u;
-#pragma unroll
-        for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
-        uint32_t incl = packed;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += o;
-        }
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t excl = incl - packed;
-        T* wout = out + (base_off + (int64_t)s_red[NW] + wc);
-        const V* wv = reinterpret_cast<const V*>(segs + (size_t)(r % kTStages) * SEG + warp * WSEG) + lane;
-        uint32_t run = 0;  // survivors of this warp's earlier chunks
-#pragma unroll
-        for (int q = 0; q < CV; ++q) {
-            const V x = wv[q * 32];
-            uint32_t at = run + ((excl >> (8 * q)) & 0xffu);
-#pragma unroll
-            for (int cc = 0; cc < VN; ++cc) {
-                const uint32_t p = (bits >> (q * VN + cc)) & 1u;
-                st_pred(wout, at, vget<V, T>(x, cc), p);
-                at += p;
-            }
-            run += (tot >> (8 * q)) & 0xffu;
-        }
-        base_off += s_tot[NW];
-        __syncthreads();  // segment r's buffer is free
-        if (tid == 0 && r + kTStages < rounds) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(r + kTStages);
-        }
-    }
-    if (c == 0 && tid == 0) atomicAdd(count, (unsigned long long)base_off);
-}
-
-template <typename T>
-auto query_tma_kernel_for(int op) {
-    switch (op) {
-    case 0: return query_tma_kernel<T, 0>;
-    case 1: return query_tma_kernel<T, 1>;
-    case 2: return query_tma_kernel<T, 2>;
-    case 3: return query_tma_kernel<T, 3>;
-    case 4: return query_tma_kernel<T, 4>;
-    case 5: return query_tma_kernel<T, 5>;
-    case 6: return query_tma_kernel<T, 6>;
-    default: return query_tma_kernel<T, 7>;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Piece kernel (the default for 16 B-aligned columns).  The column is cut
@@ -1070,7 +835,7 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
         SDFGB_LAUNCHED("query_push_kernel");
         return SDFGB_OK;
     }
-    if (vec && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && !getenv("SDFGB_QUERY_TMA")) {
+    if (vec && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
         // piece kernel: co-resident CTAs, one grid barrier per 64 MB piece
         auto pk = query_piece_kernel_for<T>(kop);
         static int pocc[2][8] = {};
@@ -1080,24 +845,6 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
         auto* cnts = W->status;
         void* args[] = {(void*)&col, (void*)&n, (void*)&tt, (void*)&out, (void*)&C, (void*)&cnts};
         SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)pk, dim3((unsigned)G), dim3(kQBlock), args, 0, s));
-        return SDFGB_OK;
-    }
-    if (vec) {
-        // TMA ring: one CTA per SM, segments of kTSegBytes
-        auto tk = query_tma_kernel_for<T>(kop);
-        static bool attr[2][8] = {};
-        if (!attr[sizeof(T) == 8][kop]) {
-            SDFGB_CUDA(cudaFuncSetAttribute((const void*)tk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)tma_query_smem<T>()));
-            attr[sizeof(T) == 8][kop] = true;
-        }
-        const int64_t segs = (n + tseg_elems<T>() - 1) / tseg_elems<T>();
-        const int64_t G = std::max<int64_t>(1, std::min<int64_t>({segs, (int64_t)num_sms(), (int64_t)kTBlock}));
-        const int64_t rounds = (segs + G - 1) / G;
-        void* args[] = {(void*)&col, (void*)&n, (void*)&tt, (void*)&out, (void*)&C, (void*)&W,
-                        (void*)&rounds, (void*)&epoch};
-        SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)tk, dim3((unsigned)G), dim3(kTBlock), args,
-                                               tma_query_smem<T>(), s));
         return SDFGB_OK;
     }
     auto kern = vec ? query_kernel_for<T, true>(kop) : query_kernel_for<T, false>(kop);
@@ -1117,11 +864,10 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
 }  // namespace sdfgb
 
 extern "C" size_t sdfgb_query_workspace_bytes(int64_t n, int elem_bytes) {
-    // one status word per (round, CTA) slot; rounds * G <= segments + G - 1 < 2 * segments + kQBlock
-    // (both kernels: the TMA segments are larger than the register-path ones)
-    const int64_t seg = std::min<int64_t>(
-        elem_bytes == 8 ? sdfgb::seg_elems<double>() : sdfgb::seg_elems<float>(),
-        elem_bytes == 8 ? sdfgb::tseg_elems<double>() : sdfgb::tseg_elems<float>());
+    // one status word per (round, CTA) slot of the register-path kernel:
+    // rounds * G <= segments + G - 1; the piece kernel needs pieces * G
+    // count slots, fewer than that
+    const int64_t seg = elem_bytes == 8 ? sdfgb::seg_elems<double>() : sdfgb::seg_elems<float>();
     const int64_t segs = (n + seg - 1) / seg;
     return offsetof(sdfgb::QueryWs, status) + (size_t)(segs + sdfgb::kTBlock) * 8;
 }

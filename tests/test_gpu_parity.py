@@ -211,6 +211,28 @@ def test_query(n, offset, op, ordered):
 
 
 @pytest.mark.parametrize("ordered", [False, True])
+@pytest.mark.parametrize("n", [100003, 3 * 4096 * 16])
+def test_query_misaligned_output(n, ordered):
+    """an output view that is not 16 B aligned (the register-path kernel
+    for FIFO order; scalar stores for the push kernel)"""
+    from paper_1902_10345_b200 import device
+    col = np.random.default_rng(n).random(n, dtype=np.float32)
+    base = torch.full((n + 1,), -1.0, dtype=torch.float32, device=DEV)
+    out = base[1:]
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    device.query(t(col), 0.5, out, cnt, device.query_workspace(n, 4, DEV), "<", ordered=ordered)
+    rout, rcnt = oracle.query(col, 0.5, np.full(n, -1.0, np.float32), np.zeros(1, np.int64), "<")
+    k = int(rcnt[0])
+    assert cnt.item() == k and base[0].item() == -1.0
+    got = out.cpu().numpy()
+    np.testing.assert_array_equal(got[k:], rout[k:])
+    if ordered:
+        np.testing.assert_array_equal(got[:k], rout[:k])
+    else:
+        np.testing.assert_array_equal(np.sort(got[:k]), np.sort(rout[:k]))
+
+
+@pytest.mark.parametrize("ordered", [False, True])
 def test_query_f64(ordered):
     from paper_1902_10345_b200 import device
     rng = np.random.default_rng(9)
