@@ -148,7 +148,7 @@ class Dist:
 
 # ---------------------------------------------------------------- timing
 
-def time_steps(step, steps, warmup, dist, stream=None, graph=False):
+def time_steps(step, steps, warmup, dist, stream=None, graph=False, finish=None):
     """W untimed steps, then K steps between CUDA events on the launching
     stream, barrier + synchronize on both sides; max over ranks.  With
     ``graph`` the K steps are captured once into a CUDA graph and the timed
@@ -158,6 +158,8 @@ def time_steps(step, steps, warmup, dist, stream=None, graph=False):
     s = stream or torch.cuda.current_stream()
     for k in range(warmup):
         step(k)
+    if finish:
+        finish()
     torch.cuda.synchronize()
     g = None
     if graph:
@@ -181,6 +183,8 @@ def time_steps(step, steps, warmup, dist, stream=None, graph=False):
     else:
         for k in range(steps):
             step(warmup + k)
+    if finish:  # in-flight collectives complete inside the timed region
+        finish()
     b.record(s)
     b.synchronize()
     torch.cuda.synchronize()
@@ -224,13 +228,16 @@ def bench_histogram(args, dist, P):
         from paper_1902_10345_b200 import multigpu as MG
         be = MG.DeviceBackend()
 
+    pending = []
+
     def step(k):
-        if multi:  # each rank bins its own image; partial bins -> all_reduce (NCCL)
-            MG.histogram(dist.pg, imgs[k % nbuf], hist, oob, be)
+        if multi:  # each rank bins its own image; partial bins -> all_reduce (NCCL), overlapped
+            MG.histogram(dist.pg, imgs[k % nbuf], hist, oob, be, pending=pending)
         else:
             device.hist(imgs[k % nbuf], hist, oob)
 
-    ms = time_steps(step, args.steps, args.warmup, dist, graph=not multi)
+    ms = time_steps(step, args.steps, args.warmup, dist, graph=not multi,
+                    finish=(lambda: MG.finish_histogram(pending, hist, oob)) if multi else None)
     assert oob.item() == 0
     by = 4 * H * W + 2 * 256 * 8
     out = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms,
@@ -270,13 +277,16 @@ def bench_query(args, dist, P):
         be = MG.DeviceBackend()
         gcnt = torch.zeros(1, dtype=torch.int64, device="cuda")
 
+    pending = []
+
     def step(k, ordered=False):
-        if multi:  # per-shard compaction; global offsets from an all-gather of counts
-            MG.query(dist.pg, col, 0.5, out, gcnt, be, "<")
+        if multi:  # per-shard compaction; the count all-gather overlaps the next shard
+            MG.query(dist.pg, col, 0.5, out, gcnt, be, "<", pending=pending)
         else:
             device.query(col, 0.5, out, cnt, ws, "<", ordered=ordered)
 
-    ms = time_steps(step, args.steps, args.warmup, dist, graph=not multi)
+    ms = time_steps(step, args.steps, args.warmup, dist, graph=not multi,
+                    finish=(lambda: MG.finish_query(pending, gcnt)) if multi else None)
     total = int((gcnt if multi else cnt).item()) // (args.steps + args.warmup)
     nsel = total // dist.world  # per-rank average survivors
     by = 4 * n + 4 * nsel + 8

@@ -67,32 +67,52 @@ def _rank_world(pg):
 
 # ----------------------------------------------------------------- histogram
 
-def histogram(pg, img_shard, hist, oob, backend, scale=256.0, div=1.0):
+def histogram(pg, img_shard, hist, oob, backend, scale=256.0, div=1.0, pending=None):
     """hist += counts of the union of all ranks' shards (every rank ends with
-    the same hist); oob likewise."""
+    the same hist); oob likewise.  With a ``pending`` list the all_reduce is
+    left in flight, overlapping the next shard (finish_histogram folds it)."""
     import torch
     nb = hist.numel()
     part = torch.zeros(nb + 1, dtype=hist.dtype, device=hist.device)  # bins, then the out-of-range count
     backend.hist(img_shard, part[:nb], part[nb:], scale, div)
+    if pending is not None:
+        pending.append((part, pg.all_reduce(part, async_op=True)))
+        return
     pg.all_reduce(part)  # one collective for bins + oob
     hist += part[:nb]
     oob += part[nb:].to(oob.dtype)
 
 
+def finish_histogram(pending, hist, oob):
+    nb = hist.numel()
+    for part, work in pending:
+        work.wait()
+        hist += part[:nb]
+        oob += part[nb:].to(oob.dtype)
+    pending.clear()
+
+
 # --------------------------------------------------------------------- query
 
-def query(pg, col_shard, thr, out_shard, count, backend, op="<", gather=False):
+def query(pg, col_shard, thr, out_shard, count, backend, op="<", gather=False, pending=None):
     """Per-shard compaction.  Returns (k_local, offset, full): this rank's
     survivors are out_shard[0:k_local] and belong at global
     out_vals[offset:offset+k].  ``count`` (replicated) is advanced by the
     global survivor count.  Without ``gather`` k_local and offset are device
     tensors (nothing waits for the host); with it they are ints and rank 0
-    also receives the concatenated survivors."""
+    also receives the concatenated survivors.  With a ``pending`` list the
+    count exchange is left in flight (finish_query completes it)."""
     import torch
     rank, world = _rank_world(pg)
     local = torch.zeros(1, dtype=torch.int64, device=col_shard.device)
     backend.query(col_shard, thr, out_shard, local, op)
     counts = torch.empty(world, dtype=torch.int64, device=col_shard.device)
+    if pending is not None and not gather:
+        # streaming use: the count exchange runs on the collective's own
+        # stream and overlaps the next shard's compaction; finish_query()
+        # folds the gathered counts into ``count``
+        pending.append((counts, pg.all_gather_into_tensor(counts, local, async_op=True)))
+        return local, None, None
     pg.all_gather_into_tensor(counts, local)
     if not gather:
         # device-side bookkeeping: no host round trip per call
@@ -109,6 +129,15 @@ def query(pg, col_shard, thr, out_shard, count, backend, op="<", gather=False):
     full = torch.cat([allv[r * max(kmax, 1): r * max(kmax, 1) + cl[r]] for r in range(world)]) \
         if rank == 0 else None
     return cl[rank], offset, full
+
+
+def finish_query(pending, count):
+    """Wait for the deferred count exchanges of query(..., pending=...) and
+    advance ``count`` by every call's global survivor count."""
+    for counts, work in pending:
+        work.wait()
+        count += counts.sum()
+    pending.clear()
 
 
 # ---------------------------------------------------------------------- spmv

@@ -122,7 +122,17 @@ def _case_histogram(rank, world):
     oob = torch.zeros(1, dtype=torch.int64)
     MG.histogram(dist, torch.from_numpy(img[rank * rows:(rank + 1) * rows].copy()), hist, oob, OracleBackend())
     ref, bad = oracle.histogram(img, np.full(256, 3, np.int64))
-    return bool(np.array_equal(hist.numpy(), ref) and oob.item() == bad)
+    ok = bool(np.array_equal(hist.numpy(), ref) and oob.item() == bad)
+    # deferred all_reduce over two calls
+    hist2 = torch.full((256,), 3, dtype=torch.int64)
+    oob2 = torch.zeros(1, dtype=torch.int64)
+    pending = []
+    for _ in range(2):
+        MG.histogram(dist, torch.from_numpy(img[rank * rows:(rank + 1) * rows].copy()), hist2, oob2, OracleBackend(),
+                     pending=pending)
+    MG.finish_histogram(pending, hist2, oob2)
+    ok = ok and np.array_equal(hist2.numpy() - 3, 2 * (ref - 3)) and oob2.item() == 2 * bad
+    return ok
 
 
 def _case_query(rank, world):
@@ -141,6 +151,13 @@ def _case_query(rank, world):
     count2 = torch.full((1,), 5, dtype=torch.int64)
     k2, off2, none = MG.query(dist, shard, 0.5, out, count2, OracleBackend(), "<")
     ok = ok and none is None and int(k2) == k and int(off2) == off and count2.item() == count.item()
+    # deferred count exchanges over three calls
+    count3 = torch.full((1,), 5, dtype=torch.int64)
+    pending = []
+    for _ in range(3):
+        MG.query(dist, shard, 0.5, out, count3, OracleBackend(), "<", pending=pending)
+    MG.finish_query(pending, count3)
+    ok = ok and count3.item() == 5 + 3 * ref.size and not pending
     return bool(ok)
 
 
