@@ -286,6 +286,11 @@ def transformed_cases():
     }
     builders = {"histogram": M.histogram, "query": lambda: M.query("<"), "spmv": M.spmv,
                 "jacobi2d": M.jacobi2d, "matmul": M.matmul}
+    from sdfg import gallery
+    for name in gallery.fixture_names():
+        fx = gallery.fixture(name)
+        builders[f"gal_{name}"] = (lambda fx=fx: gallery.fixture(fx.name).sdfg)
+        inputs[f"gal_{name}"] = fx.make_inputs(np.random.default_rng(300))
     for motif, build in builders.items():
         g = build()
         for tname in sorted(registry):
