@@ -43,8 +43,11 @@ for a GPU (not translated from them):
   work-queue kernel: tickets, per-item ready flags, and quiescence when every
   pushed item has finished (codegen.py:526-543 runs P sequential workers).
 
+* a vectorised memlet (tile > 1 on the last dimension, Vectorization) runs
+  the tasklet once per lane.
+
 Not lowered (CodegenError): other consume conditions, custom WCR functions,
-vectorised (tile > 1) memlets, stream pops outside consume scopes.
+symbolic vector widths, stream pops outside consume scopes.
 """
 
 from __future__ import annotations
@@ -724,6 +727,31 @@ class Lowering:
         reads, writes = _subscripts(code)
         t = self.tcount
         self.tcount += 1
+        # Vectorization (library.py:763-840): memlets with a vector tile on
+        # their last dimension; the body runs once per lane (codegen.py:408-444)
+        width = 1
+        for e in list(st.in_edges(n.id)) + list(st.out_edges(n.id)):
+            if e.memlet.is_empty or not e.memlet.subset:
+                continue
+            tile = e.memlet.subset[-1].tile
+            if not _is_one(tile):
+                try:
+                    w = int(X.evaluate(tile, {}))
+                except X.ExprError as exc:
+                    raise LoweringError(f"tasklet '{n.name}': symbolic vector width") from exc
+                if width not in (1, w):
+                    raise LoweringError(f"tasklet '{n.name}': mixed vector widths {width} and {w}")
+                width = w
+        lane = f"lv{t}"
+
+        def point(sub):
+            pt = [env.emit(r.begin) for r in sub]
+            if width > 1 and not _is_one(sub[-1].tile):
+                pt[-1] = f"({pt[-1]}) + {lane}"
+            return pt
+        if width > 1:
+            out.append(f"{ind}for (int64_t {lane} = 0; {lane} < {width}; ++{lane}) {{")
+            ind = ind + "    "
         out.append(f"{ind}{{  /* tasklet {n.name} */")
         ind2 = ind + "    "
         types, names, aread, awrite, dynamic = {}, {}, {}, {}, set()
@@ -740,8 +768,6 @@ class Lowering:
                     names[c] = v
                     continue
                 raise LoweringError("stream pops outside a consume scope are not lowered")
-            if any(not _is_one(r.tile) for r in m.subset):
-                raise LoweringError("vectorised memlets are not lowered")
             v = f"k{t}_{_ident(c)}"
             if c in reads:
                 out.append(f"{ind2}const {CT[d.basetype]}* {v} = {self.cname(m.data)} + "
@@ -749,7 +775,7 @@ class Lowering:
                 # indexes run from the block origin through the container (codegen.py:417-420)
                 aread[c] = (v, f"({self.size_expr(m.data, env)} - ({self.origin(m.data, m.subset, env)}))")
             else:
-                pt = [env.emit(r.begin) for r in m.subset]
+                pt = point(m.subset)
                 out.append(f"{ind2}const {CT[d.basetype]} {v} = {self.cname(m.data)}"
                            f"[{self.flat(m.data, pt, env)}];")
             names[c] = v
@@ -800,7 +826,7 @@ class Lowering:
                         out.append(f"{ind2}{guard}stream_push({self.cname(target.data)}, n_{s}, cap_{s}, {v}, g_err);")
                     continue
                 sub = m.subset if m.data == target.data or m.reindex is None else m.reindex
-                pt = [env.emit(r.begin) for r in sub]
+                pt = point(sub)
                 lv = f"{self.cname(target.data)}[{self.flat(target.data, pt, env)}]"
                 if m.wcr is None:
                     out.append(f"{ind2}{guard}{lv} = {v};")
@@ -810,6 +836,8 @@ class Lowering:
                 else:
                     raise LoweringError(f"custom WCR '{m.wcr}' is not lowered")
         out.append(f"{ind}}}")
+        if width > 1:
+            out.append(f"{ind[:-4]}}}")
 
     # -- nested graphs ----------------------------------------------------------
 

@@ -310,7 +310,23 @@ def transformed_cases():
             save_case(name, "small", g2, {k: np.array(v, copy=True) for k, v in arrays.items()}, symbols)
 
 
+def vector_cases():
+    """Vectorization (library.py:763-840): an element-wise map widened to 4-
+    and 8-lane tiles; the same inputs through the plain graph."""
+    from sdfg.rewriting import apply_transformation, find_matches
+    rng = np.random.default_rng(31)
+    arrays = {"x": rng.random(64), "y": rng.random(64), "a": np.array([1.75])}
+    g = M.axpy(64)
+    save_graph("axpy", g)
+    save_case("axpy", "n64", g, dict(arrays), {})
+    for w in (4, 8):
+        gv, _ = apply_transformation(g, find_matches(g, "Vectorization")[0], {"width": w})
+        save_graph(f"x_axpy_Vectorization{w}", gv)
+        save_case(f"x_axpy_Vectorization{w}", "n64", gv, {k: v.copy() for k, v in arrays.items()}, {})
+
+
 if __name__ == "__main__":
+    vector_cases()
     transformed_cases()
     gallery_cases()
     histogram_cases()

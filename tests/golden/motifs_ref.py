@@ -131,6 +131,26 @@ def laplace1d() -> Sdfg:
     return gallery.fixture("laplace").sdfg
 
 
+def axpy(n: int = 64) -> Sdfg:
+    """Element-wise ``y[i] = a * x[i] + y[i]`` over a constant-length map --
+    the shape the reference's Vectorization rule applies to
+    (library.py:763-840)."""
+    g = Sdfg("axpy")
+    g.add_array("x", [str(n)], "float64")
+    g.add_array("y", [str(n)], "float64")
+    g.add_array("a", ["1"], "float64")
+    st = g.add_state("main", is_start=True)
+    xr, yr, ar, yw = st.add_access("x"), st.add_access("y"), st.add_access("a"), st.add_access("y")
+    me, mx = st.add_map("i", f"0:{n - 1}")
+    t = st.add_tasklet("fma", ["xi", "yi", "av"], ["o"], "o = av * xi + yi")
+    st.add_memlet_path(xr, me, t, dst_conn="xi", memlet=Memlet.simple("x", "[i]"))
+    st.add_memlet_path(yr, me, t, dst_conn="yi", memlet=Memlet.simple("y", "[i]"))
+    st.add_memlet_path(ar, me, t, dst_conn="av", memlet=Memlet.simple("a", "[0]"))
+    st.add_memlet_path(t, mx, yw, src_conn="o", memlet=Memlet.simple("y", "[i]"))
+    g.finalize()
+    return g
+
+
 def matmul_raw() -> Sdfg:
     return gallery.fixture("matmul").sdfg
 
