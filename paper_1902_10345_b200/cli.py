@@ -217,8 +217,9 @@ def execution_report(g: Graph, symbols: dict) -> dict:
                 # a scope instance reads the memlet's whole block (interpreter.py:531-533)
                 def vol(pe, sub=m.subset):
                     v = 1
-                    for r in sub:
-                        v *= max(0, int(X.evaluate(r.end, pe)) - int(X.evaluate(r.begin, pe)) + 1)
+                    for r in sub:  # points x vector tile (symbolic.py:579-618)
+                        b, en, sd = (int(X.evaluate(x, pe)) for x in (r.begin, r.end, r.stride))
+                        v *= max(0, (en - b) // sd + 1) * int(X.evaluate(r.tile, pe))
                     return v
                 cnt = _instances(st, parent, scope, env, per_point=vol)
             else:
