@@ -46,6 +46,7 @@ class Memlet:
     reindex: Optional[tuple] = None
     accesses: Optional[Expr] = None
     wcr: Optional[str] = None
+    wcr_doc: Optional[dict] = None  # custom WCR: code, inputs, outputs, identity (serialization.py:40-49)
 
     @property
     def is_empty(self) -> bool:
@@ -187,6 +188,7 @@ def _memlet(doc: dict) -> Memlet:
         reindex=parse_subset(doc["reindex"]) if "reindex" in doc else None,
         accesses=parse_expr(doc["accesses"]) if "accesses" in doc else None,
         wcr=(doc.get("wcr") or {}).get("kind"),
+        wcr_doc=doc.get("wcr"),
     )
 
 

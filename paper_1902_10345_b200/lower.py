@@ -46,8 +46,11 @@ for a GPU (not translated from them):
 * a vectorised memlet (tile > 1 on the last dimension, Vectorization) runs
   the tasklet once per lane.
 
-Not lowered (CodegenError): other consume conditions, custom WCR functions,
-symbolic vector widths, stream pops outside consume scopes.
+* a custom WCR (ir.py:100-121) becomes a __device__ combine function
+  translated from its tasklet, applied with a compare-and-swap loop.
+
+Not lowered (CodegenError): other consume conditions, symbolic vector
+widths, stream pops outside consume scopes.
 """
 
 from __future__ import annotations
@@ -508,6 +511,7 @@ class Lowering:
                         if e.dst_conn == "IN_stream" and not e.memlet.is_empty:
                             self.consumed.add(e.memlet.data)
         self.pop_vars: dict = {}  # stream -> C variable of the element a consume worker popped
+        self.custom_wcr: dict = {}
 
     # -- containers ---------------------------------------------------------
 
@@ -598,6 +602,40 @@ class Lowering:
         a += [f"s_{_ident(s)}" for s in self.sym_names]
         a.append("g_err")
         return ", ".join(a)
+
+    # -- custom write-conflict resolution --------------------------------------
+
+    def wcr_fn(self, m, basetype: str) -> str:
+        """Name of the combine function for memlet ``m``: a built-in one, or a
+        __device__ function translated from the custom WCR's tasklet
+        (ir.py:100-121: ``out = f(old, new)``)."""
+        if m.wcr in ("sum", "product", "min", "max"):
+            return m.wcr
+        if m.wcr != "custom" or not m.wcr_doc or "code" not in m.wcr_doc:
+            raise LoweringError(f"WCR '{m.wcr}' is not lowered")
+        doc = m.wcr_doc
+        key = (doc["code"], tuple(doc["inputs"]), tuple(doc["outputs"]), basetype)
+        if key not in self.custom_wcr:
+            old, new = doc["inputs"]
+            out = doc["outputs"][0]
+            name = f"custom{len(self.custom_wcr)}"
+            types = {old: basetype, new: basetype, out: basetype}
+            names = {old: "a_old", new: "a_new", out: "r_out"}
+            tc = TaskletC(ast.parse(doc["code"]).body, types, names, {}, {}, {out}, set())
+            t = CT[basetype]
+            body = "\n".join(tc.emit("    "))
+            self.devfns.insert(0, f"GEN_HD {t} wcr_{name}_f({t} a_old, {t} a_new) {{\n    {t} r_out = 0;\n"
+                                  f"{body}\n    return r_out;\n}}\n"
+                                  f"GEN_DEV void wcr_{name}({t}* p, {t} v) {{ wcr_cas(p, v, [](const {t} a, const {t} b) "
+                                  f"{{ return wcr_{name}_f(a, b); }}); }}\n"
+                                  f"GEN_HD void pwcr_{name}({t}* p, {t} v) {{ *p = wcr_{name}_f(*p, v); }}\n"
+                                  f"#define GEN_WR_{name} 1\n"
+                                  f"template <typename T> GEN_DEV void g_wr_{name}(T* p, int64_t i, int64_t n, T v, "
+                                  f"int* err) {{ if (i < 0 || i >= n) {{ gen_fail(err, 1); return; }} wcr_{name}(p + i, v); }}\n"
+                                  f"template <typename T> GEN_DEV void g_wr_p{name}(T* p, int64_t i, int64_t n, T v, "
+                                  f"int* err) {{ if (i < 0 || i >= n) {{ gen_fail(err, 1); return; }} pwcr_{name}(p + i, v); }}\n")
+            self.custom_wcr[key] = name
+        return self.custom_wcr[key]
 
     # -- write targets --------------------------------------------------------
 
@@ -792,11 +830,10 @@ class Lowering:
             v = f"k{t}_{_ident(c)}"
             names[c] = v
             if c in writes:
-                if m.wcr not in (None, "sum", "product", "min", "max"):
-                    raise LoweringError(f"custom WCR '{m.wcr}' is not lowered")
+                fn = None if m.wcr is None else self.wcr_fn(m, td.basetype)
                 priv = tg[0].data in self.private
                 out.append(f"{ind2}{CT[td.basetype]}* {v} = {self.cname(tg[0].data)};")
-                awrite[c] = (v, self.size_expr(tg[0].data, env), m.wcr, priv)
+                awrite[c] = (v, self.size_expr(tg[0].data, env), fn, priv)
                 continue
             out.append(f"{ind2}{CT[td.basetype]} {v} = 0;")
             if m.is_dynamic:
@@ -830,11 +867,10 @@ class Lowering:
                 lv = f"{self.cname(target.data)}[{self.flat(target.data, pt, env)}]"
                 if m.wcr is None:
                     out.append(f"{ind2}{guard}{lv} = {v};")
-                elif m.wcr in ("sum", "product", "min", "max"):
-                    priv = target.data in self.private
-                    out.append(f"{ind2}{guard}{'p' if priv else ''}wcr_{m.wcr}(&{lv}, ({CT[td.basetype]})({v}));")
                 else:
-                    raise LoweringError(f"custom WCR '{m.wcr}' is not lowered")
+                    fn = self.wcr_fn(m, td.basetype)
+                    priv = target.data in self.private
+                    out.append(f"{ind2}{guard}{'p' if priv else ''}wcr_{fn}(&{lv}, ({CT[td.basetype]})({v}));")
         out.append(f"{ind}}}")
         if width > 1:
             out.append(f"{ind[:-4]}}}")
@@ -1091,14 +1127,21 @@ class Lowering:
         ine = next(e for e in st.in_edges(n.id) if e.dst_conn == "in")
         oute = next(e for e in st.out_edges(n.id) if e.src_conn == "out")
         tgt = self.targets(st, oute)[0]
-        wcr = n.doc.get("wcr", {}).get("kind") if isinstance(n.doc.get("wcr"), dict) else n.doc.get("wcr")
-        if wcr not in ("sum", "product", "min", "max"):
-            raise LoweringError(f"reduce with '{wcr}' is not lowered")
+        wdoc = n.doc.get("wcr") if isinstance(n.doc.get("wcr"), dict) else {"kind": n.doc.get("wcr")}
+        kind = wdoc.get("kind")
         axes = [int(a) for a in n.doc.get("axes", [])]
         td = self.g.data[tgt.data]
-        ident = {("sum", "float64"): "0.0", ("sum", "int64"): "0LL", ("product", "float64"): "1.0",
-                 ("product", "int64"): "1LL", ("min", "float64"): "INFINITY", ("max", "float64"): "-INFINITY",
-                 ("min", "int64"): "INT64_MAX", ("max", "int64"): "INT64_MIN"}[(wcr, td.basetype)]
+
+        class _M:  # the reduce's resolution, shaped like a memlet for wcr_fn
+            wcr, wcr_doc = kind, wdoc
+        wcr = self.wcr_fn(_M, td.basetype)
+        if kind == "custom":
+            iv = float(wdoc["identity"])
+            ident = repr(iv) if td.basetype == "float64" else f"{int(iv)}LL"
+        else:
+            ident = {("sum", "float64"): "0.0", ("sum", "int64"): "0LL", ("product", "float64"): "1.0",
+                     ("product", "int64"): "1LL", ("min", "float64"): "INFINITY", ("max", "float64"): "-INFINITY",
+                     ("min", "int64"): "INT64_MAX", ("max", "int64"): "INT64_MIN"}[(kind, td.basetype)]
         denv = Env(self, {}, host=False)
         tsub = oute.memlet.subset if oute.memlet.data == tgt.data else oute.memlet.reindex
         isub = ine.memlet.subset

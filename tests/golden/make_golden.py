@@ -325,7 +325,15 @@ def vector_cases():
         save_case(f"x_axpy_Vectorization{w}", "n64", gv, {k: v.copy() for k, v in arrays.items()}, {})
 
 
+def custom_wcr_cases():
+    g = M.maxabs(200, 7)
+    save_graph("maxabs", g)
+    rng = np.random.default_rng(41)
+    save_case("maxabs", "n200", g, {"x": rng.uniform(-1, 1, 200), "out": np.full(7, 0.5)}, {})
+
+
 if __name__ == "__main__":
+    custom_wcr_cases()
     vector_cases()
     transformed_cases()
     gallery_cases()

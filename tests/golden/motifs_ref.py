@@ -151,6 +151,28 @@ def axpy(n: int = 64) -> Sdfg:
     return g
 
 
+def maxabs(n: int = 200, bins: int = 7) -> Sdfg:
+    """``out[i % B] = x[i]`` under a custom WCR keeping the smallest
+    magnitude (ir.py:100-121 custom WcrFunc with its own identity)."""
+    from sdfg.ir import WcrFunc
+    from sdfg.tasklets import parse_tasklet
+    g = Sdfg("maxabs")
+    g.add_array("x", [str(n)], "float64")
+    g.add_array("out", [str(bins)], "float64")
+    st = g.add_state("main", is_start=True)
+    me, mx = st.add_map("i", f"0:{n - 1}")
+    t = st.add_tasklet("pick", ["v"], ["o"], "o = v")
+    # the reference applies WCR on blocks (interpreter.py:300-303), so the
+    # function must be branch-free: smallest magnitude seen so far
+    keep = WcrFunc("custom", custom=parse_tasklet("out = min(old, abs(new))", ["old", "new"], ["out"]),
+                   custom_identity=1e300)
+    st.add_memlet_path(st.add_access("x"), me, t, dst_conn="v", memlet=Memlet.simple("x", "[i]"))
+    st.add_memlet_path(t, mx, st.add_access("out"), src_conn="o",
+                       memlet=Memlet.simple("out", f"[i % {bins}]", wcr=keep))
+    g.finalize()
+    return g
+
+
 def matmul_raw() -> Sdfg:
     return gallery.fixture("matmul").sdfg
 

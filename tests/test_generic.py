@@ -25,7 +25,7 @@ from paper_1902_10345_b200.lower import LoweringError, lower
 GALLERY = ["branching", "fibonacci", "histogram", "indirection", "laplace", "mandelbrot", "matmul", "query",
            "spmv"]
 MOTIF_GRAPHS = ["histogram", "histogram_int", "query", "query_gallery", "spmv", "jacobi2d", "laplace1d",
-                "matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "axpy"]
+                "matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "axpy", "maxabs"]
 # every motif graph after every reference transformation that matches it
 TRANSFORMED = sorted(os.path.basename(p)[:-len(".sdfg.json")]
                      for p in glob.glob(os.path.join(os.path.dirname(graph_path("x")), "x_*.sdfg.json")))
