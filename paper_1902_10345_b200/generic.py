@@ -34,7 +34,8 @@ _STATUS = {1: (OutOfBoundsError, "subscript write out of bounds"),
            2: (ExecutionError, "subscript read out of bounds"),
            3: (ExecutionError, "stream overflow"),
            4: (OutOfBoundsError, "stream drain overflows its target array"),
-           5: (ExecutionError, "consume scope made no progress (watchdog)")}
+           5: (ExecutionError, "consume scope made no progress (watchdog)"),
+           6: (OutOfBoundsError, "memlet index outside its container")}
 
 
 def nvcc() -> str:

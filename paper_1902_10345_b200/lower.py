@@ -138,7 +138,8 @@ template <typename T> GEN_HD void pwcr_max(T* p, T v) { *p = v > *p ? v : *p; }
 
 // first error wins: 1 = out-of-bounds subscript write, 2 = out-of-bounds
 // subscript read, 3 = stream overflow, 4 = drain overflows its target,
-// 5 = a consume worker waited past its watchdog
+// 5 = a consume worker waited past its watchdog, 6 = a memlet index outside
+// its container (OutOfBoundsError, interpreter.py:216-233)
 GEN_DEV void gen_fail(int* err, int code) { atomicCAS(err, 0, code); }
 
 template <typename T>
@@ -536,6 +537,12 @@ class Lowering:
             out = f"(({out}) * ({env.emit(d.dims[k])}) + ({idx[k]}))"
         return out
 
+    def in_bounds(self, data: str, idx: list, env: Env) -> str:
+        """Every index inside its dimension (the interpreter checks each
+        access, interpreter.py:216-233; the C path does not)."""
+        d = self.g.data[data]
+        return " && ".join(f"(uint64_t)({i}) < (uint64_t)({env.emit(dim)})" for i, dim in zip(idx, d.dims))
+
     def size_expr(self, data: str, env: Env) -> str:
         d = self.g.data[data]
         return "(" + " * ".join(f"({env.emit(x)})" for x in d.dims) + ")"
@@ -814,8 +821,9 @@ class Lowering:
                 aread[c] = (v, f"({self.size_expr(m.data, env)} - ({self.origin(m.data, m.subset, env)}))")
             else:
                 pt = point(m.subset)
-                out.append(f"{ind2}const {CT[d.basetype]} {v} = {self.cname(m.data)}"
-                           f"[{self.flat(m.data, pt, env)}];")
+                out.append(f"{ind2}const {CT[d.basetype]} {v} = ({self.in_bounds(m.data, pt, env)}) ? "
+                           f"{self.cname(m.data)}[{self.flat(m.data, pt, env)}] : "
+                           f"(gen_fail(g_err, 6), ({CT[d.basetype]})0);")
             names[c] = v
         commits = []
         for e in st.out_edges(n.id):
@@ -865,6 +873,8 @@ class Lowering:
                 sub = m.subset if m.data == target.data or m.reindex is None else m.reindex
                 pt = point(sub)
                 lv = f"{self.cname(target.data)}[{self.flat(target.data, pt, env)}]"
+                ok = self.in_bounds(target.data, pt, env)
+                guard = f"{guard}if (!({ok})) gen_fail(g_err, 6); else "
                 if m.wcr is None:
                     out.append(f"{ind2}{guard}{lv} = {v};")
                 else:

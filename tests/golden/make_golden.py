@@ -325,6 +325,22 @@ def vector_cases():
         save_case(f"x_axpy_Vectorization{w}", "n64", gv, {k: v.copy() for k, v in arrays.items()}, {})
 
 
+def oob_cases():
+    """test_interpreter.py:176-189: a static memlet read past the container
+    raises (InterpreterError naming the memlet)."""
+    from sdfg.ir import Memlet as Mm, Sdfg as Sg
+    g = Sg("oob")
+    g.add_array("x", ["4"], "float64")
+    g.add_array("y", ["4"], "float64")
+    st = g.add_state("s", is_start=True)
+    t = st.add_tasklet("t", ["a"], ["b"], "b = a")
+    st.add_edge(st.add_access("x"), None, t, "a", Mm.simple("x", "[7]"))
+    st.add_edge(t, "b", st.add_access("y"), None, Mm.simple("y", "[0]"))
+    g.finalize()
+    save_graph("oob", g)
+    save_case("oob", "read7", g, {"x": np.zeros(4), "y": np.zeros(4)}, {})
+
+
 def custom_wcr_cases():
     g = M.maxabs(200, 7)
     save_graph("maxabs", g)
@@ -333,6 +349,7 @@ def custom_wcr_cases():
 
 
 if __name__ == "__main__":
+    oob_cases()
     custom_wcr_cases()
     vector_cases()
     transformed_cases()

@@ -25,7 +25,7 @@ from paper_1902_10345_b200.lower import LoweringError, lower
 GALLERY = ["branching", "fibonacci", "histogram", "indirection", "laplace", "mandelbrot", "matmul", "query",
            "spmv"]
 MOTIF_GRAPHS = ["histogram", "histogram_int", "query", "query_gallery", "spmv", "jacobi2d", "laplace1d",
-                "matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "axpy", "maxabs"]
+                "matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "axpy", "maxabs", "oob"]
 # every motif graph after every reference transformation that matches it
 TRANSFORMED = sorted(os.path.basename(p)[:-len(".sdfg.json")]
                      for p in glob.glob(os.path.join(os.path.dirname(graph_path("x")), "x_*.sdfg.json")))
@@ -110,7 +110,8 @@ def test_generic_matches_reference_interpreter(graph, case, cuda_ok):
     from paper_1902_10345_b200.generic import compile_generic
     prog = compile_generic(_doc(graph))
     if case.error:
-        with pytest.raises(ExecutionError):
+        from paper_1902_10345_b200 import OutOfBoundsError
+        with pytest.raises(OutOfBoundsError if case.error == "OutOfBoundsError" else ExecutionError):
             prog.run(case.inputs, case.symbols)
         return
     _compare(graph, case, prog.run(case.inputs, case.symbols))
