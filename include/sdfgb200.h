@@ -147,6 +147,10 @@ int sdfgb_gemm_f32(const float* A, const float* B, float* C,
  * cross-check of the tensor-core path in tests. */
 int sdfgb_gemm_f32_simt(const float* A, const float* B, float* C,
                         int64_t M, int64_t N, int64_t K, void* stream);
+/* Native precision (float64): k-ordered IEEE multiply + add per element,
+ * bit-identical to the reference's MapReduceFusion loop after init_C. */
+int sdfgb_gemm_f64(const double* A, const double* B, double* C,
+                   int64_t M, int64_t N, int64_t K, void* stream);
 
 /* -------------------------------------------------------- host entries
  * Drop-in for CompiledSdfg._fn(*ptrs, *syms) (codegen.py:886): host
@@ -175,6 +179,8 @@ int sdfgb_host_jacobi2d(double* A, int64_t N, int64_t T, double coef,
 /* void matmul(double* A, double* B, double* C, int64_t M, int64_t N, int64_t K) */
 int sdfgb_host_matmul(const double* A, const double* B, double* C,
                       int64_t M, int64_t N, int64_t K);
+int sdfgb_host_matmul_f64(const double* A, const double* B, double* C,
+                          int64_t M, int64_t N, int64_t K);
 
 #ifdef __cplusplus
 }

@@ -50,12 +50,14 @@ SIGNATURES = {
     "sdfgb_gemm_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
     "sdfgb_gemm_f32": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _SZ, _P]),
     "sdfgb_gemm_f32_simt": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P]),
+    "sdfgb_gemm_f64": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "sdfgb_host_histogram": (_INT, [_P, _P, _I64, _I64, _I64, _F64, _F64, _INT]),
     "sdfgb_host_histogram_i64": (_INT, [_P, _P, _I64, _I64, _I64]),
     "sdfgb_host_query": (_INT, [_P, _P, _P, _P, _I64, _INT, _INT]),
     "sdfgb_host_spmv": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _INT]),
     "sdfgb_host_jacobi2d": (_INT, [_P, _I64, _I64, _F64, _P, _P, _INT, _INT]),
     "sdfgb_host_matmul": (_INT, [_P, _P, _P, _I64, _I64, _I64]),
+    "sdfgb_host_matmul_f64": (_INT, [_P, _P, _P, _I64, _I64, _I64]),
 }
 
 

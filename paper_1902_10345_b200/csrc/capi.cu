@@ -378,6 +378,25 @@ extern "C" int sdfgb_host_jacobi2d(double* A, int64_t N, int64_t T, double coef,
 }
 
 // --------------------------------------------------------------------- matmul
+extern "C" int sdfgb_host_matmul_f64(const double* A, const double* B, double* C, int64_t M, int64_t N, int64_t K) {
+    // native precision: float64 end to end, k-ordered IEEE multiply + add
+    if (M < 0 || N < 0 || K < 0 || (M * N > 0 && !C) || (M * K > 0 && !A) || (K * N > 0 && !B))
+        return set_error(SDFGB_ERR_INVALID, "matmul: bad arguments");
+    if (M == 0 || N == 0) return SDFGB_OK;
+    Session ss;
+    SDFGB_TRY(ss.open());
+    cudaStream_t s = ss.s();
+    double* dd;
+    SDFGB_TRY(ss.get(0, M * K + K * N + M * N, &dd));
+    double *dA = dd, *dB = dd + M * K, *dC = dB + K * N;
+    SDFGB_TRY(h2d(dA, A, M * K, s));
+    SDFGB_TRY(h2d(dB, B, K * N, s));
+    SDFGB_TRY(sdfgb_gemm_f64(dA, dB, dC, M, N, K, s));
+    SDFGB_TRY(d2h(C, dC, M * N, s));
+    SDFGB_CUDA(cudaStreamSynchronize(s));
+    return SDFGB_OK;
+}
+
 extern "C" int sdfgb_host_matmul(const double* A, const double* B, double* C, int64_t M, int64_t N, int64_t K) {
     if (M < 0 || N < 0 || K < 0 || (M * N > 0 && !C) || (M * K > 0 && !A) || (K * N > 0 && !B))
         return set_error(SDFGB_ERR_INVALID, "matmul: bad arguments");

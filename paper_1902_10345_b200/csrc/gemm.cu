@@ -473,22 +473,37 @@ gemm_3xtf32_flush_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_
     }
 }
 
-// ------------------------------------------------------------ SIMT cross-check
-// 64x64 tile, 256 threads, 4x4 per thread, k-sequential FFMA per element.
+// ------------------------------------------------------------ SIMT GEMMs
+// 64x64 tile, 256 threads, 4x4 per thread, each element accumulated over k in
+// order.  float: FFMA (the cross-check of the tensor-core kernel).  double
+// (native precision): separate IEEE multiply and add from 0 in k order --
+// exactly the reference's MapReduceFusion loop `C += A*B` after init_C
+// (library.py:461-554; its C is compiled without FMA contraction), so the
+// result is bit-identical to the reference's generated code.
+template <typename T>
+__device__ __forceinline__ T mac(T acc, T a, T b);
+template <>
+__device__ __forceinline__ float mac<float>(float acc, float a, float b) { return fmaf(a, b, acc); }
+template <>
+__device__ __forceinline__ double mac<double>(double acc, double a, double b) {
+    return __dadd_rn(acc, __dmul_rn(a, b));
+}
+
+template <typename T>
 __global__ void __launch_bounds__(256)
-gemm_simt_kernel(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
+gemm_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
                  int64_t M, int64_t N, int64_t K) {
-    __shared__ float As[16][64 + 4];
-    __shared__ float Bs[16][64 + 4];
+    __shared__ T As[16][64 + 4];
+    __shared__ T Bs[16][64 + 4];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
     const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
-    float acc[4][4] = {};
+    T acc[4][4] = {};
     for (int64_t k0 = 0; k0 < K; k0 += 16) {
         for (int e = threadIdx.x; e < 16 * 64; e += 256) {
             const int kk = e % 16, mm = e / 16;
-            As[kk][mm] = (m0 + mm < M && k0 + kk < K) ? A[(m0 + mm) * K + k0 + kk] : 0.f;
+            As[kk][mm] = (m0 + mm < M && k0 + kk < K) ? A[(m0 + mm) * K + k0 + kk] : T(0);
             const int nn = e % 64, kb = e / 64;
-            Bs[kb][nn] = (n0 + nn < N && k0 + kb < K) ? B[(k0 + kb) * N + n0 + nn] : 0.f;
+            Bs[kb][nn] = (n0 + nn < N && k0 + kb < K) ? B[(k0 + kb) * N + n0 + nn] : T(0);
         }
         __syncthreads();
 #pragma unroll
@@ -496,7 +511,7 @@ gemm_simt_kernel(const float* __restrict__ A, const float* __restrict__ B, float
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(As[kk][ty * 4 + i], Bs[kk][tx * 4 + j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) acc[i][j] = mac<T>(acc[i][j], As[kk][ty * 4 + i], Bs[kk][tx * 4 + j]);
         __syncthreads();
     }
     for (int i = 0; i < 4; ++i)
@@ -588,7 +603,19 @@ extern "C" int sdfgb_gemm_f32_simt(const float* A, const float* B, float* C, int
         return set_error(SDFGB_ERR_INVALID, "gemm_simt: bad arguments");
     if (M == 0 || N == 0) return SDFGB_OK;
     dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64));
-    gemm_simt_kernel<<<grid, 256, 0, as_stream(stream)>>>(A, B, C, M, N, K);
+    gemm_simt_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(A, B, C, M, N, K);
+    SDFGB_LAUNCHED("gemm_simt_kernel");
+    return SDFGB_OK;
+}
+
+extern "C" int sdfgb_gemm_f64(const double* A, const double* B, double* C, int64_t M, int64_t N, int64_t K,
+                              void* stream) {
+    using namespace sdfgb;
+    if (M < 0 || N < 0 || K < 0 || (M * N > 0 && (!C || (K > 0 && (!A || !B)))))
+        return set_error(SDFGB_ERR_INVALID, "gemm_f64: bad arguments");
+    if (M == 0 || N == 0) return SDFGB_OK;
+    dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64));
+    gemm_simt_kernel<double><<<grid, 256, 0, as_stream(stream)>>>(A, B, C, M, N, K);
     SDFGB_LAUNCHED("gemm_simt_kernel");
     return SDFGB_OK;
 }

@@ -144,6 +144,18 @@ def gemm(A, B, C, ws, stream=None):
     _lib.check(L.sdfgb_gemm_f32(_p(A), _p(B), _p(C), M, N, K, _p(ws), ws.numel(), _stream(stream)))
 
 
+def gemm_f64(A, B, C, stream=None):
+    """C = A @ B in float64, each element summed in k order with separately
+    rounded multiply and add (the reference's MapReduceFusion loop)."""
+    import torch
+    L = _lib.load()
+    for t, n in ((A, "A"), (B, "B"), (C, "C")):
+        _require(t, torch.float64, n)
+    M, K = A.shape
+    N = B.shape[1]
+    _lib.check(L.sdfgb_gemm_f64(_p(A), _p(B), _p(C), M, N, K, _stream(stream)))
+
+
 def gemm_simt(A, B, C, stream=None):
     L = _lib.load()
     M, K = A.shape

@@ -273,7 +273,8 @@ class CompiledB200Sdfg:
         A, B, C = b[plan.roles["A"]], b[plan.roles["B"]], b[plan.roles["C"]]
         M, K = plan.shape(plan.roles["A"], syms)
         N = plan.shape(plan.roles["B"], syms)[1]
-        _lib.check(self._lib.sdfgb_host_matmul(_ptr(A), _ptr(B), _ptr(C), M, N, K))
+        fn = self._lib.sdfgb_host_matmul_f64 if prec == _lib.PREC_NATIVE else self._lib.sdfgb_host_matmul
+        _lib.check(fn(_ptr(A), _ptr(B), _ptr(C), M, N, K))
 
 
 def compile_b200(sdfg: Any, precision: str = "fp32") -> CompiledB200Sdfg:

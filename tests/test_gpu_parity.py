@@ -64,8 +64,6 @@ def _f32_exact(a):
 @pytest.mark.parametrize("precision", ["native", "fp32"])
 @pytest.mark.parametrize("c", CASES, ids=repr)
 def test_dropin_matches_reference_interpreter(c, precision, order):
-    if c.motif.startswith("matmul") and precision == "native":
-        pytest.skip("GEMM runs 3xTF32 only")
     if order == "fifo" and not c.motif.startswith("query"):
         pytest.skip("stream order only applies to the query motif")
     prog = b200.invoke_toolchain(b200.generate(marked(c.motif, precision, order)))
@@ -107,6 +105,13 @@ def test_dropin_matches_reference_interpreter(c, precision, order):
         elif c.motif == "spmv":
             rtol = 1e-12 if precision == "native" else 1e-5
             np.testing.assert_allclose(g, exp, rtol=rtol, atol=rtol * (np.abs(exp).max() + 1e-30))
+        elif precision == "native":  # matmul, float64 k-ordered multiply + add
+            if c.motif == "matmul":
+                # MapReduceFusion form: the interpreter accumulates WCR sums in k order
+                np.testing.assert_array_equal(g, exp, err_msg=name)
+            else:
+                # Reduce node form: numpy's pairwise add.reduce order (interpreter.py:619)
+                np.testing.assert_allclose(g, exp, rtol=1e-12, atol=1e-12 * (np.abs(exp).max() + 1e-30))
         else:  # matmul, 3xTF32
             scale = np.abs(exp).max() + 1e-30
             assert np.abs(g - exp).max() / scale < 1e-4, name
@@ -348,6 +353,21 @@ def test_gemm_3xtf32(M, N, K):
     C2 = torch.zeros((M, N), dtype=torch.float32, device=DEV)
     device.gemm_simt(t(a), t(b), C2)
     assert (np.abs(C2.cpu().numpy() - ref) / scale).max() < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (5, 7, 3), (65, 130, 47), (256, 128, 300), (3, 2, 0)])
+def test_gemm_f64_native_is_k_ordered(M, N, K):
+    """native precision: bit-identical to the k-ordered WCR sum (0 + p0 + p1 + ...)"""
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(M * N + K)
+    a = rng.random((M, K)) - 0.5
+    b = rng.random((K, N)) - 0.5
+    ref = np.zeros((M, N))
+    for k in range(K):
+        ref = ref + a[:, k:k + 1] * b[k:k + 1, :]
+    C = torch.full((M, N), 7.0, dtype=torch.float64, device=DEV)
+    device.gemm_f64(t(a), t(b), C)
+    np.testing.assert_array_equal(C.cpu().numpy(), ref)
 
 
 # ------------------------------------------------ BASELINE shapes (properties)
