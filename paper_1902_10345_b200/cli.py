@@ -33,6 +33,7 @@ import numpy as np
 from . import expr as X
 from .dispatch import STORAGE_PREFIX, generate, gpu_storage, invoke_toolchain
 from .errors import CodegenError, ExecutionError, ToolchainError
+from .generic import compile_generic
 from .graph import Graph, GraphFormatError, from_json
 
 EXIT_OK, EXIT_VALIDATION, EXIT_USAGE, EXIT_RUNTIME = 0, 1, 2, 3
@@ -258,18 +259,29 @@ def cmd_run(args) -> int:
         arrays = {k: np.asarray(v) for k, v in t.get("arrays", {}).items()}
         symbols = {k: int(v) for k, v in t.get("symbols", {}).items()}
     marked = _mark(doc, args.precision, args.stream_order)
-    code = generate(marked)
-    prog = invoke_toolchain(code)
-    outputs = prog.run(arrays, symbols)
     g = from_json(marked)
-    rep = {"outputs": {}, "backend": "b200",
-           "path": f"motif:{code.plan.motif}" if code.plan is not None else "generic",
-           "precision": code.precision, "stream_order": code.stream_order}
+    measured = None
+    if args.report == "device":
+        # the generic lowering's counter build: every edge measured on the GPU
+        prog = compile_generic(from_json(doc), report=True)
+        outputs, measured = prog.run_report(arrays, symbols)
+        rep = {"outputs": {}, "backend": "b200", "path": "generic", "precision": "native",
+               "stream_order": "any", "report": "device"}
+    else:
+        code = generate(marked)
+        prog = invoke_toolchain(code)
+        outputs = prog.run(arrays, symbols)
+        rep = {"outputs": {}, "backend": "b200",
+               "path": f"motif:{code.plan.motif}" if code.plan is not None else "generic",
+               "precision": code.precision, "stream_order": code.stream_order, "report": "static"}
     for name, arr in outputs.items():
         shape = [int(X.evaluate(d, symbols)) for d in g.data[name].dims]
         a = np.asarray(arr).reshape(shape)
         rep["outputs"][name] = a.tolist() if a.size <= 4096 else {"truncated": True, "size": int(a.size)}
-    rep.update({k: v for k, v in execution_report(g, symbols).items() if v is not None})
+    if measured is not None:
+        rep.update(measured)
+    else:
+        rep.update({k: v for k, v in execution_report(g, symbols).items() if v is not None})
     print(json.dumps(rep, indent=2, sort_keys=True) if args.format == "json" else json.dumps(rep, sort_keys=True))
     return EXIT_OK
 
@@ -315,6 +327,9 @@ def build_parser() -> argparse.ArgumentParser:
         if name == "run":
             s.add_argument("--input", help="JSON tensor file with arrays and symbols")
             s.add_argument("--journal", help="transformation journal to replay first")
+            s.add_argument("--report", choices=("static", "device"), default="static",
+                           help="ExecutionReport: static volumes (dynamic edges listed), or every edge "
+                                "counted on the device by the generic lowering's counter build")
         else:
             s.add_argument("--out", required=True)
             s.add_argument("--compile", action="store_true")

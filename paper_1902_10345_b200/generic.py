@@ -29,7 +29,7 @@ from .graph import Graph, load
 from .lower import Lowered, lower
 
 GEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_gen")
-_LOCK = threading.Lock()
+VISIT_LOG = 1 << 20  # state visits logged by report builds
 _STATUS = {1: (OutOfBoundsError, "subscript write out of bounds"),
            2: (ExecutionError, "subscript read out of bounds"),
            3: (ExecutionError, "stream overflow"),
@@ -55,18 +55,21 @@ def build(lowered: Lowered) -> str:
     key = hashlib.sha256((lowered.source + " ".join(flags)).encode()).hexdigest()[:16]
     base = os.path.join(GEN_DIR, f"{lowered.name}_{key}")
     so = base + ".so"
-    with _LOCK:
-        if os.path.exists(so):
-            return so
-        cu = base + ".cu"
-        with open(cu, "w") as f:
-            f.write(lowered.source)
-        tmp = f"{so}.{os.getpid()}.tmp"
-        cmd = [nvcc()] + flags + ["-o", tmp, cu, "-lcudart"]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise ToolchainError(f"nvcc failed for '{lowered.name}':\n{r.stderr}")
-        os.replace(tmp, so)
+    if os.path.exists(so):
+        return so
+    # no lock around nvcc: concurrent builders of one key each compile to a
+    # private temporary and the atomic rename makes the last one win
+    tag = f"{os.getpid()}.{threading.get_ident()}"
+    cu = f"{base}.{tag}.cu"
+    with open(cu, "w") as f:
+        f.write(lowered.source)
+    tmp = f"{so}.{tag}.tmp"
+    cmd = [nvcc()] + flags + ["-o", tmp, cu, "-lcudart"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise ToolchainError(f"nvcc failed for '{lowered.name}':\n{r.stderr}")
+    os.replace(cu, base + ".cu")
+    os.replace(tmp, so)
     return so
 
 
@@ -81,6 +84,12 @@ class GenericProgram:
         self._fn = getattr(self._lib, lowered.entry)
         self._fn.restype = ctypes.c_int
         self._fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
+        if lowered.report_keys is not None:  # counters + state-visit log
+            self._fn.argtypes += [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+
+    @property
+    def reports(self) -> bool:
+        return self.lowered.report_keys is not None
 
     @property
     def pointer_args(self):
@@ -91,6 +100,33 @@ class GenericProgram:
         return self.lowered.symbol_args
 
     def run(self, arrays: Mapping[str, Any], symbols: Mapping[str, int]) -> dict:
+        return self._run(arrays, symbols)[0]
+
+    def run_report(self, arrays: Mapping[str, Any], symbols: Mapping[str, int]) -> tuple:
+        """``run`` plus the interpreter's ExecutionReport fields
+        (interpreter.py:107-132) measured on the device: states_visited,
+        elements_moved per memlet edge, total_moved, tasklet_invocations.
+        Needs a report build (``compile_generic(g, report=True)``)."""
+        if not self.reports:
+            raise ExecutionError("this program was compiled without report counters")
+        return self._run(arrays, symbols)
+
+    def _report(self, counts, vis, nv: int) -> dict:
+        keys = self.lowered.report_keys
+        states = [self.lowered.state_names[i] for i in vis[:min(nv, len(vis))]]
+        visited = set(states)
+        moved = {}
+        for k, c in zip(keys, counts):
+            if k == "__tasklets":
+                continue
+            st = k.rsplit(":e", 1)[0]
+            if c or ("/" not in st and st in visited):
+                moved[k] = int(c)
+        return {"states_visited": states, "elements_moved": dict(sorted(moved.items())),
+                "total_moved": sum(moved.values()),
+                "tasklet_invocations": int(counts[keys.index("__tasklets")])}
+
+    def _run(self, arrays: Mapping[str, Any], symbols: Mapping[str, int]) -> tuple:
         import torch
         if not torch.cuda.is_available():
             raise ExecutionError("the generic B200 path needs a CUDA device")
@@ -118,8 +154,15 @@ class GenericProgram:
         svals = (ctypes.c_int64 * max(1, len(self.symbol_args)))(*[syms[s] for s in self.symbol_args])
         status = ctypes.c_int(0)
         stream = torch.cuda.current_stream().cuda_stream
+        extra = []
+        if self.reports:
+            counts = np.zeros(len(self.lowered.report_keys), np.uint64)
+            vis = np.zeros(VISIT_LOG, np.int64)
+            nv = np.zeros(1, np.int64)
+            extra = [counts.ctypes.data_as(ctypes.c_void_p), vis.ctypes.data_as(ctypes.c_void_p),
+                     ctypes.c_int64(VISIT_LOG), nv.ctypes.data_as(ctypes.c_void_p)]
         rc = self._fn(ctypes.cast(ptrs, ctypes.c_void_p), ctypes.cast(svals, ctypes.c_void_p),
-                      ctypes.c_void_p(stream), ctypes.byref(status))
+                      ctypes.c_void_p(stream), ctypes.byref(status), *extra)
         if rc != 0:
             raise ExecutionError(f"generic program '{g.name}' failed on the device (cuda status {-status.value})")
         if status.value:
@@ -128,7 +171,7 @@ class GenericProgram:
         for (name, _), t in zip(self.pointer_args, dev):
             if bufs[name].size:
                 bufs[name].reshape(-1)[:] = t.cpu().numpy()
-        return bufs
+        return bufs, (self._report(counts, vis, int(nv[0])) if self.reports else None)
 
 
     def run_device(self, tensors: list, symbols: Mapping[str, int], stream=None) -> None:
@@ -142,6 +185,8 @@ class GenericProgram:
             want = torch.float64 if bt == "float64" else torch.int64
             if t.dtype != want or not t.is_cuda or not t.is_contiguous():
                 raise ExecutionError(f"container '{name}' must be a contiguous CUDA {want} tensor")
+        if self.reports:
+            raise ExecutionError("run_device takes the timed build (compile_generic without report)")
         ptrs = (ctypes.c_void_p * max(1, len(tensors)))(*[t.data_ptr() for t in tensors])
         svals = (ctypes.c_int64 * max(1, len(self.symbol_args)))(*[syms[s] for s in self.symbol_args])
         status = ctypes.c_int(0)
@@ -156,9 +201,9 @@ class GenericProgram:
             raise exc(f"{msg} in '{self.graph.name}'")
 
 
-def compile_generic(sdfg: Any) -> GenericProgram:
+def compile_generic(sdfg: Any, report: bool = False) -> GenericProgram:
     """Lower + nvcc + load.  CodegenError for constructs the lowering does
-    not cover (consume scopes, custom WCR, vector memlets)."""
+    not cover.  ``report=True`` builds the ExecutionReport variant."""
     g = load(sdfg)
-    lw = lower(g)
+    lw = lower(g, report=report)
     return GenericProgram(g, lw, build(lw))

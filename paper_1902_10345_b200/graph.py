@@ -242,4 +242,6 @@ def to_doc(obj: Any) -> dict:
 
 
 def load(obj: Any) -> Graph:
+    if isinstance(obj, Graph):
+        return obj
     return from_json(to_doc(obj))

@@ -193,6 +193,9 @@ __global__ void gen_drain(const T* __restrict__ buf, const unsigned long long* _
         dst[i] = buf[i];
 }
 
+// ExecutionReport builds: add a device-resident count (a stream's items) to a slot
+__global__ void gen_rep_addp(unsigned long long* slot, const unsigned long long* v) { *slot += *v; }
+
 static int gen_blocks(int64_t total) {
     int64_t b = (total + 255) / 256;
     if (b < 1) b = 1;
@@ -310,6 +313,7 @@ class TaskletC:
         self.outputs = outputs
         self.dynamic = dynamic        # outputs needing a __set flag
         self.locals: dict[str, str] = {}
+        self.wcount: dict[str, str] = {}  # connector -> C counter of its subscript writes (report builds)
         self._infer(body)
 
     def type_of(self, n: ast.expr) -> str:
@@ -431,6 +435,8 @@ class TaskletC:
                 idx = self.ex(tgt.slice)
                 fn = "g_wr" if wcr is None else f"g_wr_{'p' if private else ''}{wcr}"
                 out.append(f"{ind}{fn}({ptr}, (int64_t)({idx}), {size}, ({CT[self.types[name]]})({val}), g_err);")
+                if name in self.wcount:
+                    out.append(f"{ind}++{self.wcount[name]};")
             return
         if isinstance(s, ast.If):
             out.append(f"{ind}if ({self.ex(s.test)}) {{")
@@ -490,13 +496,23 @@ class Lowered:
     symbol_args: list
     digest: str = ""
     notes: list = field(default_factory=list)
+    # ExecutionReport builds (lower(g, report=True)): counter slot -> key
+    # ("<state>:e<id>", nested "<graph>/<state>:e<id>", "__tasklets"), and
+    # the state index order of the visit log
+    report_keys: Optional[list] = None
+    state_names: Optional[list] = None
 
 
 class Lowering:
-    def __init__(self, g: Graph, fn_prefix: str = "gen", nested: bool = False):
+    def __init__(self, g: Graph, fn_prefix: str = "gen", nested: bool = False, report: Optional[dict] = None,
+                 keyprefix: str = ""):
         self.g = g
         self.prefix = fn_prefix
         self.nested = nested
+        # ExecutionReport build: {"slots": {key: index}} shared with nested
+        # lowerings; None for the normal (timed) build, which has no counters
+        self.rep = report
+        self.keyprefix = keyprefix
         assigned = {a for t in g.transitions for a, _ in t.assignments}
         self.sym_names = list(g.symbols) + sorted(assigned - set(g.symbols))
         self.kernels: list[str] = []
@@ -593,6 +609,8 @@ class Lowering:
                 ps.append(f"{CT[d.basetype]}* {self.cname(name)}")
         ps += [f"int64_t s_{_ident(s)}" for s in self.sym_names]
         ps.append("int* g_err")
+        if self.rep is not None:
+            ps.append("unsigned long long* g_rep")
         return ", ".join(ps)
 
     def kargs(self) -> str:
@@ -608,7 +626,138 @@ class Lowering:
                 a.append(self.cname(name))
         a += [f"s_{_ident(s)}" for s in self.sym_names]
         a.append("g_err")
+        if self.rep is not None:
+            a.append("g_rep")
         return ", ".join(a)
+
+    # -- ExecutionReport counters (interpreter.py:369-382, 514-545) -----------
+    # Every memlet edge counts what the interpreter's _produce counts: the
+    # memlet's `accesses` when it has one, else the actual elements -- the
+    # block a scope instance or access node reads, one per scalar a tasklet
+    # assigns (zero when a dynamic output stays unassigned), one per subscript
+    # write, the items a stream drain moves -- and an exit edge sums what
+    # crosses it.  Scope-level counts are atomics on the device; counts of
+    # top-level nodes are host additions once per state visit.
+
+    def slot(self, key: str) -> int:
+        slots = self.rep["slots"]
+        return slots.setdefault(key, len(slots))
+
+    def ekey(self, st: State, e) -> str:
+        return f"{self.keyprefix}{st.name}:e{e.id}"
+
+    def dcount(self, key: str, expr: str, ind: str, out: list) -> None:
+        if self.rep is None:
+            return
+        k = self.slot(key)
+        if expr != "0":
+            out.append(f"{ind}atomicAdd(&g_rep[{k}], (unsigned long long)({expr}));")
+
+    def hcount(self, key: str, expr: str, out: list) -> None:
+        if self.rep is None:
+            return
+        k = self.slot(key)
+        if expr != "0":
+            out.append(f"    g_reph[{k}] += (unsigned long long)({expr});")
+
+    def vol(self, subset, env: Env) -> str:
+        if not subset:
+            return "1LL"
+        return "(" + " * ".join(f"g_rlen({env.emit(r.begin)}, {env.emit(r.end)}, {env.emit(r.stride)}) * "
+                                f"({env.emit(r.tile)})" for r in subset) + ")"
+
+    def exit_chain(self, st: State, e) -> list:
+        """Edges a value committed on ``e`` crosses after it: scope exits
+        (the interpreter's _boundary_actual) and local-stream forwards."""
+        dst = st.nodes[e.dst]
+        out = []
+        if dst.kind == "access":
+            d = self.g.data.get(dst.data)
+            if d is not None and d.kind == "stream" and d.transient:
+                for o in st.out_edges(dst.id):
+                    if st.nodes[o.dst].kind in ("map_exit", "consume_exit") and o.dst_conn:
+                        out.append(o)
+                        out += self.exit_chain(st, o)
+            return out
+        if dst.kind in ("map_exit", "consume_exit") and e.dst_conn:
+            conn = "OUT_" + e.dst_conn[3:]
+            for nxt in st.out_edges(dst.id):
+                if nxt.src_conn == conn:
+                    out.append(nxt)
+                    out += self.exit_chain(st, nxt)
+        return out
+
+    def chain_counts(self, st: State, e, actual: str, ind: str, out: list) -> None:
+        for c in self.exit_chain(st, e):
+            if c.memlet.accesses is None and not c.memlet.is_empty:
+                self.dcount(self.ekey(st, c), actual, ind, out)
+
+    def instance_counts(self, st: State, n, env: Env, ind: str, out: list) -> None:
+        """One scope instance: the block every entry edge reads (:514-536)."""
+        if self.rep is None:
+            return
+        for e in st.out_edges(n.id):
+            m = e.memlet
+            if m.is_empty:
+                v = "0"
+            elif n.kind == "consume_entry" and e.src_conn == "OUT_stream":
+                v = "1"
+            elif self.g.data[m.data].kind == "stream":
+                v = "0"
+            else:
+                v = self.vol(m.subset, env)
+            self.dcount(self.ekey(st, e), v, ind, out)
+
+    def access_counts(self, st: State, n, env: Env, ind: str, out: list, host: bool) -> None:
+        """An access node firing (_fire_access / _fire_stream_access)."""
+        if self.rep is None:
+            return
+        stream = self.g.data[n.data].kind == "stream"
+        for e in st.out_edges(n.id):
+            m = e.memlet
+            key = self.ekey(st, e)
+            dkind = st.nodes[e.dst].kind
+            if m.is_empty:
+                v = "0"
+            elif m.accesses is not None:
+                v = env.emit(m.accesses)
+            elif stream:
+                # drains count their items where they run (top_access / the
+                # forwarded pushes); handles into a scope move nothing
+                v = "0"
+            else:
+                v = self.vol(m.subset, env)
+                if dkind in ("map_exit", "consume_exit") and not host:
+                    self.chain_counts(st, e, v, ind, out)
+            if host:
+                self.hcount(key, v, out)
+            else:
+                self.dcount(key, v, ind, out)
+
+    def exit_of(self, st: State, entry_id: int):
+        for x in st.nodes:
+            if x.kind in ("map_exit", "consume_exit") and x.doc.get("entry") == entry_id:
+                return x
+        return None
+
+    def finish_counts(self, st: State, entry_id: int, env: Env, ind: str, out: list, host: bool) -> None:
+        """A scope finishing (_finish_scope): exit edges with `accesses`
+        count it once; the others summed their commits already."""
+        if self.rep is None:
+            return
+        x = self.exit_of(st, entry_id)
+        if x is None:
+            return
+        for o in st.out_edges(x.id):
+            m = o.memlet
+            if m.is_empty or m.accesses is None:
+                v = "0"
+            else:
+                v = env.emit(m.accesses)
+            if host:
+                self.hcount(self.ekey(st, o), v, out)
+            else:
+                self.dcount(self.ekey(st, o), v, ind, out)
 
     # -- custom write-conflict resolution --------------------------------------
 
@@ -706,6 +855,7 @@ class Lowering:
         return env.child(more)
 
     def emit_inner_map(self, st: State, parent: dict, n, env: Env, ind: str, out: list) -> None:
+        outer = env
         env = self.dyn_range_locals(st, n, env, ind, out)
         more = {}
         depth = 0
@@ -717,13 +867,16 @@ class Lowering:
                        f"{v} += {s}) {{")
             more[p] = v
             depth += 1
+        self.instance_counts(st, n, env.child(more), ind + "    " * depth, out)
         self.emit_scope(st, parent, n.id, env.child(more), ind + "    " * depth, out, True)
         for d in reversed(range(depth)):
             out.append(f"{ind}{'    ' * d}}}")
+        self.finish_counts(st, n.id, outer, ind, out, host=False)
 
     def emit_access_device(self, st: State, n, env: Env, ind: str, out: list) -> None:
         """Region copies into an access node inside a scope (LocalStorage
         copies, nested-graph scalar moves): element loops per thread."""
+        self.access_counts(st, n, env, ind, out, host=False)
         for e in sorted(st.in_edges(n.id), key=lambda e: e.id):
             src = st.nodes[e.src]
             if e.memlet.is_empty or src.kind in ("tasklet", "map_exit", "nested"):
@@ -788,6 +941,15 @@ class Lowering:
                     raise LoweringError(f"tasklet '{n.name}': mixed vector widths {width} and {w}")
                 width = w
         lane = f"lv{t}"
+        if self.rep is not None:
+            # per firing: the invocation, and every output edge with `accesses`
+            self.dcount("__tasklets", "1", ind, out)
+            for e in st.out_edges(n.id):
+                m = e.memlet
+                if m.is_empty:
+                    self.dcount(self.ekey(st, e), "0", ind, out)
+                elif m.accesses is not None:
+                    self.dcount(self.ekey(st, e), env.emit(m.accesses), ind, out)
 
         def point(sub):
             pt = [env.emit(r.begin) for r in sub]
@@ -826,6 +988,7 @@ class Lowering:
                            f"(gen_fail(g_err, 6), ({CT[d.basetype]})0);")
             names[c] = v
         commits = []
+        wcounts = []  # (edge, C count of subscript writes) for the report
         for e in st.out_edges(n.id):
             if e.memlet.is_empty or e.src_conn is None:
                 continue
@@ -842,6 +1005,9 @@ class Lowering:
                 priv = tg[0].data in self.private
                 out.append(f"{ind2}{CT[td.basetype]}* {v} = {self.cname(tg[0].data)};")
                 awrite[c] = (v, self.size_expr(tg[0].data, env), fn, priv)
+                if self.rep is not None:
+                    out.append(f"{ind2}int64_t {v}__nw = 0;")
+                    wcounts.append((e, f"{v}__nw"))
                 continue
             out.append(f"{ind2}{CT[td.basetype]} {v} = 0;")
             if m.is_dynamic:
@@ -857,7 +1023,21 @@ class Lowering:
             if c not in names:
                 raise LoweringError(f"tasklet '{n.name}': input '{c}' has no memlet")
         tc = TaskletC(code.body, types, names, aread, awrite, set(prog_outs), dynamic)
+        tc.wcount = {e.src_conn: cv for e, cv in wcounts}
         out.extend(tc.emit(ind2))
+        if self.rep is not None:
+            # actual elements per lane: one per assigned scalar, one per
+            # subscript write; the same amount crosses every exit behind it
+            for c, v, m, tg in commits:
+                e = next(x for x in st.out_edges(n.id) if x.src_conn == c and x.memlet is m)
+                act = f"{v}__set" if m.is_dynamic else "1"
+                if m.accesses is None:
+                    self.dcount(self.ekey(st, e), act, ind2, out)
+                self.chain_counts(st, e, act, ind2, out)
+            for e, cv in wcounts:
+                if e.memlet.accesses is None:
+                    self.dcount(self.ekey(st, e), cv, ind2, out)
+                self.chain_counts(st, e, cv, ind2, out)
         for c, v, m, tg in commits:
             for target in tg:
                 td = self.g.data[target.data]
@@ -890,7 +1070,7 @@ class Lowering:
     def emit_nested_call(self, st: State, n, env: Env, ind: str, out: list) -> None:
         inner = from_json(n.doc["sdfg"])
         fn = f"{self.prefix}_nested{len(self.devfns)}_{_ident(inner.name)}"
-        sub = Lowering(inner, fn, nested=True)
+        sub = Lowering(inner, fn, nested=True, report=self.rep, keyprefix=f"{self.keyprefix}{inner.name}/")
         self.devfns.append(sub.device_function(fn))
         self.devfns[0:0] = sub.devfns  # deeper nests first
         bound = {}
@@ -914,7 +1094,12 @@ class Lowering:
                 raise LoweringError(f"nested symbol '{s}' is not mapped")
             args.append(env.emit(X.parse_expr(mapping[s])))
         args.append("g_err")
+        if self.rep is not None:
+            args.append("g_rep")
         out.append(f"{ind}{fn}({', '.join(args)});")
+        for e in st.out_edges(n.id):  # _fire_nested: accesses or nothing
+            m = e.memlet
+            self.dcount(self.ekey(st, e), "0" if m.is_empty or m.accesses is None else env.emit(m.accesses), ind, out)
 
     def device_function(self, fn: str) -> str:
         """The nested graph as a __device__ function: private transients,
@@ -924,6 +1109,8 @@ class Lowering:
                   if not d.transient and d.kind == "array"]
         params += [f"int64_t s_{_ident(s)}" for s in g.symbols]
         params.append("int* g_err")
+        if self.rep is not None:
+            params.append("unsigned long long* g_rep")
         body = []
         for name, d in g.data.items():
             if d.kind == "stream":
@@ -995,6 +1182,7 @@ class Lowering:
                 body.append(f"        rem /= n{k};")
             more[n.params[k]] = v
         penv = denv.child(more)
+        self.instance_counts(st, n, penv, "        ", body)
         # private transients: fresh, zeroed per iteration
         for name in sorted(self.private):
             if self._owned_by(name, st, parent, n.id):
@@ -1005,6 +1193,7 @@ class Lowering:
         body += inner
         body.append("    }")
         k = self.new_kernel(body, f"{st.name}_map{n.id}")
+        self.finish_counts(st, n.id, host_env, "    ", out, host=True)
         if dynamic:
             out.append(f"    {k}<<<148, 256, 0, st>>>({self.kargs()}); GEN_CHECK();")
             return
@@ -1054,11 +1243,14 @@ class Lowering:
                 f"        const {bt} elem = {self.cname(S)}[h];"]
         penv = denv.child({n.doc["param"]: f"(wid % g_imax(1LL, {denv.emit(X.parse_expr(n.doc['num_pes']))}))"})
         inner: list = []
+        self.dcount(self.ekey(st, se), "1", "        ", inner)  # popped (interpreter.py:595)
+        self.instance_counts(st, n, penv, "        ", inner)
         self.emit_scope(st, parent, n.id, penv, "        ", inner, True)
         body += inner
         body += ["        __threadfence();", f"        atomicAdd(&q_{s}[1], 1ull);", "    }"]
         del self.pop_vars[S]
         k = self.new_kernel(body, f"{st.name}_consume{n.id}")
+        self.finish_counts(st, n.id, Env(self, {}, host=True), "    ", out, host=True)
         out.append(f"    {k}<<<148 * 4, 128, 0, st>>>({self.kargs()}); GEN_CHECK();")
         out.append(f"    gen_queue_reset<<<gen_blocks(cap_{s}), 256, 0, st>>>(r_{s}, n_{s}, q_{s}, cap_{s}); "
                    f"GEN_CHECK();")
@@ -1100,6 +1292,9 @@ class Lowering:
                 s = _ident(sdata)
                 out.append(f"    gen_drain<<<gen_blocks(cap_{s}), 256, 0, st>>>({self.cname(sdata)}, n_{s}, "
                            f"{self.cname(n.data)}, {self.size_expr(n.data, host_env)}, g_err); GEN_CHECK();")
+                if self.rep is not None and m.accesses is None:  # the items drained
+                    out.append(f"    gen_rep_addp<<<1, 1, 0, st>>>(g_rep + {self.slot(self.ekey(st, e))}, n_{s}); "
+                               f"GEN_CHECK();")
                 out.append(f"    cudaMemsetAsync(n_{s}, 0, 8, st); ub_{s} = 0;")
                 continue
             if d.kind == "stream":
@@ -1180,6 +1375,12 @@ class Lowering:
         htl = " * ".join(f"g_rlen({host_env.emit(r.begin)}, {host_env.emit(r.end)}, 1)" for r in tsub)
         hil = " * ".join(f"g_rlen({host_env.emit(r.begin)}, {host_env.emit(r.end)}, 1)" for r in isub)
         out.append(f"    {k1}<<<gen_blocks({htl}), 256, 0, st>>>({self.kargs()}); GEN_CHECK();")
+        if self.rep is not None:  # _fire_reduce produces the reduced block
+            kl = [f"g_rlen({host_env.emit(r.begin)}, {host_env.emit(r.end)}, {host_env.emit(r.stride)})"
+                  for k, r in enumerate(isub) if k not in axes]
+            m = oute.memlet
+            v = host_env.emit(m.accesses) if m.accesses is not None else ("(" + " * ".join(kl) + ")" if kl else "1LL")
+            self.hcount(self.ekey(st, oute), v, out)
         out.append(f"    {k2}<<<gen_blocks({hil}), 256, 0, st>>>({self.kargs()}); GEN_CHECK();")
 
     def stream_pushes(self, st: State, parent: dict, host_env: Env) -> dict:
@@ -1214,8 +1415,10 @@ class Lowering:
         g = self.g
         henv = Env(self, {}, host=True)
         ptr_args = g.pointer_args()
+        rsig = (", unsigned long long* g_reph, int64_t* g_vis, int64_t g_vcap, int64_t* g_nvis"
+                if self.rep is not None else "")
         lines = ["extern \"C\" int " + self.prefix + "_run(void** ptrs, const int64_t* syms, void* stream_, "
-                 "int* status) {",
+                 "int* status" + rsig + ") {",
                  "    cudaStream_t st = (cudaStream_t)stream_;",
                  "    gen_pool_keep();",
                  "    cudaError_t gen_ce = cudaSuccess;",
@@ -1227,6 +1430,8 @@ class Lowering:
         for s in self.sym_names[len(g.symbols):]:
             lines.append(f"    int64_t s_{_ident(s)} = 0;")
         lines.append("    int* g_err = nullptr;")
+        if self.rep is not None:
+            lines += ["    unsigned long long* g_rep = nullptr;", "    int64_t g_nv = 0;"]
         trans = [(n, d) for n, d in g.data.items() if d.transient and d.kind == "array" and n not in self.private]
         streams = [(n, d) for n, d in g.data.items() if d.kind == "stream"]
         for name, d in trans:
@@ -1242,6 +1447,9 @@ class Lowering:
                 lines += [f"    unsigned* r_{s} = nullptr;", f"    unsigned long long* q_{s} = nullptr;"]
         lines.append("    if (cudaMallocAsync((void**)&g_err, 16, st) != cudaSuccess) return 2;")
         lines.append("    cudaMemsetAsync(g_err, 0, 16, st);")
+        if self.rep is not None:
+            lines.append("    if (cudaMallocAsync((void**)&g_rep, @NREP@ * 8, st) != cudaSuccess) goto gen_fail;")
+            lines.append("    cudaMemsetAsync(g_rep, 0, @NREP@ * 8, st);")
         for name, d in trans:
             lines.append(f"    {{ const size_t nb = (size_t)({self.size_expr(name, henv)}) * sizeof({CT[d.basetype]});")
             lines.append(f"      if (cudaMallocAsync((void**)&{self.cname(name)}, nb ? nb : 8, st) != cudaSuccess) "
@@ -1262,6 +1470,8 @@ class Lowering:
             parent = st.scope_parent()
             lines.append(f"st_{_ident(st.name)}:;")
             lines.append("    {")
+            if self.rep is not None:
+                lines.append(f"    if (g_nv < g_vcap) g_vis[g_nv] = {g.states.index(st)}; ++g_nv;")
             for sname, trips in self.stream_pushes(st, parent, henv).items():
                 if sname in self.consumed:
                     continue  # fixed-capacity work queue
@@ -1287,6 +1497,7 @@ class Lowering:
                     self.top_single(st, parent, n, lines, "nested")
                 elif n.kind == "access":
                     self.top_access(st, n, henv, lines)
+                    self.access_counts(st, n, henv, "    ", lines, host=True)
                 elif n.kind == "reduce":
                     self.top_reduce(st, n, henv, lines)
                 elif n.kind == "consume_entry":
@@ -1304,6 +1515,12 @@ class Lowering:
         lines.append("    }")
         lines.append("    gen_ce = cudaStreamSynchronize(st);")
         lines.append("    if (gen_ce != cudaSuccess) goto gen_fail;")
+        if self.rep is not None:
+            lines += ["    {", "    unsigned long long dv[@NREP@];",
+                      "    gen_ce = cudaMemcpy(dv, g_rep, sizeof(dv), cudaMemcpyDeviceToHost);",
+                      "    if (gen_ce != cudaSuccess) goto gen_fail;",
+                      "    for (int i = 0; i < @NREP@; ++i) g_reph[i] += dv[i];",
+                      "    *g_nvis = g_nv;", "    }", "    cudaFreeAsync(g_rep, st);"]
         free = [f"    if ({self.cname(n)}) cudaFreeAsync({self.cname(n)}, st);" for n, _ in trans]
         for name, _ in streams:
             free += [f"    if ({self.cname(name)}) cudaFreeAsync({self.cname(name)}, st);",
@@ -1317,16 +1534,24 @@ class Lowering:
         lines.append("gen_fail:")
         lines += free
         lines.append("    if (g_err) cudaFreeAsync(g_err, st);")
+        if self.rep is not None:
+            lines.append("    if (g_rep) cudaFreeAsync(g_rep, st);")
         lines.append("    cudaStreamSynchronize(st);")
         lines.append("    *status = -(int)gen_ce;")
         lines.append("    return 2;")
         lines.append("#undef GEN_CHECK")
         lines.append("}")
+        keys = None
+        if self.rep is not None:
+            self.slot("__tasklets")
+            keys = sorted(self.rep["slots"], key=self.rep["slots"].get)
+            lines = [ln.replace("@NREP@", str(len(keys))) for ln in lines]
         host = "\n".join(lines)
         src = "\n".join([f"// generated by paper_1902_10345_b200.lower for SDFG '{g.name}'", PRELUDE,
                          SUBSCRIPT_HELPERS] + self.devfns + self.kernels + [host]) + "\n"
         digest = hashlib.sha256(src.encode()).hexdigest()[:16]
-        return Lowered(g.name, src, f"{self.prefix}_run", ptr_args, list(g.symbols), digest)
+        return Lowered(g.name, src, f"{self.prefix}_run", ptr_args, list(g.symbols), digest,
+                       report_keys=keys, state_names=[x.name for x in g.states] if keys is not None else None)
 
 
 def _is_one(e) -> bool:
@@ -1345,5 +1570,7 @@ def _subscripts(code: ast.Module):
     return reads, writes
 
 
-def lower(g: Graph) -> Lowered:
-    return Lowering(g, "gen_" + _ident(g.name)).program()
+def lower(g: Graph, report: bool = False) -> Lowered:
+    """``report=True``: the ExecutionReport build -- the same program with
+    per-edge element counters and a state-visit log (slower: atomics)."""
+    return Lowering(g, "gen_" + _ident(g.name), report={"slots": {}} if report else None).program()

@@ -91,3 +91,70 @@ def test_execution_report_matches_the_interpreter_on_static_edges():
             tl += 1
         cases += 1
     assert cases > 40 and edges > 400 and tl > 20, (cases, edges, tl)
+
+
+def _report_cases():
+    from paper_1902_10345_b200.lower import LoweringError, lower
+    seen = {}
+    for c in load_cases():
+        if c.moved is None or c.error:
+            continue
+        if c.motif not in seen:
+            try:
+                lower(load(graph_path(c.motif)), report=True)
+                seen[c.motif] = True
+            except LoweringError:
+                seen[c.motif] = False
+        if seen[c.motif]:
+            yield c
+
+
+def test_report_build_has_a_counter_for_every_counted_edge():
+    """the counter build covers every edge key the interpreter reports"""
+    from paper_1902_10345_b200.lower import lower
+    n = 0
+    for c in _report_cases():
+        keys = set(lower(load(graph_path(c.motif)), report=True).report_keys)
+        missing = [k for k, v in c.moved.items() if v and k not in keys]
+        assert not missing, f"{c}: {missing}"
+        n += 1
+    assert n > 50
+
+
+@pytest.mark.gpu
+def test_device_report_matches_the_interpreter(cuda_ok):
+    """ExecutionReport measured on the device (lower(report=True)) ==
+    the reference interpreter's, edge by edge, on every golden case --
+    including the dynamic edges the static report cannot count (stream
+    pushes, data-dependent ranges, consume scopes, nested graphs)"""
+    from paper_1902_10345_b200.generic import compile_generic
+    progs, n, dyn = {}, 0, 0
+    for c in _report_cases():
+        if c.motif not in progs:
+            progs[c.motif] = compile_generic(load(graph_path(c.motif)), report=True)
+        _, rep = progs[c.motif].run_report(c.inputs, c.symbols)
+        if c.states is not None:
+            assert rep["states_visited"] == c.states, repr(c)
+        keys = set(rep["elements_moved"]) | set(c.moved)
+        bad = {k: (rep["elements_moved"].get(k, 0), c.moved.get(k, 0)) for k in keys
+               if rep["elements_moved"].get(k, 0) != c.moved.get(k, 0)}
+        assert not bad, f"{c}: (device, interpreter) {bad}"
+        assert rep["total_moved"] == sum(c.moved.values()), repr(c)
+        assert rep["tasklet_invocations"] == c.tasklets, repr(c)
+        static = cli.execution_report(load(graph_path(c.motif)), c.symbols)
+        dyn += bool(static.get("dynamic_edges"))
+        n += 1
+    assert n > 60 and dyn > 20, (n, dyn)
+
+
+@pytest.mark.gpu
+def test_run_with_device_report(tmp_path, capsys, cuda_ok):
+    case = load_cases("spmv")[0]
+    inp = tmp_path / "in.json"
+    inp.write_text(json.dumps({"arrays": {k: v.tolist() for k, v in case.inputs.items()},
+                               "symbols": case.symbols}))
+    assert cli.main(["--format", "json", "run", graph_path("spmv"), "--input", str(inp), "--report", "device"]) == 0
+    rep = json.loads(capsys.readouterr().out)
+    assert rep["report"] == "device" and rep["elements_moved"] == {k: v for k, v in sorted(case.moved.items())
+                                                                   if k in rep["elements_moved"]}
+    assert rep["total_moved"] == sum(case.moved.values())
