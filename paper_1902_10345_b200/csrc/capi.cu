@@ -171,18 +171,36 @@ extern "C" int sdfgb_host_histogram(const double* img, int64_t* hist, int64_t H,
     SDFGB_TRY(ss.get(0, n, &dimg));
     SDFGB_TRY(ss.get(1, bins + 1, &dhist));
     doob = reinterpret_cast<uint64_t*>(dhist + bins);
-    cudaStream_t s = ss.s();
-    SDFGB_TRY(h2d(dimg, img, n, s));
+    cudaStream_t s = ss.s(), hs = ss.pool->h2d;
     SDFGB_TRY(h2d(dhist, hist, bins, s));
     SDFGB_CUDA(cudaMemsetAsync(doob, 0, 8, s));
-    if (precision == SDFGB_PREC_FP32) {
-        float* dimgf;
-        SDFGB_TRY(ss.get(2, n, &dimgf));
-        SDFGB_TRY(convert(dimg, dimgf, n, s));
-        SDFGB_TRY(sdfgb_hist_f32(dimgf, n, scale, div, dhist, bins, doob, s));
-    } else {
-        SDFGB_TRY(sdfgb_hist_f64(dimg, n, scale, div, dhist, bins, doob, s));
+    float* dimgf = nullptr;
+    if (precision == SDFGB_PREC_FP32) SDFGB_TRY(ss.get(2, n, &dimgf));
+    // pipelined: the image streams in on the copy stream while earlier
+    // chunks are binned (WCR sum: chunk launches accumulate into `hist`)
+    const int64_t chunk = std::max<int64_t>(std::min<int64_t>(n, (int64_t)1 << 21), 1);
+    const int64_t nch = (n + chunk - 1) / chunk;
+    std::vector<cudaEvent_t> ev(nch);
+    int rc = SDFGB_OK;
+    for (int64_t i = 0; i < nch; ++i)
+        if (rc == SDFGB_OK) rc = check_cuda(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event");
+    for (int64_t i = 0; i < nch && rc == SDFGB_OK; ++i) {
+        const int64_t off = i * chunk, len = std::min(chunk, n - off);
+        rc = h2d(dimg + off, img + off, len, hs);
+        if (rc == SDFGB_OK) rc = check_cuda(cudaEventRecord(ev[i], hs), "event");
+        if (rc == SDFGB_OK) rc = check_cuda(cudaStreamWaitEvent(s, ev[i], 0), "wait");
+        if (rc != SDFGB_OK) break;
+        if (precision == SDFGB_PREC_FP32) {
+            rc = convert(dimg + off, dimgf + off, len, s);
+            if (rc == SDFGB_OK) rc = sdfgb_hist_f32(dimgf + off, len, scale, div, dhist, bins, doob, s);
+        } else {
+            rc = sdfgb_hist_f64(dimg + off, len, scale, div, dhist, bins, doob, s);
+        }
     }
+    if (rc != SDFGB_OK) cudaStreamSynchronize(hs);
+    for (int64_t i = 0; i < nch; ++i)
+        if (ev[i]) cudaEventDestroy(ev[i]);
+    if (rc != SDFGB_OK) return rc;
     uint64_t oob = 0;
     SDFGB_TRY(d2h(&oob, doob, 1, s));
     SDFGB_CUDA(cudaStreamSynchronize(s));
@@ -412,24 +430,49 @@ extern "C" int sdfgb_host_matmul(const double* A, const double* B, double* C, in
     float* f;
     SDFGB_TRY(ss.get(1, M * Kp + Kp * N + M * N, &f));
     float *fA = f, *fB = f + M * Kp, *fC = fB + Kp * N;
-    SDFGB_TRY(h2d(dA, A, M * K, s));
-    SDFGB_TRY(h2d(dB, B, K * N, s));
-    if (Kp != K) {
-        // zero-padded K columns of A / rows of B contribute nothing
-        SDFGB_CUDA(cudaMemsetAsync(fA, 0, (size_t)(M * Kp + Kp * N) * 4, s));
-        SDFGB_TRY(convert_rows(dA, fA, M, K, Kp, s));
-    } else {
-        SDFGB_TRY(convert(dA, fA, M * K, s));
-    }
-    SDFGB_TRY(convert(dB, fB, K * N, s));
+    cudaStream_t hs = ss.pool->h2d, ds = ss.pool->d2h;
+    // Pipelined over row panels of A and C: B comes in first, then each A
+    // panel streams in while the previous panel multiplies and the one
+    // before ships C back (every C element sees the same k loop, so the
+    // panel split does not change results)
+    const int64_t prow = std::min<int64_t>(M, std::max<int64_t>(128, (M / 8 + 127) / 128 * 128));
+    const int64_t np = (M + prow - 1) / prow;
     void* ws;
-    const size_t wsb = sdfgb_gemm_workspace_bytes(M, N, Kp);
+    const size_t wsb = sdfgb_gemm_workspace_bytes(prow, N, Kp);
     uint8_t* w8;
     SDFGB_TRY(ss.get(2, (int64_t)wsb, &w8));
     ws = w8;
-    SDFGB_TRY(sdfgb_gemm_f32(fA, fB, fC, M, N, Kp, ws, wsb, s));
-    SDFGB_TRY(convert(fC, dC, M * N, s));
-    SDFGB_TRY(d2h(C, dC, M * N, s));
-    SDFGB_CUDA(cudaStreamSynchronize(s));
-    return SDFGB_OK;
+    std::vector<cudaEvent_t> ev(2 * np + 1);
+    int rc = SDFGB_OK;
+    for (auto& e : ev)
+        if (rc == SDFGB_OK) rc = check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    if (rc == SDFGB_OK) rc = check_cuda(cudaEventRecord(ev[2 * np], s), "event");  // after earlier work on s
+    if (rc == SDFGB_OK) rc = check_cuda(cudaStreamWaitEvent(hs, ev[2 * np], 0), "wait");
+    if (rc == SDFGB_OK) rc = h2d(dB, B, K * N, hs);
+    for (int64_t p = 0; p < np && rc == SDFGB_OK; ++p) {
+        const int64_t r0 = p * prow, rows = std::min(prow, M - r0);
+        rc = h2d(dA + r0 * K, A + r0 * K, rows * K, hs);
+        if (rc == SDFGB_OK) rc = check_cuda(cudaEventRecord(ev[p], hs), "event");
+        if (rc == SDFGB_OK) rc = check_cuda(cudaStreamWaitEvent(s, ev[p], 0), "wait");
+        if (rc != SDFGB_OK) break;
+        if (p == 0) {
+            // zero-padded K columns of A / rows of B contribute nothing
+            if (Kp != K) rc = check_cuda(cudaMemsetAsync(fA, 0, (size_t)(M * Kp + Kp * N) * 4, s), "memset");
+            if (rc == SDFGB_OK) rc = convert(dB, fB, K * N, s);
+        }
+        if (rc == SDFGB_OK && Kp != K) rc = convert_rows(dA + r0 * K, fA + r0 * Kp, rows, K, Kp, s);
+        if (rc == SDFGB_OK && Kp == K) rc = convert(dA + r0 * K, fA + r0 * K, rows * K, s);
+        if (rc == SDFGB_OK) rc = sdfgb_gemm_f32(fA + r0 * Kp, fB, fC + r0 * N, rows, N, Kp, ws, wsb, s);
+        if (rc == SDFGB_OK) rc = convert(fC + r0 * N, dC + r0 * N, rows * N, s);
+        if (rc == SDFGB_OK) rc = check_cuda(cudaEventRecord(ev[np + p], s), "event");
+        if (rc == SDFGB_OK) rc = check_cuda(cudaStreamWaitEvent(ds, ev[np + p], 0), "wait");
+        if (rc == SDFGB_OK) rc = d2h(C + r0 * N, dC + r0 * N, rows * N, ds);
+    }
+    const int sync_rc = check_cuda(cudaStreamSynchronize(ds), "D2H");
+    cudaStreamSynchronize(hs);
+    cudaStreamSynchronize(s);
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+    if (rc != SDFGB_OK) return rc;
+    return sync_rc;
 }

@@ -528,3 +528,43 @@ def test_full_gemm_rows_sampled(n):
     ref = oracle.matmul(a, bh)
     got = C[rows].cpu().numpy()
     assert (np.abs(got - ref) / np.abs(ref)).max() < 1e-4
+
+
+# ------------------------------------------------ pipelined host entries (C ABI)
+
+def _vp(a):
+    import ctypes
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def test_host_histogram_pipelined_chunks():
+    """more than one 2^21-element chunk, ragged tail, existing counts kept"""
+    from paper_1902_10345_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(11)
+    img = rng.random((2100, 1100))
+    hist = rng.integers(0, 5, 256).astype(np.int64)
+    ref, _ = oracle.histogram(img.astype(np.float32), hist.copy())
+    got = hist.copy()
+    _lib.check(L.sdfgb_host_histogram(_vp(img), _vp(got), 2100, 1100, 256, 256.0, 1.0, _lib.PREC_FP32))
+    np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("M,N,K", [(2000, 96, 37), (1500, 130, 64), (130, 70, 5)])
+def test_host_matmul_pipelined_panels(M, N, K):
+    """row panels of A/C streamed through the copy streams; K % 4 != 0 pads"""
+    from paper_1902_10345_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(M + K)
+    A = rng.random((M, K))
+    B = rng.random((K, N))
+    C = np.full((M, N), 3.0)
+    _lib.check(L.sdfgb_host_matmul(_vp(A), _vp(B), _vp(C), M, N, K))
+    ref = A.astype(np.float32).astype(np.float64) @ B.astype(np.float32).astype(np.float64)
+    assert np.abs(C - ref).max() / np.abs(ref).max() < 1e-5
+    C64 = np.zeros((M, N))
+    _lib.check(L.sdfgb_host_matmul_f64(_vp(A), _vp(B), _vp(C64), M, N, K))
+    seq = np.zeros((M, N))
+    for k in range(K):
+        seq = seq + A[:, k:k + 1] * B[k:k + 1, :]
+    np.testing.assert_array_equal(C64, seq)
