@@ -125,8 +125,15 @@ class Dist:
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if os.environ.get("SDFGB_BENCH_SHARE_GPU") == "1":
+                # plumbing check only (never a measurement): ranks share the
+                # visible GPUs and talk over gloo
+                self.local %= torch.cuda.device_count()
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("gloo")
+            else:
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.pg = dist
 
     def barrier(self):

@@ -233,9 +233,24 @@ def _ghost_exchange(pg, plane, slab: JacobiSlab, rank, world):
     if rank < world - 1 and bot:
         ops.append(pg.P2POp(pg.isend, plane[top + rows - bot:top + rows].contiguous(), rank + 1))
         ops.append(pg.P2POp(pg.irecv, plane[top + rows:top + rows + bot], rank + 1))
-    if ops:
-        for r in pg.batch_isend_irecv(ops):
+    if not ops:
+        return
+    if plane.is_cuda and pg.get_backend() == "gloo":
+        # gloo moves host memory only: stage the rows through the host
+        import torch
+        staged, back = [], []
+        for op in ops:
+            h = op.tensor.cpu() if op.op is pg.isend else torch.empty(op.tensor.shape, dtype=op.tensor.dtype)
+            if op.op is pg.irecv:
+                back.append((op.tensor, h))
+            staged.append(pg.P2POp(op.op, h, op.peer))
+        for r in pg.batch_isend_irecv(staged):
             r.wait()
+        for dev, h in back:
+            dev.copy_(h)
+        return
+    for r in pg.batch_isend_irecv(ops):
+        r.wait()
 
 
 # ---------------------------------------------------------------------- gemm
