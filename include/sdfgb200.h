@@ -50,6 +50,7 @@ extern "C" {
 #define SDFGB_ERR_CUDA 2        /* CUDA runtime / launch failure            */
 #define SDFGB_ERR_OOB 3         /* out-of-bounds WCR index (OutOfBoundsError) */
 #define SDFGB_ERR_WORKSPACE 4   /* workspace too small                       */
+#define SDFGB_ERR_COMM 5        /* NCCL missing or a collective failed        */
 
 /* comparison operators of a stream-push predicate (tasklets.py _CMPOPS) */
 #define SDFGB_CMP_LT 0
@@ -151,6 +152,49 @@ int sdfgb_gemm_f32_simt(const float* A, const float* B, float* C,
  * bit-identical to the reference's MapReduceFusion loop after init_C. */
 int sdfgb_gemm_f64(const double* A, const double* B, double* C,
                    int64_t M, int64_t N, int64_t K, void* stream);
+
+/* ------------------------------------------------- multi-GPU entries
+ * One process per GPU: each call is this rank's share of a motif plus the
+ * exchange step of SURVEY.md §8e, on the caller's NCCL communicator
+ * (ncclComm_t as void*) and stream.  Results are bit-identical to the
+ * one-GPU entries.  NCCL is loaded at run time (libnccl.so.2); without it
+ * these return SDFGB_ERR_COMM.  Python counterpart: multigpu.py.        */
+int sdfgb_nccl_available(void);
+int sdfgb_nccl_unique_id(void* id_out /* 128 bytes */);
+int sdfgb_nccl_comm_init(void** comm_out, int nranks, const void* id, int rank);
+int sdfgb_nccl_comm_destroy(void* comm);
+/* hist += counts of the union of all ranks' shards (every rank ends with the
+ * same hist and oob): local partial -> ncclAllReduce(sum) -> fold. */
+size_t sdfgb_hist_mgpu_workspace_bytes(int64_t bins);
+int sdfgb_hist_f32_mgpu(const float* img, int64_t n, double scale, double div,
+                        int64_t* hist, int64_t bins, uint64_t* oob,
+                        void* ws, size_t ws_bytes, void* comm, void* stream);
+/* Sharded query: this rank's survivors -> out_vals[0:k); counts[world]
+ * (device) receives every rank's k by ncclAllGather; count[0] += total and
+ * offset[0] = this rank's global output offset (survivors on lower ranks). */
+int sdfgb_query_f32_mgpu(const float* col, int64_t n, int op, double thr, float* out_vals,
+                         int64_t* count, int64_t* offset, int64_t* counts,
+                         void* ws, size_t ws_bytes, void* comm, void* stream);
+/* Row-block SpMV: ncclAllGather of the equal x shards (w_shard each) into
+ * x_full, then b[i] += ... over this rank's H_local rows (col holds global
+ * column ids). */
+int sdfgb_spmv_csr_f32_mgpu(const int32_t* rowptr, const int32_t* col, const float* val,
+                            const float* x_shard, int64_t w_shard, float* x_full, float* b,
+                            int64_t H_local, void* comm, void* stream);
+/* Jacobi on a row slab A[2, top + rows + bot, N] (N % 4 == 0): top / bot are
+ * 7 ghost rows towards each neighbour (0 at the global edge, whose plane edge
+ * is the true border).  One grouped ncclSend/ncclRecv of ghost rows per
+ * temporal block of up to 7 steps; canonical 5-point order. */
+int sdfgb_jacobi2d_f32_mgpu(float* A, int64_t top, int64_t rows, int64_t bot, int64_t N, int64_t T,
+                            double coef, void* comm, void* stream);
+/* P x Q grid GEMM: C block (i, j) = A row panel i x B column panel j.  A_piece
+ * (a_rows x K) is this rank's share of panel i, gathered over row_comm (size
+ * Q) into A_panel (a_rows*Q x K); B_piece (b_rows x nq) its share of panel j,
+ * gathered over col_comm (size P, b_rows*P == K) into B_panel (K x nq).
+ * ws: sdfgb_gemm_workspace_bytes(a_rows*Q, nq, K). */
+int sdfgb_gemm_f32_mgpu(const float* A_piece, int64_t a_rows, const float* B_piece, int64_t b_rows,
+                        int64_t K, int64_t nq, float* A_panel, float* B_panel, float* C_block,
+                        void* ws, size_t ws_bytes, void* row_comm, void* col_comm, void* stream);
 
 /* -------------------------------------------------------- host entries
  * Drop-in for CompiledSdfg._fn(*ptrs, *syms) (codegen.py:886): host

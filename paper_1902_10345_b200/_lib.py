@@ -42,6 +42,16 @@ SIGNATURES = {
     "sdfgb_query_f64": (_INT, [_P, _I64, _INT, _F64, _P, _P, _P, _SZ, _P]),
     "sdfgb_spmv_csr_f32": (_INT, [_P, _P, _P, _P, _P, _I64, _P]),
     "sdfgb_spmv_csr_f64": (_INT, [_P, _P, _P, _P, _P, _I64, _P]),
+    "sdfgb_nccl_available": (_INT, []),
+    "sdfgb_nccl_unique_id": (_INT, [_P]),
+    "sdfgb_nccl_comm_init": (_INT, [_P, _INT, _P, _INT]),
+    "sdfgb_nccl_comm_destroy": (_INT, [_P]),
+    "sdfgb_hist_mgpu_workspace_bytes": (_SZ, [_I64]),
+    "sdfgb_hist_f32_mgpu": (_INT, [_P, _I64, _F64, _F64, _P, _I64, _P, _P, _SZ, _P, _P]),
+    "sdfgb_query_f32_mgpu": (_INT, [_P, _I64, _INT, _F64, _P, _P, _P, _P, _P, _SZ, _P, _P]),
+    "sdfgb_spmv_csr_f32_mgpu": (_INT, [_P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P]),
+    "sdfgb_jacobi2d_f32_mgpu": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _F64, _P, _P]),
+    "sdfgb_gemm_f32_mgpu": (_INT, [_P, _I64, _P, _I64, _I64, _I64, _P, _P, _P, _P, _SZ, _P, _P, _P]),
     "sdfgb_jacobi2d_f32": (_INT, [_P, _I64, _I64, _F64, _P, _P, _INT, _P]),
     "sdfgb_jacobi2d_f64": (_INT, [_P, _I64, _I64, _F64, _P, _P, _INT, _P]),
     "sdfgb_jacobi2d_step_f32": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _I64, _F64, _P, _P, _INT, _P]),

@@ -12,7 +12,7 @@ if [ "$1" = "build" ]; then
   for spec in "$@"; do
     name=${spec%%:*}; defs=${spec#*:}
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr \
-      $defs -shared -o $OUT/lib_${name}.so capi.cu tma.cu hist.cu query.cu spmv.cu jacobi.cu gemm.cu -lcudart &
+      $defs -shared -o $OUT/lib_${name}.so capi.cu tma.cu hist.cu query.cu spmv.cu jacobi.cu gemm.cu mgpu.cu -lcudart -ldl &
   done; wait; ls $OUT; exit 0
 fi
 shift
