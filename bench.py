@@ -221,6 +221,31 @@ def pinned(shape, dtype):
 # Algorithmic bytes = compulsory footprint of the propagated memlet subsets
 # x element size.
 
+def _hist_peers(dist, hist, oob):
+    """Map every rank's hist/oob for the fused P2P histogram and prove the
+    mapping with one probe call; (None, reason) -> the NCCL all_reduce path."""
+    import torch
+    from paper_1902_10345_b200 import multigpu as MG
+    try:
+        peers = MG.PeerHist(dist.pg, hist, oob)
+        probe = torch.zeros(4096, dtype=torch.float32, device="cuda")  # every element -> bin 0
+        MG.histogram_p2p(dist.pg, probe, peers)
+        MG.finish_histogram_p2p(dist.pg)
+        ok = torch.tensor([int(hist[0].item() == 4096 * dist.world and hist.sum().item() == 4096 * dist.world)],
+                          device="cuda")
+        dist.pg.all_reduce(ok, op=dist.pg.ReduceOp.MIN)
+        dist.barrier()
+        hist.zero_()
+        oob.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if ok.item():
+            return peers, "p2p: sdfgb_hist_f32_p2p adds each rank's bins into every rank's hist over NVLink"
+        return None, "nccl all_reduce (p2p probe mismatch)"
+    except Exception as exc:  # no IPC / peer access: keep the collective path
+        return None, f"nccl all_reduce (p2p unavailable: {type(exc).__name__})"
+
+
 def bench_histogram(args, dist, P):
     import torch
     from paper_1902_10345_b200 import device, _lib
@@ -231,20 +256,30 @@ def bench_histogram(args, dist, P):
     hist = torch.zeros(256, dtype=torch.int64, device="cuda")
     oob = torch.zeros(1, dtype=torch.int64, device="cuda")
     multi = dist.pg is not None
+    exchange = None
     if multi:
         from paper_1902_10345_b200 import multigpu as MG
         be = MG.DeviceBackend()
+        peers, exchange = _hist_peers(dist, hist, oob)
 
     pending = []
 
     def step(k):
-        if multi:  # each rank bins its own image; partial bins -> all_reduce (NCCL), overlapped
+        if multi and peers is not None:
+            # fused: the kernel adds its bins into every rank's hist over NVLink
+            MG.histogram_p2p(dist.pg, imgs[k % nbuf], peers)
+        elif multi:  # each rank bins its own image; partial bins -> all_reduce (NCCL), overlapped
             MG.histogram(dist.pg, imgs[k % nbuf], hist, oob, be, pending=pending)
         else:
             device.hist(imgs[k % nbuf], hist, oob)
 
-    ms = time_steps(step, args.steps, args.warmup, dist, graph=not multi,
-                    finish=(lambda: MG.finish_histogram(pending, hist, oob)) if multi else None)
+    def finish():
+        if peers is not None:
+            MG.finish_histogram_p2p(dist.pg)
+        else:
+            MG.finish_histogram(pending, hist, oob)
+
+    ms = time_steps(step, args.steps, args.warmup, dist, graph=not multi, finish=finish if multi else None)
     assert oob.item() == 0
     by = 4 * H * W + 2 * 256 * 8
     out = {"value": dist.world * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms,
@@ -252,7 +287,7 @@ def bench_histogram(args, dist, P):
            "roofline": roof("hbm", by / ms / 1e6, P, "hist_smem_kernel"),
            "l2": f"{nbuf} rotating 64 MiB inputs (> 126 MB L2)",
            "config": {"workload": "Histogram 4096x4096 fp32, 256 bins (configs[0])", "H": H, "W": W,
-                      "bins": 256}}
+                      "bins": 256, **({"exchange": exchange} if exchange else {})}}
     if args.e2e:
         himg = pinned((H, W), torch.float64)
         himg.copy_(imgs[0].double().cpu())

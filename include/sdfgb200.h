@@ -169,6 +169,15 @@ size_t sdfgb_hist_mgpu_workspace_bytes(int64_t bins);
 int sdfgb_hist_f32_mgpu(const float* img, int64_t n, double scale, double div,
                         int64_t* hist, int64_t bins, uint64_t* oob,
                         void* ws, size_t ws_bytes, void* comm, void* stream);
+/* The same histogram with the all-reduce fused into the kernel: this rank's
+ * counts are added (system-scope atomics, over NVLink) straight into the hist
+ * and oob of every one of the npeers <= 8 ranks, given as device pointers
+ * mapped into this process (CUDA IPC).  After every rank's call has
+ * completed (the caller's barrier), each hist holds hist_in + all counts.
+ * No collective, no workspace; bins <= 12287. */
+int sdfgb_hist_f32_p2p(const float* img, int64_t n, double scale, double div,
+                       int64_t* const* peer_hist, uint64_t* const* peer_oob, int npeers,
+                       int64_t bins, void* stream);
 /* Sharded query: this rank's survivors -> out_vals[0:k); counts[world]
  * (device) receives every rank's k by ncclAllGather; count[0] += total and
  * offset[0] = this rank's global output offset (survivors on lower ranks). */

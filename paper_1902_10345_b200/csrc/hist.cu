@@ -82,11 +82,21 @@ __device__ __forceinline__ void smem_inc(uint32_t addr) {
     asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
 }
 
+// Where a CTA's counts go: one hist/oob pair (the one-GPU entries), or every
+// rank's pair mapped into this process (peer memory over NVLink): the
+// compute step and the all-reduce of the multi-GPU histogram in one kernel,
+// each cluster leader adding its bins straight into every rank's histogram.
+constexpr int kMaxPeers = 8;
+struct HistOut {
+    unsigned long long* hist[kMaxPeers];
+    unsigned long long* oob[kMaxPeers];
+    int n;  // destinations (1 = local only)
+};
+
 template <typename T, int MODE>
 __global__ void __cluster_dims__(kHistCluster, 1, 1) __launch_bounds__(kHistBlock)
 hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale, double div,
-                 int64_t bins64, int reps, unsigned long long* __restrict__ hist,
-                 unsigned long long* __restrict__ oob) {
+                 int64_t bins64, int reps, const HistOut out) {
     extern __shared__ uint32_t sh[];
     using V = typename Vec16<T>::type;
     constexpr int VN = Vec16<T>::n;
@@ -159,9 +169,22 @@ hist_smem_kernel(const T* __restrict__ in, int64_t n, int64_t head, double scale
     }
     cluster.sync();
     if (cluster.block_rank() == 0) {
-        for (uint32_t k = tid; k < row; k += blockDim.x) {
-            const uint32_t c = sh[k];
-            if (c) atomicAdd(k < bins ? &hist[k] : oob, (unsigned long long)c);
+        if (out.n == 1) {
+            for (uint32_t k = tid; k < row; k += blockDim.x) {
+                const uint32_t c = sh[k];
+                if (c) atomicAdd(k < bins ? &out.hist[0][k] : out.oob[0], (unsigned long long)c);
+            }
+        } else {
+            // system-scope adds into every rank's bins; clusters start at
+            // different ranks so the NVLink traffic spreads over the peers
+            const int first = (int)(blockIdx.x / kHistCluster) % out.n;
+            for (int q = 0; q < out.n; ++q) {
+                const int r = (first + q) % out.n;
+                for (uint32_t k = tid; k < row; k += blockDim.x) {
+                    const uint32_t c = sh[k];
+                    if (c) atomicAdd_system(k < bins ? &out.hist[r][k] : out.oob[r], (unsigned long long)c);
+                }
+            }
         }
     }
 }
@@ -181,15 +204,26 @@ hist_global_kernel(const T* __restrict__ in, int64_t n, double scale, double div
 
 template <typename T, int MODE>
 int launch_hist(const T* img, int64_t n, double scale, double div, int64_t* hist, int64_t bins,
-                uint64_t* oob, void* stream) {
-    if (n < 0 || bins <= 0 || (n > 0 && !img) || !hist || !oob)
+                uint64_t* oob, void* stream, const HistOut* peers = nullptr) {
+    if (n < 0 || bins <= 0 || (n > 0 && !img) || (!peers && (!hist || !oob)))
         return set_error(SDFGB_ERR_INVALID, "hist: bad arguments (n=%lld bins=%lld)",
                          (long long)n, (long long)bins);
     if (n == 0) return SDFGB_OK;
     cudaStream_t s = as_stream(stream);
-    auto* H = reinterpret_cast<unsigned long long*>(hist);
-    auto* O = reinterpret_cast<unsigned long long*>(oob);
+    HistOut out = {};
+    if (peers) {
+        out = *peers;
+    } else {
+        out.hist[0] = reinterpret_cast<unsigned long long*>(hist);
+        out.oob[0] = reinterpret_cast<unsigned long long*>(oob);
+        out.n = 1;
+    }
+    auto* H = out.hist[0];
+    auto* O = out.oob[0];
     if (bins + 1 > kMaxSmemBins || bins >= (1ll << 31)) {
+        if (out.n != 1)
+            return set_error(SDFGB_ERR_INVALID, "hist_p2p: %lld bins exceed the shared-memory kernel",
+                             (long long)bins);
         int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
         hist_global_kernel<T, MODE><<<blocks, 256, 0, s>>>(img, n, scale, div, bins, H, O);
         SDFGB_LAUNCHED("hist_global_kernel");
@@ -235,7 +269,7 @@ int launch_hist(const T* img, int64_t n, double scale, double div, int64_t* hist
     attr[0].val.programmaticStreamSerializationAllowed = SDFGB_H_PDL;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SDFGB_CUDA(cudaLaunchKernelEx(&cfg, kern, img, n, head, scale, div, bins, reps, H, O));
+    SDFGB_CUDA(cudaLaunchKernelEx(&cfg, kern, img, n, head, scale, div, bins, reps, out));
     SDFGB_LAUNCHED("hist_smem_kernel");
     return SDFGB_OK;
 }
@@ -251,6 +285,23 @@ bool pow2_exact(double scale, double div, int64_t bins) {
     return frexp(scale, &e) == 0.5;
 }
 }  // namespace
+
+extern "C" int sdfgb_hist_f32_p2p(const float* img, int64_t n, double scale, double div,
+                                  int64_t* const* peer_hist, uint64_t* const* peer_oob, int npeers,
+                                  int64_t bins, void* stream) {
+    if (npeers < 1 || npeers > sdfgb::kMaxPeers || !peer_hist || !peer_oob)
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "hist_p2p: 1..%d destinations", sdfgb::kMaxPeers);
+    sdfgb::HistOut out = {};
+    for (int r = 0; r < npeers; ++r) {
+        if (!peer_hist[r] || !peer_oob[r]) return sdfgb::set_error(SDFGB_ERR_INVALID, "hist_p2p: null destination");
+        out.hist[r] = reinterpret_cast<unsigned long long*>(peer_hist[r]);
+        out.oob[r] = reinterpret_cast<unsigned long long*>(peer_oob[r]);
+    }
+    out.n = npeers;
+    if (pow2_exact(scale, div, bins))
+        return sdfgb::launch_hist<float, sdfgb::kPow2>(img, n, scale, div, nullptr, bins, nullptr, stream, &out);
+    return sdfgb::launch_hist<float, sdfgb::kScaled>(img, n, scale, div, nullptr, bins, nullptr, stream, &out);
+}
 
 extern "C" int sdfgb_hist_f32(const float* img, int64_t n, double scale, double div,
                               int64_t* hist, int64_t bins, uint64_t* oob, void* stream) {

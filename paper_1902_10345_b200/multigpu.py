@@ -92,6 +92,63 @@ def finish_histogram(pending, hist, oob):
     pending.clear()
 
 
+class PeerHist:
+    """Every rank's ``hist`` / ``oob`` device tensors mapped into this process
+    (CUDA IPC handles exchanged once through ``pg``), for
+    :func:`histogram_p2p`.  The tensors must stay alive and keep their
+    storage while the mapping is in use."""
+
+    def __init__(self, pg, hist, oob):
+        import ctypes
+        import torch
+        from torch.multiprocessing.reductions import reduce_tensor
+        rank, world = _rank_world(pg)
+        if world > 8:
+            raise ValueError("hist_p2p maps at most 8 ranks")
+        if hist.dtype != torch.int64 or oob.dtype != torch.int64 or not hist.is_cuda:
+            raise TypeError("hist / oob must be int64 CUDA tensors")
+        mine = (reduce_tensor(hist), reduce_tensor(oob))
+        handles = [None] * world
+        pg.all_gather_object(handles, mine)
+        self.hists, self.oobs = [], []
+        for r, ((hf, ha), (of, oa)) in enumerate(handles):
+            if r == rank:
+                self.hists.append(hist)
+                self.oobs.append(oob)
+            else:
+                self.hists.append(hf(*ha))
+                self.oobs.append(of(*oa))
+        self.world = world
+        self.bins = hist.numel()
+        self.hist_ptrs = (ctypes.c_void_p * world)(*[t.data_ptr() for t in self.hists])
+        self.oob_ptrs = (ctypes.c_void_p * world)(*[t.data_ptr() for t in self.oobs])
+
+
+def histogram_p2p(pg, img_shard, peers: PeerHist, scale=256.0, div=1.0, stream=None):
+    """hist += counts of this rank's shard on EVERY rank, from inside the
+    histogram kernel (sdfgb_hist_f32_p2p: system-scope atomics into the
+    peers' bins over NVLink) -- the partial-bins all-reduce fused into the
+    compute.  Every rank's hist is complete once all ranks' calls are:
+    :func:`finish_histogram_p2p` synchronises and barriers."""
+    import torch
+    from . import _lib
+    if img_shard.dtype != torch.float32:
+        raise TypeError("histogram_p2p takes float32 images")
+    L = _lib.load()
+    st = stream if stream is not None else torch.cuda.current_stream()
+    import ctypes
+    _lib.check(L.sdfgb_hist_f32_p2p(img_shard.data_ptr(), img_shard.numel(), float(scale), float(div),
+                                    ctypes.cast(peers.hist_ptrs, ctypes.c_void_p),
+                                    ctypes.cast(peers.oob_ptrs, ctypes.c_void_p), peers.world, peers.bins,
+                                    st.cuda_stream))
+
+
+def finish_histogram_p2p(pg, stream=None):
+    import torch
+    (stream or torch.cuda.current_stream()).synchronize()  # this rank's remote adds are done
+    pg.barrier()                                          # and every other rank's
+
+
 # --------------------------------------------------------------------- query
 
 def query(pg, col_shard, thr, out_shard, count, backend, op="<", gather=False, pending=None):

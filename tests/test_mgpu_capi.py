@@ -160,3 +160,60 @@ def test_gemm_mgpu_one_rank(comm):
     _lib.check(L.sdfgb_gemm_f32_mgpu(_p(dA), M, _p(dB), K, K, N, _p(Ap), _p(Bp), _p(C), _p(ws), ws.numel(),
                                      comm, comm, _s()))
     np.testing.assert_array_equal(C.cpu().numpy(), ref.cpu().numpy())
+
+
+def _p2p_worker(rank, world, port, shards, h0, out_q):
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_1902_10345_b200 import multigpu as MG
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        hist = torch.from_numpy(h0.copy()).cuda()
+        oob = torch.zeros(1, dtype=torch.int64, device="cuda")
+        peers = MG.PeerHist(dist, hist, oob)
+        img = torch.from_numpy(shards[rank]).cuda()
+        for _ in range(2):  # two calls: counts accumulate on every rank
+            MG.histogram_p2p(dist, img, peers)
+        MG.finish_histogram_p2p(dist)
+        out_q.put((rank, hist.cpu().numpy(), int(oob.item())))
+        dist.barrier()  # keep every exported buffer alive until all ranks have read
+        dist.destroy_process_group()
+    except Exception as exc:  # surfaced by the parent
+        out_q.put((rank, repr(exc), -1))
+
+
+@pytest.mark.gpu
+def test_hist_p2p_two_processes_one_gpu(cuda_ok):
+    """the fused compute + all-reduce histogram over CUDA IPC peer mappings:
+    two processes (on the one GPU here) each add their shard's counts into
+    both processes' hist from inside the kernel; no kernel waits on another"""
+    import socket
+    import torch.multiprocessing as mp
+    rng = np.random.default_rng(8)
+    shards = [rng.random((513, 700), dtype=np.float32) for _ in range(2)]
+    shards[1][3, :4] = [1.5, -2.0, np.nan, 0.25]
+    h0 = rng.integers(0, 4, 256).astype(np.int64)
+    ref = h0.copy()
+    oob_ref = 0
+    for sh in shards:
+        r, o = oracle.histogram(sh, np.zeros(256, np.int64))
+        ref += 2 * r
+        oob_ref += 2 * o
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, 2, port, shards, h0, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, hist, oob in sorted(res, key=lambda x: x[0]):
+        assert not isinstance(hist, str), hist
+        np.testing.assert_array_equal(hist, ref)
+        assert oob == oob_ref
