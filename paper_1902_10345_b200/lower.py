@@ -519,6 +519,7 @@ class Lowering:
         self.devfns: list[str] = []
         self.kcount = 0
         self.tcount = 0
+        self.scoped: dict = {}  # transient -> (state, top entry): thread-sliced per-iteration scratch
         self.private = self._find_private()
         self.consumed = set()
         for st in g.states:
@@ -591,6 +592,11 @@ class Lowering:
                 sz = self.static_size(d)
                 if sz is not None and sz <= MAX_PRIVATE:
                     out.add(name)
+                else:
+                    # symbolic or large: each thread of the owning map's grid gets
+                    # its own slice of one HBM buffer (iterations run concurrently;
+                    # the reference's sequential loop shares one buffer)
+                    self.scoped[name] = next(iter(owners))
         return out
 
     # -- parameters ----------------------------------------------------------
@@ -1161,6 +1167,10 @@ class Lowering:
                       for e in st.in_edges(n.id))
         denv = Env(self, {}, host=False)
         body = []
+        scoped = sorted(x for x, (sn, top) in self.scoped.items() if sn == st.name and top == n.id)
+        for x in scoped:  # this thread's slice
+            body.append(f"    {self.cname(x)} += (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * "
+                        f"{self.size_expr(x, denv)};")
         if dynamic:
             # data-dependent range (e.g. the SpMV row map after MapToForLoop):
             # every thread reads the bounds from HBM, the grid is fixed
@@ -1194,15 +1204,27 @@ class Lowering:
         body.append("    }")
         k = self.new_kernel(body, f"{st.name}_map{n.id}")
         self.finish_counts(st, n.id, host_env, "    ", out, host=True)
+
+        def grow(nth: str) -> None:
+            for x in scoped:
+                c, bt = self.cname(x), CT[self.g.data[x].basetype]
+                out.append(f"      {{ const int64_t need = ({nth}) * {self.size_expr(x, host_env)};")
+                out.append(f"        if (need > tcap_{_ident(x)}) {{ if ({c}) cudaFreeAsync({c}, st); {c} = nullptr;")
+                out.append(f"          if (cudaMallocAsync((void**)&{c}, (size_t)need * sizeof({bt}), st) != "
+                           f"cudaSuccess) goto gen_fail;")
+                out.append(f"          cudaMemsetAsync({c}, 0, (size_t)need * sizeof({bt}), st); "
+                           f"tcap_{_ident(x)} = need; }} }}")
         if dynamic:
+            grow("148LL * 256")
             out.append(f"    {k}<<<148, 256, 0, st>>>({self.kargs()}); GEN_CHECK();")
             return
         # host: launch over the same flattened range
         tot = " * ".join(f"g_rlen({host_env.emit(r.begin)}, {host_env.emit(r.end)}, {host_env.emit(r.stride)})"
                          for r in n.ranges)
         out.append(f"    {{ const int64_t tot = {tot};")
-        out.append(f"      if (tot > 0) {{ {k}<<<gen_blocks(tot), 256, 0, st>>>({self.kargs()}); "
-                   f"GEN_CHECK(); }} }}")
+        out.append("      if (tot > 0) {")
+        grow("(int64_t)gen_blocks(tot) * 256")
+        out.append(f"      {k}<<<gen_blocks(tot), 256, 0, st>>>({self.kargs()}); GEN_CHECK(); }} }}")
 
     def top_consume(self, st: State, parent: dict, n, out: list) -> None:
         """A consume scope (codegen.py:526-543: P workers popping until the
@@ -1212,6 +1234,8 @@ class Lowering:
         to pop), runs the scope body on the item, and counts it finished
         after the body's pushes.  Only ``size(S) > 0`` conditions -- run
         until the stream is drained -- are lowered."""
+        if any(sn == st.name and top == n.id for sn, top in self.scoped.values()):
+            raise LoweringError("a consume scope's transients need a static size")
         se = next((e for e in st.in_edges(n.id) if e.dst_conn == "IN_stream"), None)
         if se is None or se.memlet.is_empty:
             raise LoweringError("consume entry without a stream")
@@ -1432,7 +1456,11 @@ class Lowering:
         lines.append("    int* g_err = nullptr;")
         if self.rep is not None:
             lines += ["    unsigned long long* g_rep = nullptr;", "    int64_t g_nv = 0;"]
-        trans = [(n, d) for n, d in g.data.items() if d.transient and d.kind == "array" and n not in self.private]
+        trans = [(n, d) for n, d in g.data.items() if d.transient and d.kind == "array" and n not in self.private
+                 and n not in self.scoped]
+        for name in sorted(self.scoped):
+            lines += [f"    {CT[g.data[name].basetype]}* {self.cname(name)} = nullptr;",
+                      f"    int64_t tcap_{_ident(name)} = 0;"]
         streams = [(n, d) for n, d in g.data.items() if d.kind == "stream"]
         for name, d in trans:
             lines.append(f"    {CT[d.basetype]}* {self.cname(name)} = nullptr;")
@@ -1522,6 +1550,7 @@ class Lowering:
                       "    for (int i = 0; i < @NREP@; ++i) g_reph[i] += dv[i];",
                       "    *g_nvis = g_nv;", "    }", "    cudaFreeAsync(g_rep, st);"]
         free = [f"    if ({self.cname(n)}) cudaFreeAsync({self.cname(n)}, st);" for n, _ in trans]
+        free += [f"    if ({self.cname(n)}) cudaFreeAsync({self.cname(n)}, st);" for n in sorted(self.scoped)]
         for name, _ in streams:
             free += [f"    if ({self.cname(name)}) cudaFreeAsync({self.cname(name)}, st);",
                      f"    if (n_{_ident(name)}) cudaFreeAsync(n_{_ident(name)}, st);"]

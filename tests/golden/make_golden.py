@@ -310,6 +310,43 @@ def transformed_cases():
             save_case(name, "small", g2, {k: np.array(v, copy=True) for k, v in arrays.items()}, symbols)
 
 
+def xform_fixture_cases():
+    """The reference's transformation micro-programs (tests/xform_fixtures.py:
+    nested_scale, flat_scale_2d, two_stage_pipeline, scale_1d,
+    looped_pipeline, two_states, nested_invoke, copy_chain, tiled_matmul)
+    as graphs xf_<name>, and each after every registered transformation that
+    matches it as x_xf_<name>_<rule> -- interpreter outputs on the fixture's
+    own input generator."""
+    import importlib.util
+    from sdfg.rewriting import apply_transformation, find_matches, registry
+    spec = importlib.util.spec_from_file_location(
+        "xform_fixtures", os.path.join(os.path.dirname(M.REF_SRC), "tests", "xform_fixtures.py"))
+    xf = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(xf)
+    names = ["nested_scale", "flat_scale_2d", "two_stage_pipeline", "scale_1d", "looped_pipeline", "two_states",
+             "nested_invoke", "copy_chain", "tiled_matmul"]
+    for k, name in enumerate(names):
+        fx = getattr(xf, name)()
+        arrays, symbols = fx.make_inputs(np.random.default_rng(400 + k))
+        base = f"xf_{name}"
+        save_graph(base, fx.sdfg)
+        save_case(base, "fx", fx.sdfg, {a: np.array(v, copy=True) for a, v in arrays.items()}, symbols)
+        for tname in sorted(registry):
+            try:
+                ms = find_matches(fx.sdfg, tname)
+            except Exception:
+                continue
+            if not ms:
+                continue
+            try:
+                g2, _ = apply_transformation(fx.sdfg, ms[0], {})
+            except Exception:
+                continue
+            gname = f"x_xf_{name}_{tname}"
+            save_graph(gname, g2)
+            save_case(gname, "fx", g2, {a: np.array(v, copy=True) for a, v in arrays.items()}, symbols)
+
+
 def vector_cases():
     """Vectorization (library.py:763-840): an element-wise map widened to 4-
     and 8-lane tiles; the same inputs through the plain graph."""
@@ -349,6 +386,7 @@ def custom_wcr_cases():
 
 
 if __name__ == "__main__":
+    xform_fixture_cases()
     oob_cases()
     custom_wcr_cases()
     vector_cases()

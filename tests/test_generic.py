@@ -26,12 +26,15 @@ GALLERY = ["branching", "fibonacci", "histogram", "indirection", "laplace", "man
            "spmv"]
 MOTIF_GRAPHS = ["histogram", "histogram_int", "query", "query_gallery", "spmv", "jacobi2d", "laplace1d",
                 "matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "axpy", "maxabs", "oob"]
+# the reference's transformation micro-programs (tests/xform_fixtures.py)
+XFORM = sorted(os.path.basename(p)[:-len(".sdfg.json")]
+               for p in glob.glob(os.path.join(os.path.dirname(graph_path("x")), "xf_*.sdfg.json")))
 # every motif graph after every reference transformation that matches it
 TRANSFORMED = sorted(os.path.basename(p)[:-len(".sdfg.json")]
                      for p in glob.glob(os.path.join(os.path.dirname(graph_path("x")), "x_*.sdfg.json")))
 # outputs assembled by atomics from several threads: order-free comparison
 UNORDERED_SUMS = {"matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "gal_matmul", "x_matmul_MapExpansion",
-                  "x_matmul_MapTiling"}
+                  "x_matmul_MapTiling", "xf_tiled_matmul", "x_xf_tiled_matmul_MapTiling"}
 STREAM_OUT = {"gal_query": ("out_vals", "count"), "query": ("out_vals", "count"),
               "query_gallery": ("out_vals", "count"), "x_query_LocalStream": ("out_vals", "count"),
               "x_query_MapTiling": ("out_vals", "count"), "x_query_RedundantArray": ("out_vals", "count")}
@@ -43,7 +46,7 @@ def _doc(name):
 
 # ------------------------------------------------------------------ CPU
 
-@pytest.mark.parametrize("name", [f"gal_{n}" for n in GALLERY] + MOTIF_GRAPHS)
+@pytest.mark.parametrize("name", [f"gal_{n}" for n in GALLERY] + MOTIF_GRAPHS + XFORM)
 def test_lowers(name):
     lw = lower(load(_doc(name)))
     assert f"extern \"C\" int {lw.entry}(" in lw.source
@@ -101,7 +104,7 @@ def _compare(graph, case, got):
 
 
 GPU_CASES = [(f"gal_{n}", c) for n in GALLERY for c in load_cases(f"gal_{n}")] + \
-            [(m, c) for m in MOTIF_GRAPHS for c in load_cases(m)]
+            [(m, c) for m in MOTIF_GRAPHS + XFORM for c in load_cases(m)]
 
 
 @pytest.mark.gpu
@@ -148,7 +151,8 @@ def test_transformed_motifs_match_the_interpreter(name, cuda_ok):
         assert got["out_vals"][0] in set(survivors.tolist())
         np.testing.assert_array_equal(got["out_vals"][1:], case.outputs["out_vals"][1:])
         return
-    motif_tol = name.startswith(("x_spmv", "x_gal_spmv"))
+    # float WCR sums assembled by device atomics (the generic lowering) or a lane tree (SpMV)
+    motif_tol = name.startswith(("x_spmv", "x_gal_spmv")) or name in UNORDERED_SUMS
     gemm_tol = name.startswith(("x_matmul", "x_gal_matmul"))  # the motif kernel is 3xTF32 at any precision
     for k, exp in case.outputs.items():
         g = np.asarray(got[k]).reshape(exp.shape)
