@@ -550,8 +550,8 @@ def bench_gemm(n, args, dist, P):
            "launches_per_step": 3,
            "roofline": {"bound": "tensor", "achieved": tf, "peak": pk, "unit": "TFLOP/s", "frac": tf / pk,
                         "peak_note": f"3xTF32 = {'sustained' if sustained else 'burst'} bf16 / 2 / 3 ({P['src']})",
-                        "achieved_note": "includes the hi/lo split pre-pass", "kernel": "gemm_3xtf32_kernel",
-                        "traffic": traffic("gemm_3xtf32_kernel")[0], "traffic_note": traffic("gemm_3xtf32_kernel")[1]},
+                        "achieved_note": "includes the hi/lo split pre-pass", "kernel": "gemm_3xtf32_pair_kernel",
+                        "traffic": traffic("gemm_3xtf32_pair_kernel")[0], "traffic_note": traffic("gemm_3xtf32_pair_kernel")[1]},
            "l2": "operands + split workspace > L2" if n >= 4096 else "",
            "config": {"workload": f"MM fp32 {n}^3 via tcgen05 3xTF32", "M": n, "N": n, "K": n},
            "steps": steps}

@@ -287,6 +287,216 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_consta
     }
 }
 
+// ------------------------------------------------------------ CTA-pair GEMM
+// cta_group::2: the two CTAs of a cluster form one 256 x 128 tile.  Each CTA
+// stages its own 128 rows of A and its half (64 rows) of the B tile; the
+// leader issues M = 256, N = 128 MMAs that read both CTAs' shared memory,
+// and each CTA's TMEM receives its 128 rows.  Per 128 x 128 x 8 step a CTA's
+// shared memory then takes 48 KB of operand fill and 6 KB of MMA reads
+// instead of 64 / 8 KB (profiles/r1_gemm_bound_experiment.txt: shared-memory
+// bytes per flop are what bounds the one-CTA kernel).
+#ifndef SDFGB_GEMM_WD
+#define SDFGB_GEMM_WD 0  // 1: trap instead of hanging on a stuck barrier (bring-up)
+#endif
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity) {
+#if SDFGB_GEMM_WD
+    long long spins = 0;
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, P1;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (++spins > (1LL << 28)) __trap();
+    }
+#else
+    mbar_wait(bar, parity);
+#endif
+}
+__device__ __forceinline__ uint32_t pair_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void pair_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// both CTAs load their halves; the bytes count on the LEADER's barrier
+// (shared::cluster address with the peer bit cleared)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on this offset in both CTAs
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+#ifndef SDFGB_GEMM_PAIR_GROUP
+#define SDFGB_GEMM_PAIR_GROUP 8  // tile rows per rasterisation group (sweep: 4 / 8 / 16 / 32)
+#endif
+constexpr int STAGES2 = 4;
+constexpr int BHALF = BN / 2;                                // B rows each CTA stages
+constexpr int BTILE2 = BHALF * BK * 4;                       // 8 KB
+constexpr int STAGE2_BYTES = 2 * TILE_BYTES + 2 * BTILE2;    // 48 KB: Ahi, Alo, Bhi half, Blo half
+constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                        const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
+                        float* __restrict__ C, int M, int N, int K) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+    uint64_t* empty = full + STAGES2;
+    uint64_t* tmem_full = empty + STAGES2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = pair_rank();
+    int m0, n0;  // this CTA's 128 rows; the pair's 128 columns
+    {
+        constexpr int G = SDFGB_GEMM_PAIR_GROUP / 2;  // pair rows per group
+        const int tiles_m = (M + 2 * BM - 1) / (2 * BM), tiles_n = (N + BN - 1) / BN;
+        const int pid = blockIdx.x / 2, group = G * tiles_n;
+        const int first_m = (pid / group) * G;
+        const int gm = min(tiles_m - first_m, G);
+        const int in_group = pid % group;
+        m0 = (first_m + in_group % gm) * 2 * BM + (int)rank * BM;
+        n0 = (in_group / gm) * BN;
+    }
+    const int KB = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES2; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAhi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAlo)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBhi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBlo)) : "memory");
+    }
+    if (warp == 2) {  // the same warp in both CTAs
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    pair_sync();  // the peer's barriers are initialised before any load signals them
+    tc_fence_after();
+    const uint32_t tmem_d = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // producer, in both CTAs
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % STAGES2;
+                const uint32_t ph = (kb / STAGES2) & 1;
+                mbar_wait_wd(&empty[s], ph ^ 1);  // both CTAs' stage s consumed by the pair MMA
+                uint8_t* st = smem + s * STAGE2_BYTES;
+                if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE2_BYTES);  // both halves
+                const uint32_t lbar = smem_u32(&full[s]) & 0xFEFFFFFFu;
+                tma_load_2d_pair(st + 0 * TILE_BYTES, &mAhi, lbar, kb * BK, m0);
+                tma_load_2d_pair(st + 1 * TILE_BYTES, &mAlo, lbar, kb * BK, m0);
+                tma_load_2d_pair(st + 2 * TILE_BYTES, &mBhi, lbar, kb * BK, n0 + (int)rank * BHALF);
+                tma_load_2d_pair(st + 2 * TILE_BYTES + BTILE2, &mBlo, lbar, kb * BK, n0 + (int)rank * BHALF);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {  // the leader issues the pair's MMAs
+            constexpr uint32_t idesc = idesc_tf32(2 * BM, BN);
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % STAGES2;
+                const uint32_t ph = (kb / STAGES2) & 1;
+                mbar_wait_wd(&full[s], ph);
+                tc_fence_after();
+                const uint32_t base = smem_u32(smem + s * STAGE2_BYTES);
+                const uint32_t dacc = tmem_d + (uint32_t)((kb % NACC) * BN);
+                const uint32_t first = kb < NACC;
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k) {
+                    const uint32_t off = k * 32;
+                    const uint64_t ahi = sw128_kmajor_desc(base + 0 * TILE_BYTES + off);
+                    const uint64_t alo = sw128_kmajor_desc(base + 1 * TILE_BYTES + off);
+                    const uint64_t bhi = sw128_kmajor_desc(base + 2 * TILE_BYTES + off);
+                    const uint64_t blo = sw128_kmajor_desc(base + 2 * TILE_BYTES + BTILE2 + off);
+                    tc_mma_tf32_pair(dacc, alo, bhi, idesc, !(first && k == 0));
+                    tc_mma_tf32_pair(dacc, ahi, blo, idesc, 1u);
+                    tc_mma_tf32_pair(dacc, ahi, bhi, idesc, 1u);
+                }
+                tc_commit_pair(&empty[s]);
+            }
+            tc_commit_pair(tmem_full);
+        }
+    } else if (warp >= 4) {  // epilogue, in both CTAs: this CTA's 128 rows
+        mbar_wait_wd(tmem_full, 0);
+        tc_fence_after();
+        const int rw = (warp & 3) * 32;
+        const int row = m0 + rw + lane;
+        const int nacc = KB < NACC ? KB : NACC;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+            uint32_t r[16];
+            tmem_ld16(tmem_d + ((uint32_t)rw << 16) + c, r);
+            for (int q = 1; q < nacc; ++q) {
+                uint32_t o[16];
+                tmem_ld16(tmem_d + ((uint32_t)rw << 16) + q * BN + c, o);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) + __uint_as_float(o[e]));
+            }
+            if (row < M) {
+                float* dst = C + (int64_t)row * N + n0 + c;
+                if (n0 + c + 16 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        reinterpret_cast<float4*>(dst)[q] =
+                            make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        if (n0 + c + q < N) dst[q] = __uint_as_float(r[q]);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    pair_sync();  // neither CTA leaves while the pair's MMAs / commits may touch it
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(TMEM_COLS));
+    }
+}
+
 // Long contractions: the same pipeline, but every CHUNK uses of an
 // accumulator are folded into per-thread fp32 registers by 8 epilogue warps
 // (2 per TMEM lane quarter) while the tensor core keeps going on the other
@@ -522,9 +732,22 @@ gemm_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict
 }
 
 // ------------------------------------------------------------ host side
-int make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t K) {
-    return encode_tiled_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, rows, K, BK, BM,
+int make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t K, int box_rows = BM) {
+    return encode_tiled_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, rows, K, BK, box_rows,
                            CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// CTA-pair kernel by default (4096^3: 611 -> 594 us; 16384^3 on par);
+// SDFGB_GEMM_PAIR=0 selects the one-CTA kernel
+bool gemm_use_pair() {
+#ifndef SDFGB_GEMM_PAIR_DEFAULT
+#define SDFGB_GEMM_PAIR_DEFAULT 1
+#endif
+    static const bool on = [] {
+        const char* e = getenv("SDFGB_GEMM_PAIR");
+        return e ? atoi(e) != 0 : SDFGB_GEMM_PAIR_DEFAULT != 0;
+    }();
+    return on;
 }
 
 }  // namespace
@@ -573,6 +796,22 @@ extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t 
     CUtensorMap mAhi, mAlo, mBhi, mBlo;
     SDFGB_TRY(make_kmajor_map(&mAhi, Ahi, M, K));
     SDFGB_TRY(make_kmajor_map(&mAlo, Alo, M, K));
+    if (K <= kFlushK && gemm_use_pair()) {
+        SDFGB_TRY(make_kmajor_map(&mBhi, Bhi, N, K, BHALF));
+        SDFGB_TRY(make_kmajor_map(&mBlo, Blo, N, K, BHALF));
+        static std::once_flag attr2;
+        static cudaError_t attr2_err = cudaSuccess;
+        std::call_once(attr2, [] {
+            attr2_err = cudaFuncSetAttribute(gemm_3xtf32_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             GEMM2_SMEM);
+        });
+        SDFGB_CUDA(attr2_err);
+        const int64_t pairs = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+        gemm_3xtf32_pair_kernel<<<(unsigned)(2 * pairs), GEMM_THREADS, GEMM2_SMEM, s>>>(mAhi, mAlo, mBhi, mBlo, C,
+                                                                                     (int)M, (int)N, (int)K);
+        SDFGB_LAUNCHED("gemm_3xtf32_pair_kernel");
+        return SDFGB_OK;
+    }
     SDFGB_TRY(make_kmajor_map(&mBhi, Bhi, N, K));
     SDFGB_TRY(make_kmajor_map(&mBlo, Blo, N, K));
     static std::once_flag attr;
