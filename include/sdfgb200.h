@@ -178,6 +178,16 @@ int sdfgb_hist_f32_mgpu(const float* img, int64_t n, double scale, double div,
 int sdfgb_hist_f32_p2p(const float* img, int64_t n, double scale, double div,
                        int64_t* const* peer_hist, uint64_t* const* peer_oob, int npeers,
                        int64_t bins, void* stream);
+/* The gathered multi-GPU query with the gather fused into the compaction:
+ * this rank's survivors are stored over NVLink straight into the gathering
+ * rank's out_root, at slots reserved with system-scope atomics on its
+ * int64 counter reserve_root (both mapped into this process, CUDA IPC).
+ * After every rank's call has completed (the caller's barrier),
+ * out_root[0:*reserve_root) holds all survivors in unspecified order (a
+ * stream's push order); the caller adds *reserve_root to count
+ * and re-zeroes it.  col 16-byte aligned; ws as for sdfgb_query_f32. */
+int sdfgb_query_f32_p2p(const float* col, int64_t n, int op, double thr, float* out_root,
+                        int64_t* reserve_root, void* ws, size_t ws_bytes, void* stream);
 /* Sharded query: this rank's survivors -> out_vals[0:k); counts[world]
  * (device) receives every rank's k by ncclAllGather; count[0] += total and
  * offset[0] = this rank's global output offset (survivors on lower ranks). */

@@ -49,6 +49,7 @@ SIGNATURES = {
     "sdfgb_hist_mgpu_workspace_bytes": (_SZ, [_I64]),
     "sdfgb_hist_f32_mgpu": (_INT, [_P, _I64, _F64, _F64, _P, _I64, _P, _P, _SZ, _P, _P]),
     "sdfgb_hist_f32_p2p": (_INT, [_P, _I64, _F64, _F64, _P, _P, _INT, _I64, _P]),
+    "sdfgb_query_f32_p2p": (_INT, [_P, _I64, _INT, _F64, _P, _P, _P, _SZ, _P]),
     "sdfgb_query_f32_mgpu": (_INT, [_P, _I64, _INT, _F64, _P, _P, _P, _P, _P, _SZ, _P, _P]),
     "sdfgb_spmv_csr_f32_mgpu": (_INT, [_P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P]),
     "sdfgb_jacobi2d_f32_mgpu": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _F64, _P, _P]),

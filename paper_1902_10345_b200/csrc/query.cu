@@ -580,7 +580,7 @@ template <typename T>
 __device__ __forceinline__ void push_store(T* __restrict__ out, unsigned long long* __restrict__ ctr, int lane,
                                            int warp, const typename Vec16<T>::type (&x)[kPChunks], uint32_t bits,
                                            const uint32_t (&pk)[2], uint32_t* sw, unsigned long long* sbase,
-                                           T* stage) {
+                                           T* stage, bool remote) {
     using V = typename Vec16<T>::type;
     constexpr int VN = Vec16<T>::n;
     constexpr int NW = kPBlock / 32;
@@ -610,7 +610,8 @@ __device__ __forceinline__ void push_store(T* __restrict__ out, unsigned long lo
             const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
             if (lane >= d) inc += o;
         }
-        if (lane == NW - 1) *sbase = atomicAdd(ctr, (unsigned long long)inc);
+        if (lane == NW - 1)
+            *sbase = remote ? atomicAdd_system(ctr, (unsigned long long)inc) : atomicAdd(ctr, (unsigned long long)inc);
         __syncwarp();
         if (lane < NW) sw[lane] = inc - v;  // exclusive warp offsets
     }
@@ -647,7 +648,12 @@ template <typename T, int OP>
 __global__ void __launch_bounds__(kPBlock, SDFGB_P_MINB)
 query_push_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
                   unsigned long long* __restrict__ count, unsigned long long* __restrict__ ctr,
-                  unsigned long long* __restrict__ done) {
+                  unsigned long long* __restrict__ done, int remote) {
+    // remote: `out` and `ctr` are the gathering rank's output and reservation
+    // counter mapped over NVLink (peer memory); every rank's tiles reserve
+    // their slots there with one system-scope atomic and store their
+    // survivors straight into it -- the compaction and the gather in one
+    // pass.  The caller folds the counter after all ranks' launches.
     using V = typename Vec16<T>::type;
     constexpr int VN = Vec16<T>::n;
     constexpr int NW = kPBlock / 32;
@@ -670,7 +676,7 @@ query_push_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ o
             for (int j = 0; j < kPChunks; ++j) x[j] = ldg_hint(col + w0 + j * CH + lane * VN, drop);
         }
         push_bits<T, OP>(col, n, w0, lane, thr, drop, full, x, bits, pk);
-        push_store<T>(out, ctr, lane, warp, x, bits, pk, s_w[0], &s_base[0], stage);
+        push_store<T>(out, ctr, lane, warp, x, bits, pk, s_w[0], &s_base[0], stage, remote != 0);
     } else {
         // persistent: the next tile's loads are issued before this tile's
         // reservation, so the atomic's round trip overlaps HBM traffic
@@ -692,15 +698,17 @@ query_push_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ o
             for (int j = 0; j < kPChunks; ++j) x[j] = nx[j];
             prefetch(t + gridDim.x);
             push_bits<T, OP>(col, n, w0, lane, thr, drop, full, x, bits, pk);
-            push_store<T>(out, ctr, lane, warp, x, bits, pk, s_w[par], &s_base[par], stage);
+            push_store<T>(out, ctr, lane, warp, x, bits, pk, s_w[par], &s_base[par], stage, remote != 0);
         }
     }
     if (tid == NW - 1) {  // the thread that reserved: publish completion after its reservations
         __threadfence();
         if (atomicAdd(done, 1ull) == (unsigned long long)gridDim.x - 1) {
             __threadfence();
-            const unsigned long long total = atomicExch(ctr, 0ull);
-            atomicAdd(count, total);
+            if (!remote) {
+                const unsigned long long total = atomicExch(ctr, 0ull);
+                atomicAdd(count, total);
+            }
             *done = 0ull;
         }
     }
@@ -831,7 +839,7 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
             G = std::min<int64_t>(G, (int64_t)std::max(po, 1) * num_sms());
         }
         if (G > 0x7fffffff) return set_error(SDFGB_ERR_INVALID, "query: n too large");
-        pk<<<(unsigned)G, kPBlock, 0, s>>>(col, n, tt, out, C, &W->ticket, &W->done);
+        pk<<<(unsigned)G, kPBlock, 0, s>>>(col, n, tt, out, C, &W->ticket, &W->done, 0);
         SDFGB_LAUNCHED("query_push_kernel");
         return SDFGB_OK;
     }
@@ -878,4 +886,37 @@ extern "C" int sdfgb_query_f32(const float* col, int64_t n, int op, double thr, 
 extern "C" int sdfgb_query_f64(const double* col, int64_t n, int op, double thr, double* out_vals,
                                int64_t* count, void* ws, size_t ws_bytes, void* stream) {
     return sdfgb::launch_query<double>(col, n, op, thr, out_vals, count, ws, ws_bytes, stream);
+}
+
+// Fused compaction + gather over NVLink (multi-GPU query, gathered output):
+// this rank's survivors go straight into the gathering rank's out_root at
+// slots reserved with system-scope atomics on its counter reserve_root
+// (both mapped into this process).  After every rank's call has completed
+// (the caller's barrier), out_root[0:*reserve_root) holds all survivors in
+// unspecified order; the caller adds *reserve_root to count and re-zeroes it.
+extern "C" int sdfgb_query_f32_p2p(const float* col, int64_t n, int op, double thr, float* out_root,
+                                   int64_t* reserve_root, void* ws, size_t ws_bytes, void* stream) {
+    using namespace sdfgb;
+    if (n < 0 || op < 0 || op > 5 || !reserve_root || (n > 0 && (!col || !out_root || !ws)))
+        return set_error(SDFGB_ERR_INVALID, "query_p2p: bad arguments");
+    if (n == 0) return SDFGB_OK;
+    if ((reinterpret_cast<uintptr_t>(col) & 15) != 0)
+        return set_error(SDFGB_ERR_INVALID, "query_p2p: col must be 16-byte aligned");
+    if (ws_bytes < sdfgb_query_workspace_bytes(n, 4) || (reinterpret_cast<uintptr_t>(ws) & 7) != 0)
+        return set_error(SDFGB_ERR_WORKSPACE, "query_p2p: workspace too small or misaligned");
+    auto* W = reinterpret_cast<QueryWs*>(ws);
+    cudaStream_t s = as_stream(stream);
+    int kop;
+    float tt;
+    fold_threshold<float>(op, thr, kop, tt);
+    constexpr int64_t tile = push_tile_elems<float>();
+    int64_t G = (n + tile - 1) / tile;
+    auto pk = query_push_kernel_for<float>(kop);
+    static int po[8] = {};
+    if (po[kop] == 0) SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&po[kop], pk, kPBlock, 0));
+    G = std::min<int64_t>(G, (int64_t)std::max(po[kop], 1) * num_sms());
+    pk<<<(unsigned)G, kPBlock, 0, s>>>(col, n, tt, out_root, nullptr,
+                                       reinterpret_cast<unsigned long long*>(reserve_root), &W->done, 1);
+    SDFGB_LAUNCHED("query_push_kernel");
+    return SDFGB_OK;
 }

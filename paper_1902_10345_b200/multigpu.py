@@ -188,6 +188,63 @@ def query(pg, col_shard, thr, out_shard, count, backend, op="<", gather=False, p
     return cl[rank], offset, full
 
 
+class QueryGather:
+    """Rank ``root``'s gathered-output buffer and reservation counter mapped
+    into every rank (CUDA IPC handles exchanged once through ``pg``), for
+    :func:`query_p2p`.  ``out_root`` / ``reserve`` are only read on the root;
+    the other ranks pass tensors of the right dtype (they are not used)."""
+
+    def __init__(self, pg, out_root, reserve, root=0):
+        import torch
+        from torch.multiprocessing.reductions import reduce_tensor
+        rank, world = _rank_world(pg)
+        if out_root.dtype != torch.float32 or reserve.dtype != torch.int64 or not out_root.is_cuda:
+            raise TypeError("out_root must be float32 and reserve int64 CUDA tensors")
+        obj = [(reduce_tensor(out_root), reduce_tensor(reserve)) if rank == root else None]
+        pg.broadcast_object_list(obj, src=root)
+        if rank == root:
+            self.out, self.reserve = out_root, reserve
+        else:
+            (of, oa), (rf, ra) = obj[0]
+            self.out, self.reserve = of(*oa), rf(*ra)
+        self.root = root
+
+
+def query_p2p(pg, col_shard, thr, gather: QueryGather, ws, op="<", stream=None):
+    """This rank's survivors of ``col OP thr`` go straight into the root's
+    output (sdfgb_query_f32_p2p: slots reserved with system-scope atomics on
+    the root's counter, survivors stored over NVLink): compaction and gather
+    in one pass, no collective.  :func:`finish_query_p2p` completes it."""
+    import torch
+    from . import _lib
+    if col_shard.dtype != torch.float32:
+        raise TypeError("query_p2p takes float32 columns")
+    L = _lib.load()
+    st = stream if stream is not None else torch.cuda.current_stream()
+    _lib.check(L.sdfgb_query_f32_p2p(col_shard.data_ptr(), col_shard.numel(), _lib.CMP[op], float(thr),
+                                     gather.out.data_ptr(), gather.reserve.data_ptr(), ws.data_ptr(), ws.numel(),
+                                     st.cuda_stream))
+
+
+def finish_query_p2p(pg, gather: QueryGather, count, stream=None):
+    """Wait for every rank's gather, advance ``count`` (replicated) by the
+    number of survivors gathered, and re-zero the root's counter.  Returns
+    that number (a host int)."""
+    import torch
+    (stream or torch.cuda.current_stream()).synchronize()
+    pg.barrier()                        # every rank's survivors have landed
+    total = int(gather.reserve.item())  # the root's counter, read over NVLink elsewhere
+    count += total
+    torch.cuda.synchronize()
+    pg.barrier()                        # everyone has read it
+    rank, _ = _rank_world(pg)
+    if rank == gather.root:
+        gather.reserve.zero_()
+        torch.cuda.synchronize()
+    pg.barrier()
+    return total
+
+
 def finish_query(pending, count):
     """Wait for the deferred count exchanges of query(..., pending=...) and
     advance ``count`` by every call's global survivor count."""

@@ -217,3 +217,59 @@ def test_hist_p2p_two_processes_one_gpu(cuda_ok):
         assert not isinstance(hist, str), hist
         np.testing.assert_array_equal(hist, ref)
         assert oob == oob_ref
+
+
+def _qgather_worker(rank, world, port, shards, out_q):
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_1902_10345_b200 import device
+    from paper_1902_10345_b200 import multigpu as MG
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        cap = sum(s.size for s in shards)
+        out = torch.full((cap if rank == 0 else 1,), -1.0, dtype=torch.float32, device="cuda")
+        reserve = torch.zeros(1, dtype=torch.int64, device="cuda")
+        g = MG.QueryGather(dist, out, reserve, root=0)
+        col = torch.from_numpy(shards[rank]).cuda()
+        ws = device.query_workspace(col.numel(), 4, "cuda")
+        count = torch.full((1,), 3, dtype=torch.int64, device="cuda")
+        totals = []
+        for _ in range(2):  # two rounds: the counter is re-zeroed between them
+            MG.query_p2p(dist, col, 0.5, g, ws, "<")
+            totals.append(MG.finish_query_p2p(dist, g, count))
+        got = out[:totals[-1]].cpu().numpy() if rank == 0 else None
+        out_q.put((rank, totals, int(count.item()), got))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:
+        out_q.put((rank, repr(exc), -1, None))
+
+
+@pytest.mark.gpu
+def test_query_p2p_gather_two_processes_one_gpu(cuda_ok):
+    """compaction + gather fused over CUDA IPC peer memory: both processes'
+    survivors land in rank 0's output at slots reserved on rank 0's counter"""
+    import socket
+    import torch.multiprocessing as mp
+    rng = np.random.default_rng(9)
+    shards = [rng.random(300_000, dtype=np.float32), rng.random(123_457 * 4, dtype=np.float32)]
+    sel = np.sort(np.concatenate([s[s < 0.5] for s in shards]))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_qgather_worker, args=(r, 2, port, shards, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, totals, count, got in res:
+        assert not isinstance(totals, str), totals
+        assert totals == [sel.size, sel.size]
+        assert count == 3 + 2 * sel.size
+    np.testing.assert_array_equal(np.sort(res[0][3]), sel)
