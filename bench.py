@@ -260,7 +260,10 @@ def bench_histogram(args, dist, P):
     if multi:
         from paper_1902_10345_b200 import multigpu as MG
         be = MG.DeviceBackend()
-        peers, exchange = _hist_peers(dist, hist, oob)
+        if os.environ.get("SDFGB_BENCH_P2P") == "1":
+            peers, exchange = _hist_peers(dist, hist, oob)
+        else:  # the fused NVLink path is opt-in until it has run on a multi-GPU box
+            peers, exchange = None, "nccl all_reduce (SDFGB_BENCH_P2P=1 selects the fused p2p kernel)"
 
     pending = []
 

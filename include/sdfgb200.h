@@ -160,6 +160,9 @@ int sdfgb_gemm_f64(const double* A, const double* B, double* C,
  * one-GPU entries.  NCCL is loaded at run time (libnccl.so.2); without it
  * these return SDFGB_ERR_COMM.  Python counterpart: multigpu.py.        */
 int sdfgb_nccl_available(void);
+/* Kernels on the current device may access memory on device `peer` (the
+ * P2P entries' peer mappings); already-enabled is success. */
+int sdfgb_enable_peer_access(int peer);
 int sdfgb_nccl_unique_id(void* id_out /* 128 bytes */);
 int sdfgb_nccl_comm_init(void** comm_out, int nranks, const void* id, int rank);
 int sdfgb_nccl_comm_destroy(void* comm);

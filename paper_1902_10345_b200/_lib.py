@@ -43,6 +43,7 @@ SIGNATURES = {
     "sdfgb_spmv_csr_f32": (_INT, [_P, _P, _P, _P, _P, _I64, _P]),
     "sdfgb_spmv_csr_f64": (_INT, [_P, _P, _P, _P, _P, _I64, _P]),
     "sdfgb_nccl_available": (_INT, []),
+    "sdfgb_enable_peer_access": (_INT, [_INT]),
     "sdfgb_nccl_unique_id": (_INT, [_P]),
     "sdfgb_nccl_comm_init": (_INT, [_P, _INT, _P, _INT]),
     "sdfgb_nccl_comm_destroy": (_INT, [_P]),

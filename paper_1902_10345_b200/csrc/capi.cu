@@ -152,6 +152,23 @@ extern "C" int sdfgb_device_count(int* count) {
     if (count) *count = e == cudaSuccess ? n : 0;
     return check_cuda(e, "cudaGetDeviceCount");
 }
+// Let kernels on the current device reach memory that lives on `peer` (the
+// IPC mappings of the P2P entries are made in the owning device's context)
+extern "C" int sdfgb_enable_peer_access(int peer) {
+    int dev = 0;
+    SDFGB_CUDA(cudaGetDevice(&dev));
+    if (peer == dev) return SDFGB_OK;
+    int can = 0;
+    SDFGB_CUDA(cudaDeviceCanAccessPeer(&can, dev, peer));
+    if (!can) return set_error(SDFGB_ERR_COMM, "device %d cannot access device %d (no peer path)", dev, peer);
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return SDFGB_OK;
+    }
+    return check_cuda(e, "cudaDeviceEnablePeerAccess");
+}
+
 extern "C" int sdfgb_host_alloc(void** ptr, size_t bytes) {
     return check_cuda(cudaHostAlloc(ptr, std::max<size_t>(bytes, 1), cudaHostAllocPortable), "cudaHostAlloc");
 }

@@ -92,6 +92,17 @@ def finish_histogram(pending, hist, oob):
     pending.clear()
 
 
+def _peer_access(tensors):
+    """IPC-rebuilt tensors live on the exporting rank's device: let this
+    rank's kernels reach them (cudaDeviceEnablePeerAccess)."""
+    import torch
+    from . import _lib
+    L = _lib.load()
+    here = torch.cuda.current_device()
+    for dev in sorted({t.device.index for t in tensors} - {here}):
+        _lib.check(L.sdfgb_enable_peer_access(dev))
+
+
 class PeerHist:
     """Every rank's ``hist`` / ``oob`` device tensors mapped into this process
     (CUDA IPC handles exchanged once through ``pg``), for
@@ -118,6 +129,7 @@ class PeerHist:
             else:
                 self.hists.append(hf(*ha))
                 self.oobs.append(of(*oa))
+        _peer_access(self.hists + self.oobs)
         self.world = world
         self.bins = hist.numel()
         self.hist_ptrs = (ctypes.c_void_p * world)(*[t.data_ptr() for t in self.hists])
@@ -207,6 +219,7 @@ class QueryGather:
         else:
             (of, oa), (rf, ra) = obj[0]
             self.out, self.reserve = of(*oa), rf(*ra)
+        _peer_access([self.out, self.reserve])
         self.root = root
 
 
