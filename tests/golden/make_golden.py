@@ -345,6 +345,16 @@ def xform_fixture_cases():
             gname = f"x_xf_{name}_{tname}"
             save_graph(gname, g2)
             save_case(gname, "fx", g2, {a: np.array(v, copy=True) for a, v in arrays.items()}, symbols)
+    # the acceptance suite's own parameterisations (test_acceptance.py:125-138)
+    accept = {"MapExpansion": ("flat_scale_2d", {"split": 1}), "MapTiling": ("scale_1d", {"tile": 4}),
+              "LocalStorage": ("tiled_matmul", {"data": "B"}), "Vectorization": ("scale_1d", {"width": 4})}
+    for tname, (name, params) in accept.items():
+        fx = getattr(xf, name)()
+        arrays, symbols = fx.make_inputs(np.random.default_rng(500 + len(tname)))
+        g2, _ = apply_transformation(fx.sdfg, find_matches(fx.sdfg, tname)[0], params)
+        gname = f"x_xf_{name}_{tname}_acc"
+        save_graph(gname, g2)
+        save_case(gname, "acc", g2, {a: np.array(v, copy=True) for a, v in arrays.items()}, symbols)
 
 
 def vector_cases():
