@@ -1187,7 +1187,9 @@ class Lowering:
         more = {}
         for k in reversed(range(len(n.params))):
             v = f"p_{_ident(n.params[k])}_{n.id}"
-            body.append(f"        const int64_t {v} = b{k} + (rem % n{k}) * s{k};")
+            # the outermost index needs no modulo: rem < n0 once the inner ones are divided out
+            idx = "rem" if k == 0 else f"(rem % n{k})"
+            body.append(f"        const int64_t {v} = b{k} + {idx} * s{k};")
             if k:
                 body.append(f"        rem /= n{k};")
             more[n.params[k]] = v
