@@ -14,6 +14,7 @@ import torch.multiprocessing as mp
 
 import oracle
 
+from conftest import REPO
 from paper_1902_10345_b200 import multigpu as MG
 
 
@@ -231,3 +232,31 @@ def test_sharded_equals_single_domain(case, world):
 
 def test_grid_shapes():
     assert [MG.grid_shape(w) for w in (1, 2, 4, 8)] == [(1, 1), (1, 2), (2, 2), (2, 4)]
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_plumbing_on_one_gpu(tmp_path):
+    """bench.py's N=2 path end to end (torchrun, per-rank shards, collectives,
+    max-over-ranks timing, one JSON line from rank 0) with both ranks on the
+    one GPU over gloo (SDFGB_BENCH_SHARE_GPU): a plumbing check, not a
+    measurement -- no kernel waits on another rank's kernel."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, SDFGB_BENCH_SHARE_GPU="1", SDFGB_BENCH_P2P="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(REPO, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e",
+           "--motif", "histogram,query,spmv,jacobi2d,gemm4096"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 2
+    for m in ("histogram", "query", "spmv", "jacobi2d", "gemm4096"):
+        assert d["motifs"][m]["value"] > 0, m
+    assert d["motifs"]["histogram"]["config"]["exchange"].startswith("p2p")
