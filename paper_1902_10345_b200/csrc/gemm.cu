@@ -356,13 +356,24 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on th
 #ifndef SDFGB_GEMM_PAIR_GROUP
 #define SDFGB_GEMM_PAIR_GROUP 8  // tile rows per rasterisation group (sweep: 4 / 8 / 16 / 32)
 #endif
-constexpr int STAGES2 = 4;
+#ifndef SDFGB_GEMM_PAIR_STAGES
+#define SDFGB_GEMM_PAIR_STAGES 4
+#endif
+#ifndef SDFGB_GEMM_PAIR_NACC
+#define SDFGB_GEMM_PAIR_NACC 4
+#endif
+#ifndef SDFGB_GEMM_PAIR_MINB
+#define SDFGB_GEMM_PAIR_MINB 1
+#endif
+constexpr int STAGES2 = SDFGB_GEMM_PAIR_STAGES;
+constexpr int PNACC = SDFGB_GEMM_PAIR_NACC;       // TMEM accumulators of the pair kernel
+constexpr int PTMEM_COLS = BN * PNACC;
 constexpr int BHALF = BN / 2;                                // B rows each CTA stages
 constexpr int BTILE2 = BHALF * BK * 4;                       // 8 KB
 constexpr int STAGE2_BYTES = 2 * TILE_BYTES + 2 * BTILE2;    // 48 KB: Ahi, Alo, Bhi half, Blo half
 constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256;
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, SDFGB_GEMM_PAIR_MINB)
 gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                         const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                         float* __restrict__ C, int M, int N, int K) {
@@ -406,7 +417,7 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_c
     if (warp == 2) {  // the same warp in both CTAs
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
+                     "r"(PTMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     tc_fence_before();
@@ -439,8 +450,8 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_c
                 mbar_wait_wd(&full[s], ph);
                 tc_fence_after();
                 const uint32_t base = smem_u32(smem + s * STAGE2_BYTES);
-                const uint32_t dacc = tmem_d + (uint32_t)((kb % NACC) * BN);
-                const uint32_t first = kb < NACC;
+                const uint32_t dacc = tmem_d + (uint32_t)((kb % PNACC) * BN);
+                const uint32_t first = kb < PNACC;
 #pragma unroll
                 for (int k = 0; k < BK / 8; ++k) {
                     const uint32_t off = k * 32;
@@ -461,7 +472,7 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_c
         tc_fence_after();
         const int rw = (warp & 3) * 32;
         const int row = m0 + rw + lane;
-        const int nacc = KB < NACC ? KB : NACC;
+        const int nacc = KB < PNACC ? KB : PNACC;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
             uint32_t r[16];
@@ -493,7 +504,7 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_c
     pair_sync();  // neither CTA leaves while the pair's MMAs / commits may touch it
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(TMEM_COLS));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(PTMEM_COLS));
     }
 }
 
