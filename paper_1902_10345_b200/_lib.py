@@ -88,11 +88,12 @@ _lock = threading.Lock()
 _lib = None
 
 
-def load(path: str = LIB_PATH):
+def load(path: str = None):
     global _lib
     with _lock:
         if _lib is not None:
             return _lib
+        path = path or LIB_PATH
         if not os.path.exists(path):
             raise BackendUnavailable(
                 f"{path} is not built; run __graft_entry__.build() (make -C paper_1902_10345_b200/csrc)")

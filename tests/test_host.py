@@ -238,3 +238,21 @@ class TestGPUTransformMapInReference:
             plan = classify(load(g))
             assert plan.motif == base.motif and plan.roles == base.roles, name
             assert len(find_matches(g, "GPUTransformMap")) == 1, name
+
+
+def test_missing_native_library_fails_loudly(tmp_path, monkeypatch):
+    """no CPU fallback: without libsdfgb200.so the product path raises"""
+    from paper_1902_10345_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(_lib.BackendUnavailable, match="not built"):
+        _lib.load(str(tmp_path / "libsdfgb200.so"))
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "libsdfgb200.so"))
+    import paper_1902_10345_b200 as b200
+    doc = json.load(open(graph_path("histogram")))
+    for d in doc["data"]:
+        if not d["transient"]:
+            d["storage"] = "GPU_Global:fp32"
+    with pytest.raises(Exception) as ei:
+        b200.invoke_toolchain(b200.generate(doc))
+    assert "libsdfgb200" in str(ei.value) or "not built" in str(ei.value)
