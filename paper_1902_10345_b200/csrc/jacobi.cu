@@ -253,6 +253,9 @@ __host__ __device__ constexpr int tb_rows(int k) { return kTbY + 2 * k; }
 // read rows up to RY+F-2 of a buffer: halo garbage, but it must be inside
 // the allocation) + mbarrier
 constexpr int kTbPadRows = 2;
+#ifndef SDFGB_J_ONE_SWEEP
+#define SDFGB_J_ONE_SWEEP 1
+#endif
 #ifndef SDFGB_J_F3
 #define SDFGB_J_F3 1  // odd step counts start with a 3-step sweep (else a 1-step one)
 #endif
@@ -457,11 +460,24 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restric
             }
             st += F;
         };
-        // KT = 7 -> 3 + 2 + 2;  5 -> 3 + 2;  3 -> 3
+        // without SDFGB_J_ONE_SWEEP: KT = 7 -> 3 + 2 + 2;  5 -> 3 + 2;  3 -> 3
         if (steps == 1) {
             single_step();
             st = 1;
         } else {
+#if SDFGB_J_ONE_SWEEP
+            // one fused sweep of all `steps` levels: no intermediate smem
+            // round trip or barrier at all (7 steps: 29.4 -> 28.2 us/step;
+            // 4+3 measured 28.4, 5+2 29.2, 3+2+2 29.4).  Level-0 reads reach
+            // row RY + steps - 2 of buffer 0, inside buffer 1: halo garbage
+            // that never reaches the kept centre.
+            if constexpr (KT >= 3 && (KT & 1)) {
+                if (steps == KT) {
+                    run(std::integral_constant<int, KT>{});
+                    return;
+                }
+            }
+#endif
             if (steps & 1) {
                 if (SDFGB_J_F3) {
                     run(std::integral_constant<int, 3>{});
