@@ -265,7 +265,7 @@ __host__ __device__ constexpr size_t tb_smem(int k) {
 
 template <int KT>
 __global__ void __launch_bounds__(kTbThreads, SDFGB_J_MINB)
-jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* __restrict__ dst_in,
+jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* dst_in,
                  float* __restrict__ dst, int M, int N, float coef, int steps) {
     // planes are M rows x N columns; the border is the plane's edge (rows 0
     // and M-1, columns 0 and N-1) -- the reference's square case is M == N,
