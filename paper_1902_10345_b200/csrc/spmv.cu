@@ -80,7 +80,9 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 #endif
 __device__ __forceinline__ float ldg_keep(const float* p, uint64_t pol) {
     float r;
-    SPMV_ASM("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+    // random 4 B gathers: allocating their lines in L1 only evicts the
+    // rowptr / b lines (no reuse across 4 M columns); 1112 -> 1094 us
+    SPMV_ASM("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
     return r;
 }
 __device__ __forceinline__ int4 ldg_stream_i4(const int32_t* p, uint64_t pol) {
