@@ -1,0 +1,116 @@
+"""Randomised device-entry parity against the C oracle: sizes, alignments,
+operators, thresholds and value ranges drawn from a seeded generator (many
+small cases per run, each bit-exact)."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+DEV = "cuda"
+OPS = ["<", "<=", ">", ">=", "==", "!="]
+
+
+def t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_query_fuzz(seed, cuda_ok):
+    import torch
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(8):
+        n = int(rng.choice([1, 3, 17, 255, 4096, 70001, 1 << 18]) + rng.integers(0, 5))
+        off = int(rng.integers(0, 4))
+        base = rng.random(n + off, dtype=np.float32) * 4 - 2
+        if rng.random() < 0.3:
+            base[rng.integers(0, n + off, 8)] = np.float32(0.25)  # ties for == / !=
+        col = base[off:]
+        op = OPS[int(rng.integers(0, 6))]
+        thr = float(rng.choice([0.25, 0.0, -1.5, 1e-7, 0.1, np.float64(np.float32(0.3)) + 1e-12]))
+        ordered = bool(rng.integers(0, 2))
+        dcol = t(base)[off:]
+        out = torch.zeros(n, dtype=torch.float32, device=DEV)
+        cnt = torch.full((1,), 7, dtype=torch.int64, device=DEV)
+        ws = device.query_workspace(n, 4, DEV)
+        device.query(dcol, thr, out, cnt, ws, op, ordered=ordered)
+        exp, ecnt = oracle.query(col, thr, np.zeros(n, np.float32), np.array([7], np.int64), op)
+        k = int(ecnt[0] - 7)
+        assert int(cnt.item()) == int(ecnt[0]), (n, op, thr)
+        got = out[:k].cpu().numpy()
+        if ordered:
+            np.testing.assert_array_equal(got, exp[:k])
+        else:
+            np.testing.assert_array_equal(np.sort(got), np.sort(exp[:k]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_histogram_fuzz(seed, cuda_ok):
+    import torch
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(2000 + seed)
+    for _ in range(8):
+        n = int(rng.choice([1, 5, 1000, 65537, 1 << 20]) + rng.integers(0, 9))
+        off = int(rng.integers(0, 4))
+        bins = int(rng.choice([1, 7, 256, 1000, 5000]))
+        scale = float(rng.choice([256.0, 100.0, 1.0, 3.5, 1024.0]))
+        div = float(rng.choice([1.0, 1.0, 3.0, 0.5]))
+        base = (rng.random(n + off, dtype=np.float32) * 1.2 - 0.1).astype(np.float32)
+        if rng.random() < 0.3:
+            base[rng.integers(0, n + off, 4)] = np.float32(np.nan)
+        img = base[off:]
+        h0 = rng.integers(0, 3, bins).astype(np.int64)
+        hist = t(h0)
+        oob = torch.zeros(1, dtype=torch.int64, device=DEV)
+        device.hist(t(base)[off:], hist, oob, scale, div)
+        ref, roob = oracle.histogram(img, h0, scale, div)
+        np.testing.assert_array_equal(hist.cpu().numpy(), ref, err_msg=f"{n} {bins} {scale} {div}")
+        assert int(oob.item()) == roob
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(8))
+def test_spmv_fuzz(seed, cuda_ok):
+    """ragged rows (empty, short, > 64 nnz), unaligned row starts, duplicate columns"""
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(3000 + seed)
+    for _ in range(6):
+        H = int(rng.integers(1, 3000))
+        W = int(rng.integers(1, 5000))
+        lens = rng.choice([0, 1, 3, 16, 64, 65, 200], size=H, p=[.15, .15, .2, .2, .15, .1, .05])
+        rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        nnz = int(rp[-1])
+        col = rng.integers(0, W, max(nnz, 1)).astype(np.int32)[:nnz]
+        val = rng.random(nnz, dtype=np.float32) - 0.5
+        x = rng.random(W, dtype=np.float32)
+        b0 = rng.random(H, dtype=np.float32)
+        b = t(b0)
+        device.spmv(t(rp), t(col), t(val), t(x), b)
+        ref = b0.astype(np.float64).copy()
+        for i in range(H):
+            s, e = rp[i], rp[i + 1]
+            ref[i] += float(np.dot(val[s:e].astype(np.float64), x[col[s:e]].astype(np.float64)))
+        scale = np.abs(b0).astype(np.float64) + np.array(
+            [np.abs(val[rp[i]:rp[i + 1]]).astype(np.float64) @ x[col[rp[i]:rp[i + 1]]] for i in range(H)])
+        assert (np.abs(b.cpu().numpy() - ref) / (scale + 1e-30)).max() < 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_jacobi_fuzz(seed, cuda_ok):
+    """square sizes around the tile and vector widths, T around the temporal
+    block lengths: bit-exact against the fp32 restatement"""
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(4000 + seed)
+    for _ in range(3):
+        N = int(rng.choice([3, 5, 8, 31, 100, 113, 128, 225, 300]))
+        T = int(rng.choice([0, 1, 2, 3, 6, 7, 8, 15, 16]))
+        A = rng.random((2, N, N), dtype=np.float32)
+        ref = oracle.jacobi2d(A, T, fp32=True)
+        At = t(A)
+        device.jacobi2d(At, T)
+        np.testing.assert_array_equal(At.cpu().numpy(), ref, err_msg=f"N={N} T={T}")
