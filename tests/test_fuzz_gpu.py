@@ -114,3 +114,32 @@ def test_jacobi_fuzz(seed, cuda_ok):
         At = t(A)
         device.jacobi2d(At, T)
         np.testing.assert_array_equal(At.cpu().numpy(), ref, err_msg=f"N={N} T={T}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_matmul_host_entry_fuzz(seed, cuda_ok):
+    """the reference-facing matmul entries on random shapes (K % 4 != 0 pads,
+    one-row / one-column panels): 3xTF32 within 1e-5 of |A||B|, float64
+    bit-exact in k order"""
+    import ctypes
+    from paper_1902_10345_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(5000 + seed)
+    for _ in range(3):
+        M, N, K = (int(v) for v in rng.integers(1, 700, 3))
+        A = rng.random((M, K)) - 0.5
+        B = rng.random((K, N)) - 0.5
+        C = np.zeros((M, N))
+        p = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        _lib.check(L.sdfgb_host_matmul(p(A), p(B), p(C), M, N, K))
+        a32, b32 = A.astype(np.float32).astype(np.float64), B.astype(np.float32).astype(np.float64)
+        err = np.abs(C - a32 @ b32) / (np.abs(a32) @ np.abs(b32) + 1e-30)
+        assert err.max() < 1e-5, (M, N, K, err.max())
+        if M * N * K <= 2_000_000:
+            C64 = np.zeros((M, N))
+            _lib.check(L.sdfgb_host_matmul_f64(p(A), p(B), p(C64), M, N, K))
+            seq = np.zeros((M, N))
+            for k in range(K):
+                seq = seq + A[:, k:k + 1] * B[k:k + 1, :]
+            np.testing.assert_array_equal(C64, seq)
