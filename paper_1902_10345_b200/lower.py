@@ -216,6 +216,22 @@ static void gen_pool_keep() {
     }
     done = true;
 }
+// Per-thread, per-device error word and pinned status word, kept across
+// runs: a run costs one memset and one 4-byte copy instead of an
+// allocation, a pageable copy and two synchronisations (reentrant: one
+// run per thread at a time, like the reference's C entry)
+static int* gen_err_dev() {
+    static thread_local int* cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (!cache[dev] && cudaMalloc((void**)&cache[dev], 16) != cudaSuccess) cache[dev] = nullptr;
+    return cache[dev];
+}
+static int* gen_status_host() {
+    static thread_local int* h = nullptr;
+    if (!h && cudaHostAlloc((void**)&h, 16, cudaHostAllocDefault) != cudaSuccess) h = nullptr;
+    return h;
+}
 template <typename T>
 static T gen_read(const T* p, cudaStream_t s) {
     T v;
@@ -1475,7 +1491,9 @@ class Lowering:
                       f"    int64_t cap_{s} = 0, ub_{s} = 0;"]
             if name in self.consumed:
                 lines += [f"    unsigned* r_{s} = nullptr;", f"    unsigned long long* q_{s} = nullptr;"]
-        lines.append("    if (cudaMallocAsync((void**)&g_err, 16, st) != cudaSuccess) return 2;")
+        lines.append("    int* g_status = gen_status_host();")
+        lines.append("    g_err = gen_err_dev();")
+        lines.append("    if (!g_err || !g_status) return 2;")
         lines.append("    cudaMemsetAsync(g_err, 0, 16, st);")
         if self.rep is not None:
             lines.append("    if (cudaMallocAsync((void**)&g_rep, @NREP@ * 8, st) != cudaSuccess) goto gen_fail;")
@@ -1539,12 +1557,10 @@ class Lowering:
             lines.append("    }")
             lines += self._dispatch(st.name, henv, "    ", prefix="st_", end="st__end")
         lines.append("st__end:;")
-        lines.append("    {")
-        lines.append("    int herr = gen_read(g_err, st);")
-        lines.append("    *status = herr;")
-        lines.append("    }")
+        lines.append("    cudaMemcpyAsync(g_status, g_err, sizeof(int), cudaMemcpyDeviceToHost, st);")
         lines.append("    gen_ce = cudaStreamSynchronize(st);")
         lines.append("    if (gen_ce != cudaSuccess) goto gen_fail;")
+        lines.append("    *status = *g_status;")
         if self.rep is not None:
             lines += ["    {", "    unsigned long long dv[@NREP@];",
                       "    gen_ce = cudaMemcpy(dv, g_rep, sizeof(dv), cudaMemcpyDeviceToHost);",
@@ -1559,12 +1575,10 @@ class Lowering:
             if name in self.consumed:
                 free += [f"    if (r_{_ident(name)}) cudaFreeAsync(r_{_ident(name)}, st);",
                          f"    if (q_{_ident(name)}) cudaFreeAsync(q_{_ident(name)}, st);"]
-        lines += free
-        lines.append("    cudaFreeAsync(g_err, st);")
-        lines.append("    return cudaStreamSynchronize(st) == cudaSuccess ? 0 : 2;")
+        lines += free  # stream-ordered: the outputs are already complete
+        lines.append("    return 0;")
         lines.append("gen_fail:")
         lines += free
-        lines.append("    if (g_err) cudaFreeAsync(g_err, st);")
         if self.rep is not None:
             lines.append("    if (g_rep) cudaFreeAsync(g_rep, st);")
         lines.append("    cudaStreamSynchronize(st);")
