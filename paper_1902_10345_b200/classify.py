@@ -285,6 +285,46 @@ def _compute_states(g: Graph) -> list:
     return [s for s in g.states if s.nodes]
 
 
+def _walk(g: Graph, start: str, until: Optional[str] = None, entry_assign: tuple = ()) -> list:
+    """States the interpreter visits from ``start`` (interpreter.py:689-709)
+    when control flow is straight-line: every transition taken is the
+    first out-transition of its state, unconditional, and assigns nothing
+    -- except the one into ``until``, which may carry ``entry_assign``.
+    Anything else (a condition, an assignment, a cycle) could run a state
+    zero or several times, so the motif kernel, which runs it once, does
+    not apply and the graph goes to the generic lowering."""
+    seq: list = []
+    cur: Optional[str] = start
+    while cur is not None and cur != until:
+        if cur in seq:
+            raise UnsupportedGraph(f"control flow revisits state '{cur}'")
+        seq.append(cur)
+        outs = g.out_transitions(cur)
+        if not outs:
+            cur = None
+            break
+        t = outs[0]
+        if t.condition != X.Num(1):
+            raise UnsupportedGraph(f"conditional transition out of state '{cur}'")
+        assigns = [(k, v) for k, v in t.assignments]
+        if assigns and not (t.dst == until and len(assigns) == 1 and assigns[0][0] == entry_assign[0]
+                            and X.same_value(assigns[0][1], entry_assign[1])):
+            raise UnsupportedGraph(f"transition out of state '{cur}' assigns symbols")
+        cur = t.dst
+    if until is not None and cur != until:
+        raise UnsupportedGraph(f"state '{until}' is not reached by straight-line control flow")
+    return seq
+
+
+def _runs_once(g: Graph, names: list) -> None:
+    """The dataflow states ``names`` run exactly once, in this order, and
+    nothing else with dataflow runs."""
+    seq = _walk(g, g.start_state)
+    got = [s for s in seq if g.state(s).nodes]
+    if got != names:
+        raise UnsupportedGraph(f"dataflow states run as {got}, not once each as {names}")
+
+
 # ----------------------------------------------------------------- histogram
 
 def match_histogram(g: Graph) -> Plan:
@@ -292,6 +332,7 @@ def match_histogram(g: Graph) -> Plan:
     if len(states) != 1:
         raise UnsupportedGraph("histogram: expects one dataflow state")
     st = states[0]
+    _runs_once(g, [st.name])
     parent = st.scope_parent()
     tops = _top_maps(st, parent)
     if len(tops) != 1:
@@ -322,6 +363,7 @@ def match_histogram(g: Graph) -> Plan:
     ke = key_edge[0]
     src = st.nodes[ke.src]
     plan = _base(g, "histogram")
+    binner = None
     if src.kind == "access" and g.data[src.data].transient:
         # two-tasklet form: binner -> bin scalar -> bump
         feeders = [e for e in st.in_edges(src.id)]
@@ -362,6 +404,11 @@ def match_histogram(g: Graph) -> Plan:
             raise UnsupportedGraph("histogram: direct subscript needs an int64 image")
         plan.motif = "histogram_int"
         plan.params.update(mode="identity")
+    if any(t is not bump and t is not binner for t in tks):
+        raise UnsupportedGraph("histogram: map body has tasklets besides the binner and the bump")
+    others = [n for i in nest.body for n in [st.nodes[i]] if n.kind not in ("tasklet", "access")]
+    if others:
+        raise UnsupportedGraph("histogram: map body has nodes besides tasklets and the bin scalar")
     imd = g.data[img]
     if len(idx) != len(imd.dims) or len(nest.order) != len(idx):
         raise UnsupportedGraph("histogram: image rank does not match the map")
@@ -383,6 +430,7 @@ def match_query(g: Graph) -> Plan:
     if len(states) != 1:
         raise UnsupportedGraph("query: expects one dataflow state")
     st = states[0]
+    _runs_once(g, [st.name])
     parent = st.scope_parent()
     tops = _top_maps(st, parent)
     if len(tops) != 1:
@@ -456,6 +504,7 @@ def match_spmv(g: Graph) -> Plan:
     if len(states) != 1:
         raise UnsupportedGraph("spmv: expects one dataflow state")
     st = states[0]
+    _runs_once(g, [st.name])
     parent = st.scope_parent()
     tops = _top_maps(st, parent)
     if len(tops) != 1:
@@ -593,6 +642,27 @@ def detect_loop(g: Graph) -> Optional[Loop]:
     return None
 
 
+def _loop_runs_once(g: Graph, loop: Loop) -> None:
+    """The guard loop is entered once from straight-line code (``v = 0`` on
+    the entering edge), its body is reached only from the guard, and the
+    exit leads straight to the end -- so the device-side T loop is the
+    whole program (interpreter.py:689-709)."""
+    _walk(g, g.start_state, until=loop.guard, entry_assign=(loop.var, X.Num(0)))
+    ins = g.in_transitions(loop.guard)
+    if len(ins) != 2 or len(g.in_transitions(loop.body)) != 1:
+        raise UnsupportedGraph("jacobi2d: guard loop is entered from more than one place")
+    outs = g.out_transitions(loop.guard)
+    if len(outs) > 2:
+        raise UnsupportedGraph("jacobi2d: guard state has more than two exits")
+    if len(outs) == 2:
+        t = outs[1]
+        if t.condition != X.Num(1) or t.assignments:
+            raise UnsupportedGraph("jacobi2d: guard exit is conditional or assigns symbols")
+        after = _walk(g, t.dst)
+        if loop.guard in after or any(g.state(s).nodes for s in after):
+            raise UnsupportedGraph("jacobi2d: dataflow or a loop after the time loop")
+
+
 def _sum_chain(n: ast.AST) -> Optional[list]:
     """Names of a left-leaning ``((a + b) + c) + ...`` chain, in order."""
     if isinstance(n, ast.Name):
@@ -610,6 +680,7 @@ def match_jacobi(g: Graph) -> Plan:
     others = [s for s in g.states if s.name != loop.body and s.nodes]
     if others:
         raise UnsupportedGraph("jacobi2d: dataflow outside the loop body")
+    _loop_runs_once(g, loop)
     st = g.state(loop.body)
     parent = st.scope_parent()
     tops = _top_maps(st, parent)
@@ -729,10 +800,7 @@ def match_matmul(g: Graph) -> Plan:
         ist, inest, itk, istmt, _ = init
         if _const(istmt.value) != 0:
             raise UnsupportedGraph("matmul: init must write the sum identity 0")
-        tr = g.out_transitions(ist.name)
-        if len(tr) != 1 or tr[0].dst != mult[0].name or tr[0].assignments or tr[0].condition != X.Num(1) \
-                or g.start_state != ist.name or g.out_transitions(mult[0].name):
-            raise UnsupportedGraph("matmul: expects start=init -> multiply -> end")
+        _runs_once(g, [ist.name, mult[0].name])
         st, nest, t, top = mult
         s, reads = _mm_core(g, st, nest, t)
         writes = _exit_write(st, t, s.targets[0].id)
@@ -746,6 +814,7 @@ def match_matmul(g: Graph) -> Plan:
     elif len(states) == 1:
         # raw form: map -> tmp[i, j, k] -> Reduce(axes=[2], sum) -> C
         st = states[0]
+        _runs_once(g, [st.name])
         parent = st.scope_parent()
         tops = _top_maps(st, parent)
         if len(tops) != 1:

@@ -395,7 +395,30 @@ def custom_wcr_cases():
     save_case("maxabs", "n200", g, {"x": rng.uniform(-1, 1, 200), "out": np.full(7, 0.5)}, {})
 
 
-if __name__ == "__main__":
+def control_flow_cases():
+    """Motifs under non-trivial control flow: a histogram run
+    three times by a guard loop, a query behind a symbol condition.  The
+    motif kernels run a state once, so these must take the generic
+    lowering, whose state machine follows the interpreter's."""
+    g = M.histogram_looped(3)
+    save_graph("histogram_looped", g)
+    rng = np.random.default_rng(5)
+    img = f32(rng.random((4, 4), dtype=F32))
+    save_case("histogram_looped", "r3", g, {"img": img, "hist": np.zeros(256, np.int64)}, {"H": 4, "W": 4})
+    q = M.query_cond()
+    save_graph("query_cond", q)
+    for case, N in {"n16": 16, "n8": 8}.items():
+        col = f32(rng.random(N, dtype=F32))
+        save_case("query_cond", case, q,
+                  {"col": col, "thr": np.array([0.5]), "out_vals": np.zeros(N),
+                   "count": np.zeros(1, np.int64)}, {"N": N})
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    for fn in sys.argv[1:]:
+        globals()[fn]()
+elif __name__ == "__main__":
+    control_flow_cases()
     xform_fixture_cases()
     oob_cases()
     custom_wcr_cases()

@@ -58,6 +58,34 @@ def histogram(bins: int = 256, name: str = "histogram") -> Sdfg:
     return g
 
 
+def _wrap_in_loop(g: Sdfg, first: str, last: str, reps: str) -> None:
+    """Put the straight-line states ``first .. last`` in a guard loop of
+    ``reps`` trips (the motif then runs several times: ADVICE r1)."""
+    init = g.add_state("loop_init", is_start=True)
+    guard = g.add_state("loop_guard")
+    g.add_transition(init, guard, assignments=[("r", "0")])
+    g.add_transition(guard, g.state(first), condition=f"r < {reps}")
+    g.add_transition(g.state(last), guard, assignments=[("r", "r + 1")])
+
+
+def histogram_looped(reps: int = 3) -> Sdfg:
+    """The binned histogram inside a ``reps``-trip guard loop: the counts
+    accumulate ``reps`` times (hist_out = hist_in + reps * counts)."""
+    g = histogram(name="histogram_looped")
+    _wrap_in_loop(g, "binning", "binning", str(reps))
+    g.finalize()
+    return g
+
+
+def query_cond() -> Sdfg:
+    """The query behind a condition on a symbol: it runs only when N > 8."""
+    g = query("<", name="query_cond")
+    pre = g.add_state("pre", is_start=True)
+    g.add_transition(pre, g.state("filter"), condition="N > 8")
+    g.finalize()
+    return g
+
+
 def histogram_int() -> Sdfg:
     """The gallery's integer-image variant (gallery.py:354-386)."""
     return gallery.fixture("histogram").sdfg

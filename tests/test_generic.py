@@ -25,7 +25,9 @@ from paper_1902_10345_b200.lower import LoweringError, lower
 GALLERY = ["branching", "fibonacci", "histogram", "indirection", "laplace", "mandelbrot", "matmul", "query",
            "spmv"]
 MOTIF_GRAPHS = ["histogram", "histogram_int", "query", "query_gallery", "spmv", "jacobi2d", "laplace1d",
-                "matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "axpy", "maxabs", "oob"]
+                "matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "axpy", "maxabs", "oob",
+                # motifs under loops / conditions: the motif kernels do not apply
+                "histogram_looped", "query_cond"]
 # the reference's transformation micro-programs (tests/xform_fixtures.py)
 XFORM = sorted(os.path.basename(p)[:-len(".sdfg.json")]
                for p in glob.glob(os.path.join(os.path.dirname(graph_path("x")), "xf_*.sdfg.json")))
@@ -37,7 +39,8 @@ UNORDERED_SUMS = {"matmul", "matmul_raw", "matmul_tiled", "matmul_chain", "gal_m
                   "x_matmul_MapTiling", "xf_tiled_matmul", "x_xf_tiled_matmul_MapTiling"}
 STREAM_OUT = {"gal_query": ("out_vals", "count"), "query": ("out_vals", "count"),
               "query_gallery": ("out_vals", "count"), "x_query_LocalStream": ("out_vals", "count"),
-              "x_query_MapTiling": ("out_vals", "count"), "x_query_RedundantArray": ("out_vals", "count")}
+              "x_query_MapTiling": ("out_vals", "count"), "x_query_RedundantArray": ("out_vals", "count"),
+              "query_cond": ("out_vals", "count")}
 
 
 def _doc(name):

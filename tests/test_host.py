@@ -14,7 +14,7 @@ from conftest import REPO, graph_path, load_cases, reference_available
 
 import paper_1902_10345_b200 as b200
 from paper_1902_10345_b200 import _lib, expr as X
-from paper_1902_10345_b200.classify import UnsupportedGraph, classify
+from paper_1902_10345_b200.classify import UnsupportedGraph, classify, match_histogram
 from paper_1902_10345_b200.graph import load
 
 needs_ref = pytest.mark.skipif(not reference_available(), reason="reference not mounted")
@@ -113,6 +113,34 @@ def test_classified_parameters():
     assert str(j.params["steps"]) == "T" and str(j.params["N"]) == "N"
     s = classify(load(graph_path("spmv")))
     assert s.pointer_args[0] == ("A_row", "int64") and s.symbol_args == ["H", "W", "nnz"]
+
+
+@pytest.mark.parametrize("name", ["histogram_looped", "query_cond"])
+def test_motif_under_control_flow_is_not_a_motif(name):
+    """A motif state in a guard loop or behind a condition may run zero or
+    several times; the motif kernel runs it once, so the classifier must
+    refuse it and the generic lowering (a state machine) runs it."""
+    with pytest.raises(UnsupportedGraph, match="control flow|conditional|revisits|assigns"):
+        classify(load(graph_path(name)))
+    doc = json.load(open(graph_path(name)))
+    for d in doc["data"]:
+        if not d["transient"]:
+            d["storage"] = "GPU_Global:native"
+    code = b200.generate(doc)
+    assert code.plan is None and code.lowered is not None
+
+
+def test_histogram_with_extra_body_tasklet_is_not_a_motif():
+    doc = json.load(open(graph_path("histogram")))
+    st = doc["states"][0]
+    extra = json.loads(json.dumps([n for n in st["nodes"] if n["kind"] == "tasklet" and n["name"] == "binner"][0]))
+    extra["name"] = "spare"
+    st["nodes"].append(extra)
+    me = [i for i, n in enumerate(st["nodes"]) if n["kind"] == "map_entry"][0]
+    st["edges"].append({"src": me, "src_conn": None, "dst": len(st["nodes"]) - 1, "dst_conn": None,
+                        "memlet": {"empty": True}})
+    with pytest.raises(UnsupportedGraph, match="besides the binner"):
+        match_histogram(load(doc))
 
 
 def test_non_motif_programs_take_the_generic_lowering():
