@@ -67,6 +67,19 @@ int sdfgb_device_count(int* count);
 /* Pinned host memory for zero-staging H2D/D2H in the host entries. */
 int sdfgb_host_alloc(void** ptr, size_t bytes);
 int sdfgb_host_free(void* ptr);
+/* Status of the last host entry (sdfgb_host_*) called on this thread: the
+ * per-graph shims keep the reference's `void <name>(...)` signature
+ * (codegen.py:839-846), so their callers read the status here afterwards. */
+int sdfgb_last_status(void);
+/* Host threads the host entries convert and stage with (SDFGB_HOST_THREADS,
+ * default: all hardware threads). */
+int sdfgb_host_threads(void);
+/* The host entries' staging conversions (no device needed; CPU tests):
+ * kind 0 f64->f32 round to nearest, 1 f64->f32 toward -inf, 2 f64->f32
+ * returning 1 iff every element round-trips, 3 f32->f64, 4 int64->int32
+ * returning the count outside [lo, hi), 5 returns 1 iff int64 src is
+ * non-decreasing (dst unused). */
+int64_t sdfgb_host_convert(int kind, const void* src, void* dst, int64_t n, int64_t lo, int64_t hi);
 
 /* ------------------------------------------------------ device entries */
 
@@ -220,8 +233,12 @@ int sdfgb_gemm_f32_mgpu(const float* A_piece, int64_t a_rows, const float* B_pie
 
 /* -------------------------------------------------------- host entries
  * Drop-in for CompiledSdfg._fn(*ptrs, *syms) (codegen.py:886): host
- * buffers in the reference's types; H2D, kernel(s), D2H, synchronous.
- * precision: 0 = fp32 on device (BASELINE), 1 = native (f64 / i64).      */
+ * buffers in the reference's types (pageable is fine); staged through a
+ * pinned ring by host threads, kernel(s), copied back; synchronous.
+ * precision: 0 = fp32 on device (BASELINE: inputs rounded to nearest fp32),
+ * 1 = native (the reference's float64 / int64 results; histogram with
+ * power-of-two binning and the query still ship 4 B per element where that
+ * is lossless).  Each records its status for sdfgb_last_status().        */
 #define SDFGB_PREC_FP32 0
 #define SDFGB_PREC_NATIVE 1
 

@@ -136,37 +136,39 @@ void orc_spmv_f32(const int32_t* rowptr, const int32_t* col, const float* val,
  * reference evaluates left to right: coef * ((((t0 + t1) + t2) + t3) + t4)
  * (tasklets.py:430-444).  ``di/dj`` give the term order.
  * ------------------------------------------------------------------- */
-void orc_jacobi2d_f64(double* A, int64_t N, int64_t T, double coef,
-                      const int32_t* di, const int32_t* dj, int32_t nterms)
-{
-    for (int64_t t = 0; t < T; ++t) {
-        const double* src = A + (t % 2) * N * N;
-        double* dst = A + ((t + 1) % 2) * N * N;
-        for (int64_t i = 1; i <= N - 2; ++i)
-            for (int64_t j = 1; j <= N - 2; ++j) {
-                double s = src[(i + di[0]) * N + (j + dj[0])];
-                for (int32_t k = 1; k < nterms; ++k)
-                    s = s + src[(i + di[k]) * N + (j + dj[k])];
-                dst[i * N + j] = coef * s;
-            }
-    }
+#define JACOBI_ORACLE(NAME, T)                                                        \
+void NAME(T* A, int64_t N, int64_t TT, T coef, const int32_t* di, const int32_t* dj,    \
+          int32_t nterms)                                                               \
+{                                                                                       \
+    int64_t off[9];                                                                     \
+    for (int32_t k = 0; k < nterms && k < 9; ++k) off[k] = (int64_t)di[k] * N + dj[k];  \
+    for (int64_t t = 0; t < TT; ++t) {                                                  \
+        const T* src = A + (t % 2) * N * N;                                             \
+        T* dst = A + ((t + 1) % 2) * N * N;                                             \
+        /* rows are independent within a step: threads change no rounding */          \
+        _Pragma("omp parallel for schedule(static) if (N > 256)")                       \
+        for (int64_t i = 1; i <= N - 2; ++i) {                                          \
+            const T* r = src + i * N;                                                   \
+            T* d = dst + i * N;                                                         \
+            if (nterms == 5) {  /* same left-to-right order, unrolled */               \
+                const int64_t o0 = off[0], o1 = off[1], o2 = off[2], o3 = off[3],      \
+                              o4 = off[4];                                              \
+                for (int64_t j = 1; j <= N - 2; ++j)                                    \
+                    d[j] = coef * ((((r[j + o0] + r[j + o1]) + r[j + o2])               \
+                                    + r[j + o3]) + r[j + o4]);                          \
+            } else {                                                                    \
+                for (int64_t j = 1; j <= N - 2; ++j) {                                  \
+                    T s = r[j + off[0]];                                                \
+                    for (int32_t k = 1; k < nterms; ++k) s = s + r[j + off[k]];        \
+                    d[j] = coef * s;                                                    \
+                }                                                                       \
+            }                                                                           \
+        }                                                                               \
+    }                                                                                   \
 }
 
-void orc_jacobi2d_f32(float* A, int64_t N, int64_t T, float coef,
-                      const int32_t* di, const int32_t* dj, int32_t nterms)
-{
-    for (int64_t t = 0; t < T; ++t) {
-        const float* src = A + (t % 2) * N * N;
-        float* dst = A + ((t + 1) % 2) * N * N;
-        for (int64_t i = 1; i <= N - 2; ++i)
-            for (int64_t j = 1; j <= N - 2; ++j) {
-                float s = src[(i + di[0]) * N + (j + dj[0])];
-                for (int32_t k = 1; k < nterms; ++k)
-                    s = s + src[(i + di[k]) * N + (j + dj[k])];
-                dst[i * N + j] = coef * s;
-            }
-    }
-}
+JACOBI_ORACLE(orc_jacobi2d_f64, double)
+JACOBI_ORACLE(orc_jacobi2d_f32, float)
 
 /* ---------------------------------------------------------------------
  * Matrix multiplication after MapReduceFusion (library.py:461-554): an
@@ -179,6 +181,8 @@ void orc_matmul_f64(const double* A, const double* B, double* C,
                     int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1)
 {
     (void)M;
+    /* rows are independent: threads change no rounding */
+#pragma omp parallel for schedule(dynamic, 4)
     for (int64_t i = r0; i < r1; ++i) {
         double* c = C + i * N;
         for (int64_t j = 0; j < N; ++j) c[j] = 0.0;
@@ -195,6 +199,7 @@ void orc_matmul_f32in_f64acc(const float* A, const float* B, double* C,
                              int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1)
 {
     (void)M;
+#pragma omp parallel for schedule(dynamic, 4)
     for (int64_t i = r0; i < r1; ++i) {
         double* c = C + (i - r0) * N;
         for (int64_t j = 0; j < N; ++j) c[j] = 0.0;

@@ -132,3 +132,34 @@ def matmul(A, B, rows=None):
     C = np.zeros((M, N), np.float64)
     lib().orc_matmul_f64(_p(a), _p(b), _p(C), M, N, K, r0, r1)
     return C[r0:r1]
+
+
+# ------------------------------------------------ the reference's own C
+
+REF_DIR = os.path.join(HERE, "_ref")
+
+
+def ref_available(key: str = None) -> bool:
+    man = os.path.join(REF_DIR, "manifest.json")
+    if not os.path.exists(man):
+        return False
+    if key is None:
+        return True
+    import json
+    return key in json.load(open(man))
+
+
+def ref_call(key: str, arrays: dict, syms: dict) -> dict:
+    """Call the reference's own generated C (oracle/_ref, built by
+    make_ref.py from codegen.generate + invoke_toolchain) the way
+    CompiledSdfg.run does (codegen.py:875-887); returns the buffers."""
+    import json
+    m = json.load(open(os.path.join(REF_DIR, "manifest.json")))[key]
+    L = ctypes.CDLL(os.path.join(REF_DIR, m["lib"]))
+    fn = getattr(L, m["entry"])
+    fn.restype = None
+    bufs = []
+    for name, bt in m["pointer_args"]:
+        bufs.append(np.ascontiguousarray(arrays[name], dtype=np.int64 if bt == "int64" else np.float64).copy())
+    fn(*[ctypes.c_void_p(b.ctypes.data) for b in bufs], *[ctypes.c_int64(syms[s]) for s in m["symbol_args"]])
+    return {n: b for (n, _), b in zip(m["pointer_args"], bufs)}

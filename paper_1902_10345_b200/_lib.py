@@ -34,6 +34,9 @@ SIGNATURES = {
     "sdfgb_device_count": (_INT, [_P]),
     "sdfgb_host_alloc": (_INT, [_P, _SZ]),
     "sdfgb_host_free": (_INT, [_P]),
+    "sdfgb_last_status": (_INT, []),
+    "sdfgb_host_threads": (_INT, []),
+    "sdfgb_host_convert": (_I64, [_INT, _P, _P, _I64, _I64, _I64]),
     "sdfgb_hist_f32": (_INT, [_P, _I64, _F64, _F64, _P, _I64, _P, _P]),
     "sdfgb_hist_f64": (_INT, [_P, _I64, _F64, _F64, _P, _I64, _P, _P]),
     "sdfgb_hist_i64": (_INT, [_P, _I64, _P, _I64, _P, _P]),

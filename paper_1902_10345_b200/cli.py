@@ -5,7 +5,7 @@ Mirrors the reference CLI's ``run`` and ``codegen`` subcommands (cli.py:120-
 with the same exit codes (0 ok, 1 validation, 2 usage, 3 runtime) and
 ``--format json``:
 
-    run GRAPH [--input TENSORS.json] [--journal J.json] [--precision fp32|native]
+    run GRAPH [--input TENSORS.json] [--journal J.json] [--precision native|fp32]
               [--stream-order any|fifo]
         marks the program for the GPU (GPUTransformMap's marker), dispatches it
         to a motif kernel or the generic lowering, runs it, and prints an
@@ -322,7 +322,7 @@ def build_parser() -> argparse.ArgumentParser:
                           ("codegen", cmd_codegen, "emit the B200 program")):
         s = sub.add_parser(name, help=hlp)
         s.add_argument("graph")
-        s.add_argument("--precision", choices=("fp32", "native"), default="fp32")
+        s.add_argument("--precision", choices=("fp32", "native"), default="native")
         s.add_argument("--stream-order", choices=("any", "fifo"), default="any")
         if name == "run":
             s.add_argument("--input", help="JSON tensor file with arrays and symbols")

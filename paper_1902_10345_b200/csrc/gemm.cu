@@ -770,30 +770,11 @@ extern "C" size_t sdfgb_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
     return 2 * r((size_t)M * K * 4) + 2 * r((size_t)N * K * 4);
 }
 
-extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
-                              void* ws, size_t ws_bytes, void* stream) {
-    using namespace sdfgb;
-    if (M < 0 || N < 0 || K < 0 || (M * N > 0 && !C))
-        return set_error(SDFGB_ERR_INVALID, "gemm: bad arguments");
-    if (M == 0 || N == 0) return SDFGB_OK;
-    cudaStream_t s = as_stream(stream);
-    if (K == 0) {  // init_C state only: C = 0 (library.py:541-554)
-        SDFGB_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
-        return SDFGB_OK;
-    }
-    if (K % 4 != 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
-        return set_error(SDFGB_ERR_INVALID, "gemm: K must be a multiple of 4 (TMA row stride)");
-    if (!A || !B || !ws || ws_bytes < sdfgb_gemm_workspace_bytes(M, N, K))
-        return set_error(SDFGB_ERR_WORKSPACE, "gemm: workspace too small");
-    auto r = [](size_t b) { return (b + 255) / 256 * 256; };
-    uint8_t* w = static_cast<uint8_t*>(ws);
-    float* Ahi = reinterpret_cast<float*>(w);
-    float* Alo = reinterpret_cast<float*>(w + r((size_t)M * K * 4));
-    float* Bhi = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4));
-    float* Blo = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4) + r((size_t)N * K * 4));
+namespace sdfgb {
 
-    split_rows_kernel<<<num_sms() * 8, 256, 0, s>>>(A, Ahi, Alo, M * K);
-    SDFGB_LAUNCHED("split_rows_kernel");
+// B (K x N, row-major) -> Bt_hi / Bt_lo (N x K, K-major): the 3xTF32 split of
+// the right operand, done once per B (the host entry's row panels share it)
+int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, cudaStream_t s) {
     if (N % 4 == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0) {  // K % 4 == 0 already
         dim3 tg((unsigned)((N + 63) / 64), (unsigned)((K + 63) / 64));
         split_transpose64_kernel<<<tg, 256, 0, s>>>(B, Bhi, Blo, K, N);
@@ -803,7 +784,14 @@ extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t 
         split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bhi, Blo, K, N);
         SDFGB_LAUNCHED("split_transpose_kernel");
     }
+    return SDFGB_OK;
+}
 
+// C = A x B with B already split (gemm_split_b); Ahi / Alo hold M x K each
+int gemm_f32_presplit(const float* A, const float* Bhi, const float* Blo, float* C, int64_t M, int64_t N,
+                      int64_t K, float* Ahi, float* Alo, cudaStream_t s) {
+    split_rows_kernel<<<num_sms() * 8, 256, 0, s>>>(A, Ahi, Alo, M * K);
+    SDFGB_LAUNCHED("split_rows_kernel");
     CUtensorMap mAhi, mAlo, mBhi, mBlo;
     SDFGB_TRY(make_kmajor_map(&mAhi, Ahi, M, K));
     SDFGB_TRY(make_kmajor_map(&mAlo, Alo, M, K));
@@ -844,6 +832,33 @@ extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t 
         SDFGB_LAUNCHED("gemm_3xtf32_kernel");
     }
     return SDFGB_OK;
+}
+
+}  // namespace sdfgb
+
+extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
+                              void* ws, size_t ws_bytes, void* stream) {
+    using namespace sdfgb;
+    if (M < 0 || N < 0 || K < 0 || (M * N > 0 && !C))
+        return set_error(SDFGB_ERR_INVALID, "gemm: bad arguments");
+    if (M == 0 || N == 0) return SDFGB_OK;
+    cudaStream_t s = as_stream(stream);
+    if (K == 0) {  // init_C state only: C = 0 (library.py:541-554)
+        SDFGB_CUDA(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
+        return SDFGB_OK;
+    }
+    if (K % 4 != 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+        return set_error(SDFGB_ERR_INVALID, "gemm: K must be a multiple of 4 (TMA row stride)");
+    if (!A || !B || !ws || ws_bytes < sdfgb_gemm_workspace_bytes(M, N, K))
+        return set_error(SDFGB_ERR_WORKSPACE, "gemm: workspace too small");
+    auto r = [](size_t b) { return (b + 255) / 256 * 256; };
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    float* Ahi = reinterpret_cast<float*>(w);
+    float* Alo = reinterpret_cast<float*>(w + r((size_t)M * K * 4));
+    float* Bhi = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4));
+    float* Blo = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4) + r((size_t)N * K * 4));
+    SDFGB_TRY(gemm_split_b(B, Bhi, Blo, K, N, s));
+    return gemm_f32_presplit(A, Bhi, Blo, C, M, N, K, Ahi, Alo, s);
 }
 
 extern "C" int sdfgb_gemm_f32_simt(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,

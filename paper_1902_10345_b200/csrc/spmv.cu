@@ -176,3 +176,10 @@ extern "C" int sdfgb_spmv_csr_f64(const int64_t* rowptr, const int64_t* col, con
                                   const double* x, double* b, int64_t H, void* stream) {
     return sdfgb::launch_spmv<int64_t, double>(rowptr, col, val, x, b, H, stream);
 }
+
+// native precision with int32 indices (the host entry narrows the int64
+// index arrays losslessly when nnz and W fit): same kernel, half the index bytes
+int sdfgb::spmv_csr_f64_i32(const int32_t* rowptr, const int32_t* col, const double* val, const double* x,
+                            double* b, int64_t H, cudaStream_t s) {
+    return sdfgb::launch_spmv<int32_t, double>(rowptr, col, val, x, b, H, s);
+}

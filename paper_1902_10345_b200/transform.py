@@ -39,7 +39,7 @@ def build_rule(engine, matching, ir):
     class GPUTransformMap(engine.Transformation):
         name = RULE_NAME
         strict = False
-        default_params = {"precision": "fp32", "stream_order": "any"}
+        default_params = {"precision": "native", "stream_order": "any"}
 
         def expressions(self):
             return [matching.Pattern([matching.PatternNode("map", (ir.MapEntry,))])]
@@ -84,7 +84,7 @@ def build_rule(engine, matching, ir):
                            for c in plan.roles.values())
 
         def apply(self, sdfg, state, match, params):
-            prec = params.get("precision", "fp32")
+            prec = params.get("precision", "native")
             if prec not in PRECISIONS:
                 raise ValueError(f"precision must be one of {PRECISIONS}, not '{prec}'")
             order = params.get("stream_order", "any")

@@ -223,14 +223,14 @@ class TestGPUTransformMapInReference:
     def test_apply_marks_storage_and_journals_precision(self):
         from sdfg.rewriting import apply_transformation, find_matches
         g = self._builders()["query"]()
-        g2, entry = apply_transformation(g, find_matches(g, "GPUTransformMap")[0], {"precision": "native"})
+        g2, entry = apply_transformation(g, find_matches(g, "GPUTransformMap")[0], {"precision": "fp32"})
         assert entry["transformation"] == "GPUTransformMap"
-        assert entry["params"] == {"precision": "native"}
-        assert g2.data["col"].storage == "GPU_Global:native"
+        assert entry["params"] == {"precision": "fp32"}  # non-default parameters are journaled
+        assert g2.data["col"].storage == "GPU_Global:fp32"
         assert g.data["col"].storage == "heap"  # input graph untouched (engine.py:195)
         assert find_matches(g2, "GPUTransformMap") == []  # not re-applicable
         code = b200.generate(g2)
-        assert code.precision == "native" and code.plan.motif == "query"
+        assert code.precision == "fp32" and code.plan.motif == "query"
 
     def test_marked_graph_stays_valid_for_the_interpreter(self):
         from sdfg.interpreter import run
@@ -249,7 +249,7 @@ class TestGPUTransformMapInReference:
         g = self._builders()["jacobi2d"]()
         g2, entry = apply_transformation(g, find_matches(g, "GPUTransformMap")[0])
         g3 = replay_journal(g, [entry])
-        assert g3.data["A"].storage == g2.data["A"].storage == "GPU_Global:fp32"
+        assert g3.data["A"].storage == g2.data["A"].storage == "GPU_Global:native"
 
     def test_hot_path_transformations_keep_the_motif(self):
         """a9: MapTiling / LocalStorage / MapExpansion keep the classification."""
@@ -284,3 +284,38 @@ def test_missing_native_library_fails_loudly(tmp_path, monkeypatch):
     with pytest.raises(Exception) as ei:
         b200.invoke_toolchain(b200.generate(doc))
     assert "libsdfgb200" in str(ei.value) or "not built" in str(ei.value)
+
+
+# ------------------------------------------- the reference's own toolchain
+
+@needs_ref
+@pytest.mark.parametrize("name", ["histogram", "query", "spmv", "jacobi2d", "matmul"])
+def test_reference_toolchain_builds_and_calls_the_shim(name, tmp_path):
+    """The reference's UNMODIFIED invoke_toolchain + CompiledSdfg (codegen.py:
+    866-913) take the B200 GeneratedB200Code as they take their own: cc
+    compiles its source, ctypes binds ``getattr(lib, code.name)`` and
+    ``run`` calls it with (*ptrs, *int64 syms).  Without a device the entry
+    reports SDFGB_ERR_CUDA through sdfgb_last_status() instead of crashing."""
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from sdfg import codegen as ref_codegen
+    code = b200.generate(graph_path(name), require_marked=False)
+    prog = ref_codegen.invoke_toolchain(code, flags=b200.dispatch.shim_link_flags(), workdir=str(tmp_path))
+    case = load_cases(name)[0]
+    prog.run(case.inputs, case.symbols)
+    L = _lib.load()
+    status = L.sdfgb_last_status()
+    try:
+        import torch
+        have_gpu = torch.cuda.is_available()
+    except Exception:
+        have_gpu = False
+    if not have_gpu:
+        assert status == _lib.ERR_CUDA
+        assert b"CUDA" in L.sdfgb_last_error() or b"cuda" in L.sdfgb_last_error()
+
+
+def test_shim_source_has_the_reference_signature():
+    for name in ("histogram", "query", "spmv", "jacobi2d", "matmul", "histogram_int"):
+        code = b200.generate(graph_path(name), require_marked=False)
+        assert code.signature() + " {" in code.source
+        assert "sdfgb_host_" in code.source
