@@ -513,8 +513,292 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* dst_in,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Strip streaming (the default temporal-blocking kernel).  One launch still
+// advances F (odd) steps, but the unit of work is a WARP, not a CTA tile:
+// a warp owns a 128-column strip (112 kept + 8 halo columns each side) of
+// H output rows and streams the strip's H + 2F input rows top to bottom.
+// Input rows arrive by TMA (128 x 3-row boxes, zero-filled outside the
+// plane) into a per-warp 4-stage shared-memory ring -- the next three
+// stages are in flight while one is consumed -- and every level 1..F of the
+// sweep is computed in registers from a 3-row window of the level below
+// (same slot rotation as jacobi_tb_kernel: row r of level k in slot
+// (r + k) mod 3, so at input row p every level writes slot p mod 3).
+//
+// Why: the tile kernel's warps each recompute a shrinking cone of
+// 2(F-k) rows per level for a 13-row band, 1.86 computed points per kept
+// point at F = 7; a warp that streams 256 rows recomputes 2.3 % in rows,
+// 1.14x in columns (16 halo of 128).  The kernel is instruction-issue
+// bound, so recomputation is time.
+//
+// Borders: level k of a launch from plane p holds state t + k, which lives
+// in plane p ^ (k & 1); the reference never writes a plane's border, so a
+// level's border rows / columns are re-imposed from that plane.  Values
+// outside the plane are garbage that only ever feeds border points.
+//   * border rows: level k reaches plane row 0 only at input rows p <= F+k
+//     (the unrolled prologue, where the test is on compile-time p, k) and
+//     row M-1 only in the last 2F input rows (a checked tail loop); the
+//     steady-state loop carries no row test.
+//   * border columns (the first / last strip only): both planes' border
+//     column over the strip's rows is staged in shared memory once, and a
+//     row step reads its F-1 values before computing, off the dependency
+//     chain of the levels.
+constexpr int kSpWarps = 4, kSpStages = 6, kSpRX = 128, kSpPad = 8, kSpX = kSpRX - 2 * kSpPad;
+constexpr int kSpStageF = 3 * kSpRX;  // floats per stage (3 rows)
+// per warp: the TMA ring, then [plane 0/1][rows] of its border column
+// (rows rounded to 16: every warp's ring stays 128 B aligned for TMA)
+__host__ __device__ constexpr int sp_rows(int nrows) { return (nrows + 15) / 16 * 16; }
+__host__ __device__ constexpr int sp_warp_floats(int nrows) { return kSpStages * kSpStageF + 2 * sp_rows(nrows); }
+__host__ __device__ constexpr size_t sp_smem(int nrows) {
+    return (size_t)kSpWarps * sp_warp_floats(nrows) * 4 + kSpWarps * kSpStages * 8;
+}
+
+template <int F>
+__global__ void __launch_bounds__(kSpWarps * 32, 4)
+jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* src, const float* dst_in,
+                    float* dst, int M, int N, int ntiles, int nstrips, int nwarps, float coef) {
+    extern __shared__ __align__(1024) float sp_smem_f[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = blockIdx.x * kSpWarps + warp;
+    if (g >= nwarps) return;  // warp-uniform; warps never synchronise with each other
+    const int strip = g % nstrips, tile = g / nstrips;
+    // tiles split the rows evenly (every tile >= 2F+2 rows, so only a
+    // tile's checked tail can meet plane row M-1 and its prologue row 0)
+    const int y0 = (int)((int64_t)tile * M / ntiles), ye = (int)((int64_t)(tile + 1) * M / ntiles);
+    const int H = (M + ntiles - 1) / ntiles;  // the tallest tile (smem sizing)
+    const int gx0 = strip * kSpX - kSpPad, gx = gx0 + 4 * lane;
+    const int nrows = (ye - y0) + 2 * F;  // input rows y0-F .. ye-1+F
+    const int RP = sp_rows(H + 2 * F);  // border-column rows per (plane, side), as sized on the host
+    float* ring = sp_smem_f + warp * (kSpStages * kSpStageF + 2 * RP);
+    float* bcol = ring + kSpStages * kSpStageF;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sp_smem_f + kSpWarps * (kSpStages * kSpStageF + 2 * RP)) +
+                     warp * kSpStages;
+    const int nst = (nrows + 2) / 3;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kSpStages; ++s) mbar_init(bars + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+        for (int s = 0; s < kSpStages; ++s)
+            if (s < nst) {
+                mbar_expect_tx(bars + s, kSpStageF * 4);
+                tma_load_2d(ring + s * kSpStageF, &src_map, bars + s, gx0, y0 - F + 3 * s);
+            }
+    }
+    // a strip holds at most one border column (the host sends planes
+    // narrower than two strips to the one-step kernel)
+    const bool colb = gx0 <= 0 || gx0 + kSpRX - 1 >= N - 1;
+    if (colb) {  // both planes' border column over the strip's input rows
+        const int c = gx0 <= 0 ? 0 : N - 1;
+        for (int i = lane; i < nrows; i += 32) {
+            const int r = y0 - F + i;
+            const bool in = r >= 0 && r < M;
+            const int64_t o = (int64_t)r * N + c;
+            bcol[i] = in ? src[o] : 0.f;
+            bcol[RP + i] = in ? dst_in[o] : 0.f;
+        }
+    }
+    __syncwarp();
+
+    auto calc = [&](const float4& nq, const float4& cq, const float4& sq) -> float4 {
+        const float lft = __shfl_up_sync(0xffffffffu, cq.w, 1);
+        const float rgt = __shfl_down_sync(0xffffffffu, cq.x, 1);
+        const float cc[4] = {cq.x, cq.y, cq.z, cq.w};
+        const float nn[4] = {nq.x, nq.y, nq.z, nq.w};
+        const float ss[4] = {sq.x, sq.y, sq.z, sq.w};
+        const float ww[4] = {lft, cq.x, cq.y, cq.z};
+        const float ee[4] = {cq.y, cq.z, cq.w, rgt};
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float acc = __fadd_rn(cc[j], nn[j]);
+            acc = __fadd_rn(acc, ss[j]);
+            acc = __fadd_rn(acc, ww[j]);
+            acc = __fadd_rn(acc, ee[j]);
+            o[j] = __fmul_rn(coef, acc);
+        }
+        return make_float4(o[0], o[1], o[2], o[3]);
+    };
+    // level k's border row r (0 or M-1) from plane p ^ (k & 1).  gx and N
+    // are multiples of 4: a lane's four columns are all inside the plane or
+    // all outside; column 0 is a lane's .x, column N-1 a lane's .w
+    auto fix_row = [&](int k, int r, float4& v) {
+        if (gx >= 0 && gx < N) v = *reinterpret_cast<const float4*>(((k & 1) ? dst_in : src) + (int64_t)r * N + gx);
+    };
+    const bool cw = gx == 0, ce = gx == N - 4;
+
+    auto sweep = [&](auto colb_tag) {
+        constexpr bool COLB = decltype(colb_tag)::value;
+        float4 w[F][3];
+#pragma unroll
+        for (int k = 0; k < F; ++k)
+#pragma unroll
+            for (int u = 0; u < 3; ++u) w[k][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+        // input row p (plane row y0 - F + p): level k computes row y0-F+p-k,
+        // valid once p >= 2k; level F (p >= 2F) is output row y0 + p - 2F.
+        // MODE 0: steady state; 1: prologue (PRO = p, compile time); 2: tail
+        // (rows may reach M-1)
+        auto step = [&](auto u_tag, int p, auto pro_tag, auto mode_tag) {
+            constexpr int u = decltype(u_tag)::value;  // p mod 3
+            constexpr int PRO = decltype(pro_tag)::value;
+            constexpr int MODE = decltype(mode_tag)::value;
+            constexpr int sn = (u + 1) % 3, sc = (u + 2) % 3;
+            const int it = p / 3;
+            const int slot = it % kSpStages, pslot = (it + kSpStages - 1) % kSpStages;
+            float* stage = ring + slot * kSpStageF;
+            const float* prev = ring + pslot * kSpStageF;
+            if constexpr (u == 0) {
+                // every lane polls and the loop condition is a warp vote, so
+                // the warp stays provably converged and the shuffles stay
+                // plain SHFLs
+                const uint32_t a = smem_u32(bars + slot), par = (uint32_t)((it / kSpStages) & 1);
+                while (!__all_sync(0xffffffffu, mbar_try_wait(a, par))) {
+                }
+            }
+            // border-column values: level k's is read one level ahead
+            float bnext = 0.f;
+            if constexpr (COLB) {
+                if (MODE != 1 || PRO >= 2) bnext = bcol[RP + p - 1];
+            }
+            // level 0 is read from the ring, not kept in registers: rows
+            // p-2 .. p (the previous stage is refilled one stage late)
+            auto l0 = [&](int q) {  // q = u - 2 .. u
+                const float* b = q >= 0 ? stage + q * kSpRX : prev + (q + 3) * kSpRX;
+                return *reinterpret_cast<const float4*>(b + 4 * lane);
+            };
+#pragma unroll
+            for (int k = 1; k < F; ++k) {
+                if (MODE != 1 || PRO >= 2 * k) {
+                    const float bk = bnext;
+                    if constexpr (COLB) {
+                        if (k + 1 < F) bnext = bcol[((k + 1) & 1) * RP + p - k - 1];
+                    }
+                    w[k][u] = k == 1 ? calc(l0(u - 2), l0(u - 1), l0(u))
+                                     : calc(w[k - 1][sn], w[k - 1][sc], w[k - 1][u]);
+                    if constexpr (COLB) {
+                        if (cw) w[k][u].x = bk;
+                        if (ce) w[k][u].w = bk;
+                    }
+                    const int r = y0 - F + p - k;
+                    if constexpr (MODE == 1) {
+                        if (PRO - k <= F && r == 0) fix_row(k, r, w[k][u]);
+                    } else if constexpr (MODE == 2) {
+                        if (r == M - 1) fix_row(k, r, w[k][u]);
+                    }
+                }
+            }
+            if (MODE != 1 || PRO >= 2 * F) {
+                const float4 o = calc(w[F - 1][sn], w[F - 1][sc], w[F - 1][u]);
+                const int r = y0 + p - 2 * F;
+                bool keep = lane >= kSpPad / 4 && lane < (kSpPad + kSpX) / 4;
+                if constexpr (MODE == 1) keep = keep && r >= 1;
+                if constexpr (MODE == 2) keep = keep && r <= M - 2;
+                float* d = dst + (int64_t)r * N + gx;
+                if constexpr (!COLB) {
+                    if (keep) *reinterpret_cast<float4*>(d) = o;
+                } else if (keep) {
+                    if (gx >= 1 && gx + 3 <= N - 2) {
+                        *reinterpret_cast<float4*>(d) = o;
+                    } else {
+                        const float e[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (gx + j >= 1 && gx + j <= N - 2) d[j] = e[j];
+                    }
+                }
+            }
+            if constexpr (u == 2) {  // the previous stage is consumed (its last reads fed level 1): refill it
+                __syncwarp();
+                const int nx = it - 1 + kSpStages;
+                if (lane == 0 && it >= 1 && nx < nst) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(bars + pslot, kSpStageF * 4);
+                    tma_load_2d(const_cast<float*>(prev), &src_map, bars + pslot, gx0,
+                                y0 - F + 3 * nx);
+                }
+            }
+        };
+        using I0 = std::integral_constant<int, 0>;
+        using I1 = std::integral_constant<int, 1>;
+        using I2 = std::integral_constant<int, 2>;
+        using NP = std::integral_constant<int, -1>;
+        using M0 = std::integral_constant<int, 0>;
+        using M2 = std::integral_constant<int, 2>;
+        constexpr int L = (2 * F + 3) / 3 * 3;  // prologue rows: multiple of 3, > 2F (holds output row y0)
+        // prologue, fully unrolled so the level guards fold
+        [&]<int... Q>(std::integer_sequence<int, Q...>) {
+            (step(std::integral_constant<int, Q % 3>{}, Q, std::integral_constant<int, Q>{},
+                  std::integral_constant<int, 1>{}),
+             ...);
+        }(std::make_integer_sequence<int, L>{});
+        // rows from pt on may reach plane row M-1 (level k at p = M-1-y0+F+k)
+        const int pt = min(nrows, M - y0 + F);
+        int p = L;
+        for (; p + 3 <= pt; p += 3) {
+            step(I0{}, p, NP{}, M0{});
+            step(I1{}, p + 1, NP{}, M0{});
+            step(I2{}, p + 2, NP{}, M0{});
+        }
+        for (; p < nrows; p += 3) {  // checked tail
+            step(I0{}, p, NP{}, M2{});
+            if (p + 1 < nrows) step(I1{}, p + 1, NP{}, M2{});
+            if (p + 2 < nrows) step(I2{}, p + 2, NP{}, M2{});
+        }
+    };
+    if (colb) sweep(std::true_type{});
+    else sweep(std::false_type{});
+}
+
+// tiles per strip: ~four co-resident waves of warps (4 CTAs x 4 warps per
+// SM) so the edge warps balance out, each tile >= 64 rows
+int strip_tiles(int64_t M, int64_t nstrips) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("SDFGB_J_STRIP_H");
+        forced = e ? atoi(e) : 0;
+    }
+    const int64_t H = forced > 0 ? forced
+                                 : std::max<int64_t>(64, M / std::max<int64_t>(1, ((int64_t)num_sms() * 64 + nstrips - 1) / nstrips));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(M / 16, (M + H - 1) / H));
+}
+
+template <int F>
+int launch_strip(const float* src, float* dst, int64_t M, int64_t N, float coef, cudaStream_t s) {
+    const int64_t nstrips = (N + kSpX - 1) / kSpX;
+    const int ntiles = strip_tiles(M, nstrips);
+    const size_t smem = sp_smem((int)((M + ntiles - 1) / ntiles) + 2 * F);
+    static size_t attr = 0;
+    if (smem > attr) {
+        SDFGB_CUDA(cudaFuncSetAttribute(jacobi_strip_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+        attr = smem;
+    }
+    CUtensorMap map;
+    SDFGB_TRY(encode_tiled_2d(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, src, M, N, kSpRX, 3,
+                              CU_TENSOR_MAP_SWIZZLE_NONE));
+    const int64_t nwarps = nstrips * ntiles;
+    const unsigned blocks = (unsigned)((nwarps + kSpWarps - 1) / kSpWarps);
+    jacobi_strip_kernel<F><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, ntiles,
+                                                               (int)nstrips, (int)nwarps, coef);
+    SDFGB_LAUNCHED("jacobi_strip_kernel");
+    return SDFGB_OK;
+}
+
+bool use_strip() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("SDFGB_J_KERNEL");
+        v = !(e && e[0] == 't');  // SDFGB_J_KERNEL=tile selects jacobi_tb_kernel
+    }
+    return v;
+}
+
 template <int KT>
 int launch_tb(const float* src_plane, float* dst, int64_t M, int64_t N, float coef, cudaStream_t s) {
+    // the strip kernel needs >= 2 strips (each holds at most one border column)
+    if (use_strip() && N > kSpX + kSpPad + 4) return launch_strip<KT>(src_plane, dst, M, N, coef, s);
     static bool attr = false;
     if (!attr) {
         SDFGB_CUDA(cudaFuncSetAttribute(jacobi_tb_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,

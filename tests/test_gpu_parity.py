@@ -320,7 +320,8 @@ def test_jacobi_bit_exact(N, T, terms):
     np.testing.assert_array_equal(At64.cpu().numpy(), ref64)
 
 
-@pytest.mark.parametrize("N,T", [(16, 4), (20, 5), (132, 6), (256, 7), (1000, 11), (1024, 12), (520, 1003)])
+@pytest.mark.parametrize("N,T", [(16, 4), (20, 5), (124, 9), (132, 6), (240, 8), (256, 7), (1000, 11), (1024, 12),
+                                 (520, 1003)])
 def test_jacobi_temporal_blocking_bit_exact(N, T):
     """fp32 canonical order with N % 4 == 0 and T >= 4 runs the TMA temporal-
     blocking kernel (odd step blocks + a final single step): both planes must
@@ -453,7 +454,8 @@ def _jacobi_rect_ref(A, T):
     return ref
 
 
-@pytest.mark.parametrize("M,N,T", [(16, 132, 9), (300, 144, 15), (1000, 256, 11), (129, 512, 8)])
+@pytest.mark.parametrize("M,N,T", [(16, 132, 9), (300, 144, 15), (1000, 256, 11), (129, 512, 8), (17, 248, 7),
+                                   (2000, 128, 8), (33, 1000, 14)])
 def test_jacobi_rect_temporal_blocking_bit_exact(M, N, T):
     from paper_1902_10345_b200 import device
     A = np.random.default_rng(M + N).random((2, M, N), dtype=np.float32)
