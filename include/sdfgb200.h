@@ -149,6 +149,12 @@ int sdfgb_jacobi2d_rect_f32(float* A, int64_t M, int64_t N, int64_t T, double co
  * halo: exact only where the edge is the true border. */
 int sdfgb_jacobi2d_block_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k,
                              double coef, void* stream);
+/* Rows [r0, r1) (clipped to the interior) of one k-step launch src -> dst:
+ * the banded form of sdfgb_jacobi2d_block_f32 that lets a slab runner send
+ * its edge bands while the interior band computes (multigpu.jacobi).  k > 1
+ * needs N >= 128 and r1 - r0 >= 16. */
+int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k,
+                            int64_t r0, int64_t r1, double coef, void* stream);
 
 /* GEMM after MapReduceFusion (library.py:461-554): C = A(MxK) * B(KxN),
  * row-major fp32, fp32-accurate through 3xTF32 on tcgen05 tensor cores.

@@ -556,7 +556,8 @@ __host__ __device__ constexpr size_t sp_smem(int nrows) {
 template <int F>
 __global__ void __launch_bounds__(kSpWarps * 32, 4)
 jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* src, const float* dst_in,
-                    float* dst, int M, int N, int ntiles, int nstrips, int nwarps, float coef) {
+                    float* dst, int M, int N, int ra, int rb, int ntiles, int nstrips, int nwarps, float coef) {
+    // output rows [ra, rb) of the plane (the whole plane, or one band of it)
     extern __shared__ __align__(1024) float sp_smem_f[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = blockIdx.x * kSpWarps + warp;
@@ -564,8 +565,8 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
     const int strip = g % nstrips, tile = g / nstrips;
     // tiles split the rows evenly (every tile >= 2F+2 rows, so only a
     // tile's checked tail can meet plane row M-1 and its prologue row 0)
-    const int y0 = (int)((int64_t)tile * M / ntiles), ye = (int)((int64_t)(tile + 1) * M / ntiles);
-    const int H = (M + ntiles - 1) / ntiles;  // the tallest tile (smem sizing)
+    const int y0 = ra + (int)((int64_t)tile * (rb - ra) / ntiles), ye = ra + (int)((int64_t)(tile + 1) * (rb - ra) / ntiles);
+    const int H = (rb - ra + ntiles - 1) / ntiles;  // the tallest tile (smem sizing)
     const int gx0 = strip * kSpX - kSpPad, gx = gx0 + 4 * lane;
     const int nrows = (ye - y0) + 2 * F;  // input rows y0-F .. ye-1+F
     const int RP = sp_rows(H + 2 * F);  // border-column rows per (plane, side), as sized on the host
@@ -765,10 +766,11 @@ int strip_tiles(int64_t M, int64_t nstrips) {
 }
 
 template <int F>
-int launch_strip(const float* src, float* dst, int64_t M, int64_t N, float coef, cudaStream_t s) {
+int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra, int64_t rb, float coef,
+                 cudaStream_t s) {
     const int64_t nstrips = (N + kSpX - 1) / kSpX;
-    const int ntiles = strip_tiles(M, nstrips);
-    const size_t smem = sp_smem((int)((M + ntiles - 1) / ntiles) + 2 * F);
+    const int ntiles = strip_tiles(rb - ra, nstrips);
+    const size_t smem = sp_smem((int)((rb - ra + ntiles - 1) / ntiles) + 2 * F);
     static size_t attr = 0;
     if (smem > attr) {
         SDFGB_CUDA(cudaFuncSetAttribute(jacobi_strip_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -780,8 +782,8 @@ int launch_strip(const float* src, float* dst, int64_t M, int64_t N, float coef,
                               CU_TENSOR_MAP_SWIZZLE_NONE));
     const int64_t nwarps = nstrips * ntiles;
     const unsigned blocks = (unsigned)((nwarps + kSpWarps - 1) / kSpWarps);
-    jacobi_strip_kernel<F><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, ntiles,
-                                                               (int)nstrips, (int)nwarps, coef);
+    jacobi_strip_kernel<F><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, (int)ra, (int)rb,
+                                                               ntiles, (int)nstrips, (int)nwarps, coef);
     SDFGB_LAUNCHED("jacobi_strip_kernel");
     return SDFGB_OK;
 }
@@ -798,7 +800,7 @@ bool use_strip() {
 template <int KT>
 int launch_tb(const float* src_plane, float* dst, int64_t M, int64_t N, float coef, cudaStream_t s) {
     // the strip kernel needs >= 2 strips (each holds at most one border column)
-    if (use_strip() && N > kSpX + kSpPad + 4) return launch_strip<KT>(src_plane, dst, M, N, coef, s);
+    if (use_strip() && N > kSpX + kSpPad + 4) return launch_strip<KT>(src_plane, dst, M, N, 0, M, coef, s);
     static bool attr = false;
     if (!attr) {
         SDFGB_CUDA(cudaFuncSetAttribute(jacobi_tb_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -914,4 +916,34 @@ extern "C" int sdfgb_jacobi2d_block_f32(const float* src, float* dst, int64_t M,
     const int32_t di[5] = {0, -1, 1, 0, 0}, dj[5] = {0, 0, 0, -1, 1};
     sdfgb::parse_terms(di, dj, 5, terms, canon);
     return sdfgb::launch_block(src, dst, M, N, k, (float)coef, terms, sdfgb::as_stream(stream));
+}
+
+// Output rows [r0, r1) only (clipped to the interior [1, M-2]) of one k-step
+// launch src (state t) -> dst (state t+k): the multi-GPU slab runner
+// computes its edge bands first, sends them, and overlaps the exchange with
+// the interior band.  k > 1 needs the strip kernel (N >= 128).
+extern "C" int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k, int64_t r0,
+                                       int64_t r1, double coef, void* stream) {
+    if (M < 16 || N < 16 || (N % 4) != 0 || !src || !dst || (reinterpret_cast<uintptr_t>(src) & 15) != 0 ||
+        (reinterpret_cast<uintptr_t>(dst) & 15) != 0 || r0 < 0 || r1 > M || r0 > r1)
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: bad arguments");
+    r0 = std::max<int64_t>(r0, 1);
+    r1 = std::min<int64_t>(r1, M - 1);
+    if (r1 <= r0) return SDFGB_OK;
+    cudaStream_t s = sdfgb::as_stream(stream);
+    if (k == 1) {
+        sdfgb::Terms terms;
+        bool canon;
+        const int32_t di[5] = {0, -1, 1, 0, 0}, dj[5] = {0, 0, 0, -1, 1};
+        sdfgb::parse_terms(di, dj, 5, terms, canon);
+        return sdfgb::launch_step<float>(src, dst, N, M, 0, r0, r1, (float)coef, terms, true, s);
+    }
+    if (N <= sdfgb::kSpX + sdfgb::kSpPad + 4)
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k > 1 bands need N >= 128 (strip kernel)");
+    if (r1 - r0 < 16)
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k > 1 bands are at least 16 rows");
+    if (k == 7) return sdfgb::launch_strip<7>(src, dst, M, N, r0, r1, (float)coef, s);
+    if (k == 5) return sdfgb::launch_strip<5>(src, dst, M, N, r0, r1, (float)coef, s);
+    if (k == 3) return sdfgb::launch_strip<3>(src, dst, M, N, r0, r1, (float)coef, s);
+    return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k must be 1, 3, 5 or 7 (got %lld)", (long long)k);
 }

@@ -120,6 +120,15 @@ def jacobi2d_block(src, dst, k, coef=0.2, stream=None):
     _lib.check(L.sdfgb_jacobi2d_block_f32(_p(src), _p(dst), M, N, int(k), float(coef), _stream(stream)))
 
 
+def jacobi2d_band(src, dst, k, r0, r1, coef=0.2, stream=None):
+    """Rows [r0, r1) of one k-step launch src -> dst (banded
+    jacobi2d_block; k > 1 needs N >= 128 and >= 16 rows)."""
+    L = _lib.load()
+    M, N = src.shape[-2], src.shape[-1]
+    _lib.check(L.sdfgb_jacobi2d_band_f32(_p(src), _p(dst), M, N, int(k), int(r0), int(r1), float(coef),
+                                         _stream(stream)))
+
+
 def jacobi2d_step(src, dst, N, rows, g0, r0, r1, coef=0.2, terms=JACOBI5, stream=None):
     L = _lib.load()
     di, dj = _terms(terms)

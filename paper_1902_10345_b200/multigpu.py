@@ -6,8 +6,9 @@ Each runner takes ``pg`` (the ``torch.distributed`` module) and a compute
 ``backend``; the default is the device kernels of :mod:`.device`.  The
 decompositions keep every element's operation order, so a sharded result is
 bit-identical to the one-device result for histogram, query and Jacobi (and
-for SpMV, whose rows stay whole).  Per-GPU work is fixed as ranks are added
-(weak scaling), as in bench.py.
+for SpMV, whose rows stay whole, and GEMM, whose K stays whole).  bench.py
+splits the configured shapes across ranks with :func:`share` (strong
+scaling) and can also give every rank the whole shape (weak scaling).
 
 The exchange steps are the ones the north star names:
   histogram  per-GPU partial bins -> all_reduce(sum)
@@ -15,14 +16,23 @@ The exchange steps are the ones the north star names:
              (output stays sharded at its global offset; gather is optional)
   spmv       row blocks, x sharded -> all_gather(x) -> row kernel
   jacobi     row blocks with 7-row ghost zones -> one send/recv of ghost
-             rows per temporal block (up to 7 steps)
-  gemm       2-D process grid -> all_gather of A row panels / B column panels
+             rows per temporal block (up to 7 steps), sent as soon as the
+             edge bands are computed and overlapped with the interior band
+  gemm       2-D process grid -> all_gather of the B column panel, then the
+             A row panel's pieces broadcast one by one, each piece's C rows
+             computed while the next piece is in flight
 """
 
 from __future__ import annotations
 
 import math
 from dataclasses import dataclass
+
+
+def share(total, rank, world):
+    """[lo, hi) of ``total`` units owned by ``rank``: contiguous, sizes
+    differing by at most one (the strong-scaling split of every motif)."""
+    return total * rank // world, total * (rank + 1) // world
 
 
 class DeviceBackend:
@@ -51,6 +61,12 @@ class DeviceBackend:
 
     def jacobi_block(self, src, dst, k, coef):
         self.d.jacobi2d_block(src, dst, k, coef)
+
+    def can_band(self, plane):
+        return plane.shape[-1] >= 128 and plane.shape[-1] % 4 == 0
+
+    def jacobi_band(self, src, dst, k, r0, r1, coef):
+        self.d.jacobi2d_band(src, dst, k, r0, r1, coef)
 
     def gemm(self, A, B, C):
         M, K = A.shape
@@ -314,24 +330,34 @@ def jacobi_slab(A_global_rows, g0, Ng, ghost=GHOST):
     return JacobiSlab(A, g0, rows, Ng, top, bot)
 
 
-def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1))):
+def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1)),
+           overlap=True):
     """T steps of the guard loop (loops.py:31-61) over row blocks with
     ghost zones: the single-GPU temporal-blocking schedule (odd blocks of
     7/5/3 steps, then one final step so the other plane ends at state T-1)
-    with, before every launch, one exchange of the source plane's ghost
-    rows with each neighbour (GHOST rows of 2 x N fp32 per block of up to
-    GHOST steps, instead of a halo per step).  Every owned row sits at least
-    GHOST rows from a ghost edge, so after k <= GHOST steps it is exact;
-    the ghost rows themselves are refreshed before they are read again.
-    Non-canonical stencil orders take one step per exchange."""
+    with one exchange of ghost rows per block of up to GHOST steps (GHOST
+    rows of N fp32 per neighbour, instead of a halo per step).  Every owned
+    row sits at least GHOST rows from a ghost edge, so after k <= GHOST
+    steps it is exact; ghost rows are refreshed before they are read again.
+
+    With ``overlap`` (and a backend that computes row bands) each block
+    first computes the owned rows within EDGE of a neighbour -- the rows the
+    neighbours' ghost zones need -- then posts the exchange of those rows
+    and computes the interior band while it is in flight; the next block
+    waits for it.  Non-canonical stencil orders take one step per block."""
     rank, world = _rank_world(pg)
     A = slab.A
     canon = tuple(map(tuple, terms)) == ((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1))
+    top, rows, bot = slab.top, slab.rows, slab.bot
+    band = bool(overlap and canon and hasattr(backend, "jacobi_band") and backend.can_band(A[0])
+                and (top or bot) and rows >= 3 * EDGE)
     # both planes' ghost rows once: the border columns of the ghost rows are
     # border values of their own plane, read by intermediate states of the
     # other parity and never exchanged again
     _ghost_exchange(pg, A[1], slab, rank, world)
+    _ghost_exchange(pg, A[0], slab, rank, world)
     t = 0
+    pending = None
     while t < T:
         if not canon:
             k = 1
@@ -341,17 +367,39 @@ def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (
         else:
             k = 1
         src, dst = A[t % 2], A[(t + 1) % 2]
-        _ghost_exchange(pg, src, slab, rank, world)
-        if canon:
-            backend.jacobi_block(src, dst, k, coef)
+        if pending is not None:
+            _finish_exchange(pending)  # src's ghost rows have landed
+            pending = None
+        if band:
+            lo, hi = top, top + rows  # owned rows
+            e0 = lo + EDGE if top else lo
+            e1 = hi - EDGE if bot else hi
+            if top:
+                backend.jacobi_band(src, dst, k, lo, e0, coef)
+            if bot:
+                backend.jacobi_band(src, dst, k, e1, hi, coef)
+            pending = _ghost_exchange(pg, dst, slab, rank, world, wait=False)
+            backend.jacobi_band(src, dst, k, e0, e1, coef)
         else:
-            M = A.shape[1]
-            backend.jacobi_step(src, dst, A.shape[-1], M, 1, M - 1, coef, terms)
+            if canon:
+                backend.jacobi_block(src, dst, k, coef)
+            else:
+                M = A.shape[1]
+                backend.jacobi_step(src, dst, A.shape[-1], M, 1, M - 1, coef, terms)
+            _ghost_exchange(pg, dst, slab, rank, world)
         t += k
+    if pending is not None:
+        _finish_exchange(pending)
 
 
-def _ghost_exchange(pg, plane, slab: JacobiSlab, rank, world):
-    """Owned edge rows -> the neighbours' ghost rows (batched send/recv)."""
+EDGE = 16  # edge-band rows computed before the exchange (>= GHOST; the strip kernel's minimum band)
+
+
+def _ghost_exchange(pg, plane, slab: JacobiSlab, rank, world, wait=True):
+    """Owned edge rows -> the neighbours' ghost rows (batched send/recv).
+    With ``wait=False`` the exchange stays in flight and the returned
+    handle goes to :func:`_finish_exchange` (NCCL: the sends/receives run on
+    the collective stream, after the work already queued on this one)."""
     ops = []
     top, rows, bot = slab.top, slab.rows, slab.bot
     if rank > 0 and top:
@@ -361,23 +409,31 @@ def _ghost_exchange(pg, plane, slab: JacobiSlab, rank, world):
         ops.append(pg.P2POp(pg.isend, plane[top + rows - bot:top + rows].contiguous(), rank + 1))
         ops.append(pg.P2POp(pg.irecv, plane[top + rows:top + rows + bot], rank + 1))
     if not ops:
-        return
+        return None
+    back = []
     if plane.is_cuda and pg.get_backend() == "gloo":
         # gloo moves host memory only: stage the rows through the host
         import torch
-        staged, back = [], []
+        staged = []
         for op in ops:
             h = op.tensor.cpu() if op.op is pg.isend else torch.empty(op.tensor.shape, dtype=op.tensor.dtype)
             if op.op is pg.irecv:
                 back.append((op.tensor, h))
             staged.append(pg.P2POp(op.op, h, op.peer))
-        for r in pg.batch_isend_irecv(staged):
-            r.wait()
-        for dev, h in back:
-            dev.copy_(h)
-        return
-    for r in pg.batch_isend_irecv(ops):
+        ops = staged
+    handle = (pg.batch_isend_irecv(ops), back)
+    if wait:
+        _finish_exchange(handle)
+        return None
+    return handle
+
+
+def _finish_exchange(handle):
+    works, back = handle
+    for r in works:
         r.wait()
+    for dev, h in back:
+        dev.copy_(h)
 
 
 # ---------------------------------------------------------------------- gemm
@@ -403,15 +459,59 @@ class GemmGrid:
         self.col_group = self.col_groups[self.j]
 
 
-def gemm(pg, grid: GemmGrid, A_piece, B_piece, C_block, backend):
-    """C block (i, j) = A row panel i x B column panel j.  A panel i is split
-    by rows over the Q ranks of grid row i, B panel j by rows (of K) over the
-    P ranks of grid column j; each is all-gathered inside its group.  K is not
-    split, so every C element keeps the single-device summation."""
+def gemm_pieces(A, B, grid: GemmGrid):
+    """This rank's inputs of the P x Q decomposition of C = A @ B, cut from
+    the whole operands: A row panel i split by rows over the Q ranks of
+    grid row i, B column panel j split by rows (of K) over the P ranks of
+    grid column j.  Returns contiguous (A_piece, B_piece); this rank's C
+    block is rows share(M, i, P) x columns share(N, j, Q)."""
+    M, K = A.shape
+    N = B.shape[1]
+    a0, a1 = share(M, grid.i, grid.P)
+    q0, q1 = share(a1 - a0, grid.j, grid.Q)
+    b0, b1 = share(N, grid.j, grid.Q)
+    k0, k1 = share(K, grid.i, grid.P)
+    return A[a0 + q0:a0 + q1].contiguous(), B[k0:k1, b0:b1].contiguous()
+
+
+def gemm(pg, grid: GemmGrid, A_piece, B_piece, C_block, backend, pipeline=True):
+    """C block (i, j) = A row panel i x B column panel j (pieces as cut by
+    :func:`gemm_pieces`).  The B panel is all-gathered inside grid column j
+    (K whole).  With ``pipeline`` the A panel's pieces are then broadcast
+    inside grid row i, all in flight at once, and the C rows of each piece
+    are computed as soon as it has landed (this rank's own piece first), so
+    the A exchange overlaps the MMA.  K is never split: every C element
+    keeps the single-device summation."""
     import torch
-    Aq = torch.empty((A_piece.shape[0] * grid.Q, A_piece.shape[1]), dtype=A_piece.dtype, device=A_piece.device)
-    pg.all_gather_into_tensor(Aq, A_piece.contiguous(), group=grid.row_group)
-    Bp = torch.empty((B_piece.shape[0] * grid.P, B_piece.shape[1]), dtype=B_piece.dtype, device=B_piece.device)
-    pg.all_gather_into_tensor(Bp, B_piece.contiguous(), group=grid.col_group)
-    backend.gemm(Aq, Bp, C_block)
-    return Aq, Bp
+    K = A_piece.shape[1]
+    kp = [share(K, r, grid.P) for r in range(grid.P)]
+    Bp = torch.empty((K, B_piece.shape[1]), dtype=B_piece.dtype, device=B_piece.device)
+    _gather_rows(pg, [Bp[a:b] for a, b in kp], B_piece, grid.i, [i * grid.Q + grid.j for i in range(grid.P)],
+                 grid.col_group)
+    rows = [share(C_block.shape[0], q, grid.Q) for q in range(grid.Q)]
+    if not pipeline or grid.Q == 1:
+        Aq = torch.empty((C_block.shape[0], K), dtype=A_piece.dtype, device=A_piece.device)
+        _gather_rows(pg, [Aq[a:b] for a, b in rows], A_piece, grid.j, [grid.i * grid.Q + q for q in range(grid.Q)],
+                     grid.row_group)
+        backend.gemm(Aq, Bp, C_block)
+        return
+    bufs = [A_piece.contiguous() if q == grid.j else
+            torch.empty((b - a, K), dtype=A_piece.dtype, device=A_piece.device) for q, (a, b) in enumerate(rows)]
+    works = [pg.broadcast(bufs[q], src=grid.i * grid.Q + q, group=grid.row_group, async_op=True)
+             for q in range(grid.Q)]
+    for q in [grid.j] + [q for q in range(grid.Q) if q != grid.j]:
+        works[q].wait()
+        a, b = rows[q]
+        if b > a:
+            backend.gemm(bufs[q], Bp, C_block[a:b])
+
+
+def _gather_rows(pg, outs, mine, me, ranks, group):
+    """outs[q] <- rank ranks[q]'s piece (row blocks of one tensor): one
+    all_gather when the pieces are equal, else one broadcast per piece."""
+    if all(o.shape == outs[0].shape for o in outs):
+        pg.all_gather(outs, mine.contiguous(), group=group)
+        return
+    outs[me].copy_(mine)
+    for q, o in enumerate(outs):
+        pg.broadcast(o, src=ranks[q], group=group)
