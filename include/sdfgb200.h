@@ -152,7 +152,7 @@ int sdfgb_jacobi2d_block_f32(const float* src, float* dst, int64_t M, int64_t N,
 /* Rows [r0, r1) (clipped to the interior) of one k-step launch src -> dst:
  * the banded form of sdfgb_jacobi2d_block_f32 that lets a slab runner send
  * its edge bands while the interior band computes (multigpu.jacobi).  k > 1
- * needs N >= 128 and r1 - r0 >= 16. */
+ * needs N >= 128 and at least 8 interior rows. */
 int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k,
                             int64_t r0, int64_t r1, double coef, void* stream);
 
@@ -225,13 +225,17 @@ int sdfgb_spmv_csr_f32_mgpu(const int32_t* rowptr, const int32_t* col, const flo
 /* Jacobi on a row slab A[2, top + rows + bot, N] (N % 4 == 0): top / bot are
  * 7 ghost rows towards each neighbour (0 at the global edge, whose plane edge
  * is the true border).  One grouped ncclSend/ncclRecv of ghost rows per
- * temporal block of up to 7 steps; canonical 5-point order. */
+ * temporal block of up to 7 steps, issued on an internal side stream once the
+ * edge bands are computed and overlapped with the interior band (N >= 128,
+ * rows >= 48); canonical 5-point order. */
 int sdfgb_jacobi2d_f32_mgpu(float* A, int64_t top, int64_t rows, int64_t bot, int64_t N, int64_t T,
                             double coef, void* comm, void* stream);
 /* P x Q grid GEMM: C block (i, j) = A row panel i x B column panel j.  A_piece
  * (a_rows x K) is this rank's share of panel i, gathered over row_comm (size
  * Q) into A_panel (a_rows*Q x K); B_piece (b_rows x nq) its share of panel j,
- * gathered over col_comm (size P, b_rows*P == K) into B_panel (K x nq).
+ * gathered over col_comm (size P, b_rows*P == K) into B_panel (K x nq).  The
+ * A pieces are broadcast on an internal side stream and each piece's C rows
+ * computed as soon as it lands (the exchange overlaps the MMA).
  * ws: sdfgb_gemm_workspace_bytes(a_rows*Q, nq, K). */
 int sdfgb_gemm_f32_mgpu(const float* A_piece, int64_t a_rows, const float* B_piece, int64_t b_rows,
                         int64_t K, int64_t nq, float* A_panel, float* B_panel, float* C_block,

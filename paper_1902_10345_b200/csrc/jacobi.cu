@@ -940,8 +940,8 @@ extern "C" int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, 
     }
     if (N <= sdfgb::kSpX + sdfgb::kSpPad + 4)
         return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k > 1 bands need N >= 128 (strip kernel)");
-    if (r1 - r0 < 16)
-        return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k > 1 bands are at least 16 rows");
+    if (r1 - r0 < 8)  // a strip tile needs >= 8 rows (its prologue never meets plane row M-1)
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k > 1 bands are at least 8 interior rows");
     if (k == 7) return sdfgb::launch_strip<7>(src, dst, M, N, r0, r1, (float)coef, s);
     if (k == 5) return sdfgb::launch_strip<5>(src, dst, M, N, r0, r1, (float)coef, s);
     if (k == 3) return sdfgb::launch_strip<3>(src, dst, M, N, r0, r1, (float)coef, s);

@@ -8,9 +8,13 @@
 //   query      local compaction -> ncclAllGather(counts) -> global offsets
 //   spmv       ncclAllGather(x shards) -> local row block
 //   jacobi     row slabs with GHOST-row ghost zones, one grouped
-//              ncclSend/ncclRecv per temporal block of up to GHOST steps
-//   gemm       P x Q grid: ncclAllGather of the A row panel in the grid row
-//              and the B column panel in the grid column, then the local GEMM
+//              ncclSend/ncclRecv per temporal block of up to GHOST steps,
+//              issued on a side stream as soon as the edge bands are done
+//              and overlapped with the interior band
+//   gemm       P x Q grid: ncclAllGather of the B column panel in the grid
+//              column, then the A row panel's pieces broadcast in the grid
+//              row on a side stream, each piece's C rows computed as soon
+//              as it lands
 //
 // Every decomposition keeps each element's operation order, so results are
 // bit-identical to the one-GPU entries (SpMV rows and GEMM's K stay whole).
@@ -25,6 +29,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -37,6 +42,8 @@ int sdfgb_spmv_csr_f32(const int32_t* rowptr, const int32_t* col, const float* v
                        int64_t H, void* stream);
 int sdfgb_jacobi2d_block_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k, double coef,
                              void* stream);
+int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k, int64_t r0, int64_t r1,
+                            double coef, void* stream);
 int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, void* ws,
                    size_t ws_bytes, void* stream);
 }
@@ -52,6 +59,7 @@ struct NcclApi {
     decltype(&ncclCommUserRank) commUserRank = nullptr;
     decltype(&ncclAllReduce) allReduce = nullptr;
     decltype(&ncclAllGather) allGather = nullptr;
+    decltype(&ncclBroadcast) broadcast = nullptr;
     decltype(&ncclSend) send = nullptr;
     decltype(&ncclRecv) recv = nullptr;
     decltype(&ncclGroupStart) groupStart = nullptr;
@@ -84,6 +92,7 @@ NcclApi& nccl() {
         SDFGB_NCCL_SYM(commUserRank, "ncclCommUserRank")
         SDFGB_NCCL_SYM(allReduce, "ncclAllReduce")
         SDFGB_NCCL_SYM(allGather, "ncclAllGather")
+        SDFGB_NCCL_SYM(broadcast, "ncclBroadcast")
         SDFGB_NCCL_SYM(send, "ncclSend")
         SDFGB_NCCL_SYM(recv, "ncclRecv")
         SDFGB_NCCL_SYM(groupStart, "ncclGroupStart")
@@ -104,6 +113,38 @@ int nccl_check(ncclResult_t r, const char* what) {
     do {                                                                                     \
         if (!::sdfgb::nccl().ok) return set_error(SDFGB_ERR_COMM, "%s", ::sdfgb::nccl().why); \
     } while (0)
+
+// A side stream plus events for overlapping exchanges with compute; every
+// return path waits for the side stream's work on the caller's stream and
+// frees both (RAII), so nothing is left in flight on error.
+struct SideStream {
+    cudaStream_t main = nullptr, side = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int rc = SDFGB_OK;
+    explicit SideStream(cudaStream_t m) : main(m) {
+        rc = check_cuda(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (int i = 0; i < 2 && rc == SDFGB_OK; ++i)
+            rc = check_cuda(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    // side waits for everything queued on main so far
+    int fork() {
+        SDFGB_CUDA(cudaEventRecord(ev[0], main));
+        return check_cuda(cudaStreamWaitEvent(side, ev[0], 0), "cudaStreamWaitEvent");
+    }
+    // main waits for everything queued on side so far
+    int join() {
+        SDFGB_CUDA(cudaEventRecord(ev[1], side));
+        return check_cuda(cudaStreamWaitEvent(main, ev[1], 0), "cudaStreamWaitEvent");
+    }
+    ~SideStream() {
+        if (side) {
+            join();
+            cudaStreamDestroy(side);
+        }
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
 
 int comm_shape(ncclComm_t c, int* rank, int* world) {
     SDFGB_NCCL(nccl().commUserRank(c, rank));
@@ -263,19 +304,37 @@ extern "C" int sdfgb_jacobi2d_f32_mgpu(float* A, int64_t top, int64_t rows, int6
     // both planes' ghost rows once: their border columns are read by
     // intermediate states of the other parity and never exchanged again
     SDFGB_TRY(ghost_exchange(A + plane, N, top, rows, bot, rank, world, c, s));
+    SDFGB_TRY(ghost_exchange(A, N, top, rows, bot, rank, world, c, s));
+    // overlapped schedule (multigpu.jacobi): edge bands, exchange of the new
+    // edge rows on the side stream, interior band; the next block waits
+    constexpr int64_t EDGE = 16;
+    const bool band = N >= 128 && (top || bot) && rows >= 3 * EDGE;
+    SideStream ss(s);
+    SDFGB_TRY(ss.rc);
     for (int64_t t = 0; t < T;) {
         int64_t k = 1;
         if (T - t > 1) {
             k = std::min<int64_t>(GHOST, T - 1 - t);
             k -= (k % 2 == 0);
         }
-        float* src = A + (t % 2) * plane;
+        const float* src = A + (t % 2) * plane;
         float* dst = A + ((t + 1) % 2) * plane;
-        SDFGB_TRY(ghost_exchange(src, N, top, rows, bot, rank, world, c, s));
-        SDFGB_TRY(sdfgb_jacobi2d_block_f32(src, dst, M, N, k, coef, stream));
+        SDFGB_TRY(ss.join());  // src's ghost rows have landed
+        if (band) {
+            const int64_t lo = top, hi = top + rows;
+            const int64_t e0 = top ? lo + EDGE : lo, e1 = bot ? hi - EDGE : hi;
+            if (top) SDFGB_TRY(sdfgb_jacobi2d_band_f32(src, dst, M, N, k, lo, e0, coef, stream));
+            if (bot) SDFGB_TRY(sdfgb_jacobi2d_band_f32(src, dst, M, N, k, e1, hi, coef, stream));
+            SDFGB_TRY(ss.fork());
+            SDFGB_TRY(ghost_exchange(dst, N, top, rows, bot, rank, world, c, ss.side));
+            SDFGB_TRY(sdfgb_jacobi2d_band_f32(src, dst, M, N, k, e0, e1, coef, stream));
+        } else {
+            SDFGB_TRY(sdfgb_jacobi2d_block_f32(src, dst, M, N, k, coef, stream));
+            SDFGB_TRY(ghost_exchange(dst, N, top, rows, bot, rank, world, c, s));
+        }
         t += k;
     }
-    return SDFGB_OK;
+    return ss.join();
 }
 
 // ----------------------------------------------------------------------- gemm
@@ -290,14 +349,40 @@ extern "C" int sdfgb_gemm_f32_mgpu(const float* A_piece, int64_t a_rows, const f
     SDFGB_TRY(comm_shape(static_cast<ncclComm_t>(col_comm), &pi, &P));
     if (b_rows * P != K) return set_error(SDFGB_ERR_INVALID, "gemm_mgpu: the B pieces must tile K");
     cudaStream_t s = as_stream(stream);
-    SDFGB_NCCL(nccl().groupStart());
-    int rc = nccl_check(nccl().allGather(A_piece, A_panel, (size_t)(a_rows * K), ncclFloat32,
-                                         static_cast<ncclComm_t>(row_comm), s), "ncclAllGather(A)");
-    if (rc == SDFGB_OK)
-        rc = nccl_check(nccl().allGather(B_piece, B_panel, (size_t)(b_rows * nq), ncclFloat32,
-                                         static_cast<ncclComm_t>(col_comm), s), "ncclAllGather(B)");
-    const int rc2 = nccl_check(nccl().groupEnd(), "ncclGroupEnd");
-    if (rc != SDFGB_OK) return rc;
-    if (rc2 != SDFGB_OK) return rc2;
-    return sdfgb_gemm_f32(A_panel, B_panel, C_block, a_rows * Q, nq, K, ws, ws_bytes, stream);
+    SDFGB_NCCL(nccl().allGather(B_piece, B_panel, (size_t)(b_rows * nq), ncclFloat32,
+                                static_cast<ncclComm_t>(col_comm), s));
+    if (Q == 1) {
+        if (A_panel != A_piece)
+            SDFGB_CUDA(cudaMemcpyAsync(A_panel, A_piece, (size_t)(a_rows * K) * 4, cudaMemcpyDeviceToDevice, s));
+        return sdfgb_gemm_f32(A_panel, B_panel, C_block, a_rows, nq, K, ws, ws_bytes, stream);
+    }
+    // the A panel's Q pieces: this rank's first (no wait), the others
+    // broadcast on the side stream and consumed as they land; K stays whole
+    // so each C row keeps the one-GPU summation
+    SideStream ss(s);
+    SDFGB_TRY(ss.rc);
+    SDFGB_CUDA(cudaMemcpyAsync(A_panel + qi * a_rows * K, A_piece, (size_t)(a_rows * K) * 4,
+                               cudaMemcpyDeviceToDevice, s));
+    SDFGB_TRY(ss.fork());
+    std::vector<cudaEvent_t> landed(Q, nullptr);
+    struct Events {
+        std::vector<cudaEvent_t>& v;
+        ~Events() {
+            for (auto e : v)
+                if (e) cudaEventDestroy(e);
+        }
+    } guard{landed};
+    for (int q = 0; q < Q; ++q) {
+        SDFGB_CUDA(cudaEventCreateWithFlags(&landed[q], cudaEventDisableTiming));
+        SDFGB_NCCL(nccl().broadcast(A_panel + q * a_rows * K, A_panel + q * a_rows * K, (size_t)(a_rows * K),
+                                    ncclFloat32, q, static_cast<ncclComm_t>(row_comm), ss.side));
+        SDFGB_CUDA(cudaEventRecord(landed[q], ss.side));
+    }
+    for (int i = 0; i < Q; ++i) {
+        const int q = (qi + i) % Q;
+        if (q != qi) SDFGB_CUDA(cudaStreamWaitEvent(s, landed[q], 0));
+        SDFGB_TRY(sdfgb_gemm_f32(A_panel + q * a_rows * K, B_panel, C_block + q * a_rows * nq, a_rows, nq, K, ws,
+                                 ws_bytes, stream));
+    }
+    return ss.join();
 }

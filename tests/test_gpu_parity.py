@@ -499,6 +499,41 @@ def test_jacobi_ghost_zone_slabs_on_one_device(ranks):
                                       ref[:, r * rows:(r + 1) * rows])
 
 
+from paper_1902_10345_b200.errors import CodegenError  # noqa: E402
+
+
+@pytest.mark.parametrize("k", [1, 3, 5, 7])
+@pytest.mark.parametrize("M,N,cuts", [(200, 256, (16, 184)), (129, 512, (40, 57)), (96, 132, (1, 95)),
+                                      (300, 1000, (23, 151))])
+def test_jacobi_band_composition(k, M, N, cuts):
+    """sdfgb_jacobi2d_band_f32: the edge bands and the interior band of one
+    k-step launch (as multigpu.jacobi computes them around the in-flight
+    ghost exchange) write exactly the rows the whole-plane launch writes,
+    with the same bits, and nothing else."""
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(M + N + k)
+    P = rng.random((2, M, N), dtype=np.float32)
+    whole = t(P)
+    device.jacobi2d_block(whole[0], whole[1], k)
+    banded = t(P)
+    e0, e1 = cuts
+    for r0, r1 in ((0, e0), (e1, M), (e0, e1)):
+        if k > 1 and 0 < min(r1, M - 1) - max(r0, 1) < 8:
+            with pytest.raises(CodegenError):
+                device.jacobi2d_band(banded[0], banded[1], k, r0, r1)
+            return
+        device.jacobi2d_band(banded[0], banded[1], k, r0, r1)
+    np.testing.assert_array_equal(banded.cpu().numpy(), whole.cpu().numpy())
+    # a single band touches only its own rows
+    one = t(P)
+    device.jacobi2d_band(one[0], one[1], k, 40 if M > 60 else 1, 60 if M > 60 else 17)
+    got, ref = one.cpu().numpy(), whole.cpu().numpy()
+    r0, r1 = (40, 60) if M > 60 else (1, 17)
+    np.testing.assert_array_equal(got[1, r0:r1], ref[1, r0:r1])
+    np.testing.assert_array_equal(got[1, :r0], P[1, :r0])
+    np.testing.assert_array_equal(got[1, r1:], P[1, r1:])
+
+
 @pytest.mark.parametrize("n", [4096, 16384])
 def test_full_gemm(n):
     """M1 checked on every element (oracle over all rows, threads over rows);
