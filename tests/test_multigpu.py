@@ -331,3 +331,28 @@ def test_bench_multi_rank_plumbing_on_one_gpu(tmp_path):
         assert d["motifs"][m]["ok"] is True, (m, full[m]["check"])  # strong split, checked result
     assert full["histogram"]["config"]["exchange"].startswith("p2p")
     assert full["jacobi2d"]["config"]["rows"] in ([0, 4096], [4096, 8192])
+
+
+@pytest.mark.gpu
+def test_bench_nccl_two_gpus(tmp_path):
+    """bench.py at N=2 exactly as the driver launches it (torchrun, NCCL, one
+    rank per GPU, strong scaling): every motif's sharded result passes its
+    check.  Needs two GPUs; skipped on a one-GPU box."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (NCCL over NVLink)")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(REPO, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    for m, v in d["motifs"].items():
+        assert v["ok"] in (True, None), (m, v)
