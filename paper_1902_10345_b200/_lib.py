@@ -97,7 +97,9 @@ def load(path: str = None):
     with _lock:
         if _lib is not None:
             return _lib
-        path = path or LIB_PATH
+        # SDFGB_LIB: an alternative build of the same library (kernel
+        # experiments under tools/); the default is the in-tree build
+        path = path or os.environ.get("SDFGB_LIB") or LIB_PATH
         if not os.path.exists(path):
             raise BackendUnavailable(
                 f"{path} is not built; run __graft_entry__.build() (make -C paper_1902_10345_b200/csrc)")
