@@ -143,6 +143,48 @@ def test_native_query_mixed_exact_and_inexact_chunks(ordered):
         np.testing.assert_array_equal(out[k:], ref_out[k:])
 
 
+def _pinned(a):
+    t = torch.empty(a.shape, dtype={np.float64: torch.float64, np.int64: torch.int64}[a.dtype.type],
+                    pin_memory=True)
+    t.numpy()[...] = a
+    return t  # keep the tensor alive; t.numpy() shares its page-locked memory
+
+
+@pytest.mark.parametrize("prec", ["native", "fp32"])
+@pytest.mark.parametrize("ordered", [False, True])
+@pytest.mark.parametrize("pinned_out", [False, True])
+def test_query_page_locked_buffers(prec, ordered, pinned_out):
+    """Page-locked (pinned) caller buffers, as the bench passes them: the
+    column still goes through the narrowing ring (chunks holding non-fp32
+    values keep float64), a pinned out_vals takes the survivors widened on
+    the device and DMA'd straight in.  Survivors are the oracle's either
+    way, in FIFO order when asked."""
+    rng = np.random.default_rng(11)
+    N = 9_000_001  # many staging chunks, ragged tail
+    col = rng.random(N, dtype=np.float32).astype(np.float64)
+    for i in (3, 2_000_003, 4_500_000, N - 2):  # non-fp32 values in narrowed and direct chunks
+        col[i] = 0.5 - 2.0 ** -40
+    col[7_000_000] = 0.5 + 2.0 ** -30
+    tcol = _pinned(col)
+    tout = _pinned(np.full(N, -1.0)) if pinned_out else None
+    out = tout.numpy() if pinned_out else np.full(N, -1.0)
+    cnt = np.array([2], np.int64)
+    p = _lib.PREC_NATIVE if prec == "native" else _lib.PREC_FP32
+    src = col if prec == "native" else col.astype(np.float32).astype(np.float64)
+    ref_out, ref_cnt = oracle.query(src, 0.5, np.full(N, -1.0), cnt.copy())
+    op = _lib.CMP["<"] | (_lib.QUERY_ORDERED if ordered else 0)
+    thr = np.array([0.5])
+    _lib.check(_lib.load().sdfgb_host_query(ctypes.c_void_p(tcol.data_ptr()), _vp(thr), _vp(out), _vp(cnt), N, op,
+                                            p))
+    k = int(ref_cnt[0] - 2)
+    assert cnt[0] == ref_cnt[0]
+    if ordered:
+        np.testing.assert_array_equal(out[:k], ref_out[:k])
+    else:
+        np.testing.assert_array_equal(np.sort(out[:k]), np.sort(ref_out[:k]))
+    np.testing.assert_array_equal(out[k:], -1.0)
+
+
 # ------------------------------------------------------------- error paths
 
 def test_failed_calls_leave_the_entries_clean():
