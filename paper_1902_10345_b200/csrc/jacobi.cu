@@ -543,6 +543,27 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* dst_in,
 //     column over the strip's rows is staged in shared memory once, and a
 //     row step reads its F-1 values before computing, off the dependency
 //     chain of the levels.
+#ifndef SDFGB_JSP_F32X2
+#define SDFGB_JSP_F32X2 0
+#endif
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void up2(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 constexpr int kSpWarps = 4, kSpStages = 6, kSpRX = 128, kSpPad = 8, kSpX = kSpRX - 2 * kSpPad;
 constexpr int kSpStageF = 3 * kSpRX;  // floats per stage (3 rows)
 // per warp: the TMA ring, then [plane 0/1][rows] of its border column
@@ -602,6 +623,30 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
     }
     __syncwarp();
 
+#if SDFGB_JSP_F32X2
+    // packed pairs (points 0,1) and (2,3): per point still
+    // coef * ((((c + n) + s) + w) + e), each add.rn/mul.rn.f32x2 lane rounding
+    // exactly like the scalar op; w/e of the pairs: (lft, c0) / (c1, c2) and
+    // (c1, c2) / (c3, rgt)
+    const uint64_t cf2 = pk2(coef, coef);
+    auto calc = [&](const float4& nq, const float4& cq, const float4& sq) -> float4 {
+        const float lft = __shfl_up_sync(0xffffffffu, cq.w, 1);
+        const float rgt = __shfl_down_sync(0xffffffffu, cq.x, 1);
+        const uint64_t x12 = pk2(cq.y, cq.z);
+        uint64_t a = add2(pk2(cq.x, cq.y), pk2(nq.x, nq.y));
+        uint64_t b = add2(pk2(cq.z, cq.w), pk2(nq.z, nq.w));
+        a = add2(a, pk2(sq.x, sq.y));
+        b = add2(b, pk2(sq.z, sq.w));
+        a = add2(a, pk2(lft, cq.x));
+        b = add2(b, x12);
+        a = add2(a, x12);
+        b = add2(b, pk2(cq.w, rgt));
+        float4 o;
+        up2(mul2(cf2, a), o.x, o.y);
+        up2(mul2(cf2, b), o.z, o.w);
+        return o;
+    };
+#else
     auto calc = [&](const float4& nq, const float4& cq, const float4& sq) -> float4 {
         const float lft = __shfl_up_sync(0xffffffffu, cq.w, 1);
         const float rgt = __shfl_down_sync(0xffffffffu, cq.x, 1);
@@ -621,6 +666,7 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
         }
         return make_float4(o[0], o[1], o[2], o[3]);
     };
+#endif
     // level k's border row r (0 or M-1) from plane p ^ (k & 1).  gx and N
     // are multiples of 4: a lane's four columns are all inside the plane or
     // all outside; column 0 is a lane's .x, column N-1 a lane's .w
