@@ -574,19 +574,45 @@ __host__ __device__ constexpr size_t sp_smem(int nrows) {
     return (size_t)kSpWarps * sp_warp_floats(nrows) * 4 + kSpWarps * kSpStages * 8;
 }
 
+#ifndef SDFGB_JSP_TIMING
+#define SDFGB_JSP_TIMING 0  // debug builds: per-warp start/end times (tools/jacobi_timing.py)
+#endif
+#if SDFGB_JSP_TIMING
+constexpr int kSpTimingMax = 1 << 16;
+__device__ uint64_t g_sp_timing[kSpTimingMax * 4];
+#endif
 template <int F>
 __global__ void __launch_bounds__(kSpWarps * 32, 4)
 jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* src, const float* dst_in,
-                    float* dst, int M, int N, int ra, int rb, int ntiles, int nstrips, int nwarps, float coef) {
+                    float* dst, int M, int N, int ra, int rb, int ntiles, int ntb, int nstrips, int nwarps,
+                    float coef) {
     // output rows [ra, rb) of the plane (the whole plane, or one band of it)
     extern __shared__ __align__(1024) float sp_smem_f[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = blockIdx.x * kSpWarps + warp;
     if (g >= nwarps) return;  // warp-uniform; warps never synchronise with each other
-    const int strip = g % nstrips, tile = g / nstrips;
-    // tiles split the rows evenly (every tile >= 2F+2 rows, so only a
-    // tile's checked tail can meet plane row M-1 and its prologue row 0)
-    const int y0 = ra + (int)((int64_t)tile * (rb - ra) / ntiles), ye = ra + (int)((int64_t)(tile + 1) * (rb - ra) / ntiles);
+    // the two border-column strips' warps first (they are the slowest, so
+    // they start in the first wave), then the interior strips, row-tile major
+    // The two border-column strips come first and are cut into ntb >= ntiles
+    // shorter tiles: their fix-ups make a row cost more, so shorter tiles
+    // starting in the first wave keep them off the launch's tail.
+    int strip, tile, nt;
+    {
+        const int nbw = 2 * ntb;  // (the host guarantees nstrips >= 2)
+        if (g < nbw) {
+            strip = (g & 1) ? nstrips - 1 : 0;
+            tile = g >> 1;
+            nt = ntb;
+        } else {
+            const int gi = g - nbw, ni = nstrips - 2;
+            strip = 1 + gi % ni;
+            tile = gi / ni;
+            nt = ntiles;
+        }
+    }
+    // tiles split the rows evenly (every tile >= 16 rows, so only a tile's
+    // checked tail can meet plane row M-1 and its prologue row 0)
+    const int y0 = ra + (int)((int64_t)tile * (rb - ra) / nt), ye = ra + (int)((int64_t)(tile + 1) * (rb - ra) / nt);
     const int H = (rb - ra + ntiles - 1) / ntiles;  // the tallest tile (smem sizing)
     const int gx0 = strip * kSpX - kSpPad, gx = gx0 + 4 * lane;
     const int nrows = (ye - y0) + 2 * F;  // input rows y0-F .. ye-1+F
@@ -612,13 +638,27 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
     // narrower than two strips to the one-step kernel)
     const bool colb = gx0 <= 0 || gx0 + kSpRX - 1 >= N - 1;
     if (colb) {  // both planes' border column over the strip's input rows
+        // (one float per row, 32 KB apart: eight rows per lane in flight at
+        // once, or the scattered loads' latency stalls this warp ~10 us)
         const int c = gx0 <= 0 ? 0 : N - 1;
-        for (int i = lane; i < nrows; i += 32) {
-            const int r = y0 - F + i;
-            const bool in = r >= 0 && r < M;
-            const int64_t o = (int64_t)r * N + c;
-            bcol[i] = in ? src[o] : 0.f;
-            bcol[RP + i] = in ? dst_in[o] : 0.f;
+        for (int i0 = 0; i0 < nrows; i0 += 8 * 32) {
+            float vs[8], vd[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = i0 + j * 32 + lane, r = y0 - F + i;
+                const bool in = i < nrows && r >= 0 && r < M;
+                const int64_t o = (int64_t)(in ? r : 0) * N + c;
+                vs[j] = in ? __ldg(src + o) : 0.f;
+                vd[j] = in ? dst_in[o] : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = i0 + j * 32 + lane;
+                if (i < nrows) {
+                    bcol[i] = vs[j];
+                    bcol[RP + i] = vd[j];
+                }
+            }
         }
     }
     __syncwarp();
@@ -704,11 +744,7 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
                 while (!__all_sync(0xffffffffu, mbar_try_wait(a, par))) {
                 }
             }
-            // border-column values: level k's is read one level ahead
-            float bnext = 0.f;
-            if constexpr (COLB) {
-                if (MODE != 1 || PRO >= 2) bnext = bcol[RP + p - 1];
-            }
+
             // level 0 is read from the ring, not kept in registers: rows
             // p-2 .. p (the previous stage is refilled one stage late)
             auto l0 = [&](int q) {  // q = u - 2 .. u
@@ -718,13 +754,10 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
 #pragma unroll
             for (int k = 1; k < F; ++k) {
                 if (MODE != 1 || PRO >= 2 * k) {
-                    const float bk = bnext;
-                    if constexpr (COLB) {
-                        if (k + 1 < F) bnext = bcol[((k + 1) & 1) * RP + p - k - 1];
-                    }
                     w[k][u] = k == 1 ? calc(l0(u - 2), l0(u - 1), l0(u))
                                      : calc(w[k - 1][sn], w[k - 1][sc], w[k - 1][u]);
-                    if constexpr (COLB) {
+                    if constexpr (COLB) {  // this level's border column value (plane p ^ (k & 1))
+                        const float bk = bcol[(k & 1) * RP + p - k];
                         if (cw) w[k][u].x = bk;
                         if (ce) w[k][u].w = bk;
                     }
@@ -745,15 +778,18 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
                 float* d = dst + (int64_t)r * N + gx;
                 if constexpr (!COLB) {
                     if (keep) *reinterpret_cast<float4*>(d) = o;
-                } else if (keep) {
-                    if (gx >= 1 && gx + 3 <= N - 2) {
-                        *reinterpret_cast<float4*>(d) = o;
-                    } else {
-                        const float e[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            if (gx + j >= 1 && gx + j <= N - 2) d[j] = e[j];
-                    }
+                } else {
+                    // predicated stores only (no lane-divergent branch, which
+                    // would wrap the next shuffles in warp re-convergence):
+                    // whole float4s inside the interior, single columns at
+                    // the border lanes
+                    const bool full = keep && gx >= 1 && gx + 3 <= N - 2;
+                    const bool part = keep && !full;
+                    if (full) *reinterpret_cast<float4*>(d) = o;
+                    if (part && gx >= 1 && gx <= N - 2) d[0] = o.x;
+                    if (part && gx + 1 >= 1 && gx + 1 <= N - 2) d[1] = o.y;
+                    if (part && gx + 2 >= 1 && gx + 2 <= N - 2) d[2] = o.z;
+                    if (part && gx + 3 >= 1 && gx + 3 <= N - 2) d[3] = o.w;
                 }
             }
             if constexpr (u == 2) {  // the previous stage is consumed (its last reads fed level 1): refill it
@@ -794,8 +830,28 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
             if (p + 2 < nrows) step(I2{}, p + 2, NP{}, M2{});
         }
     };
+#if SDFGB_JSP_TIMING
+    uint64_t t0 = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
+#ifdef SDFGB_JSP_NOCOLB_DEBUG  // timing experiments only: border strips without their fix-ups (wrong results)
+    sweep(std::false_type{});
+#else
     if (colb) sweep(std::true_type{});
     else sweep(std::false_type{});
+#endif
+#if SDFGB_JSP_TIMING
+    uint64_t t1 = 0;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (lane == 0 && g < kSpTimingMax) {
+        g_sp_timing[g * 4 + 0] = t0;
+        g_sp_timing[g * 4 + 1] = t1;
+        g_sp_timing[g * 4 + 2] = smid;
+        g_sp_timing[g * 4 + 3] = (uint64_t)colb | ((uint64_t)tile << 8) | ((uint64_t)strip << 32);
+    }
+#endif
 }
 
 // tiles per strip: ~four co-resident waves of warps (4 CTAs x 4 warps per
@@ -826,10 +882,12 @@ int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra,
     CUtensorMap map;
     SDFGB_TRY(encode_tiled_2d(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, src, M, N, kSpRX, 3,
                               CU_TENSOR_MAP_SWIZZLE_NONE));
-    const int64_t nwarps = nstrips * ntiles;
+    // border strips: twice the tiles (rows per tile >= 16)
+    const int ntb = (int)std::max<int64_t>(ntiles, std::min<int64_t>(2 * ntiles, (rb - ra) / 16));
+    const int64_t nwarps = 2 * ntb + (nstrips - 2) * ntiles;
     const unsigned blocks = (unsigned)((nwarps + kSpWarps - 1) / kSpWarps);
     jacobi_strip_kernel<F><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, (int)ra, (int)rb,
-                                                               ntiles, (int)nstrips, (int)nwarps, coef);
+                                                               ntiles, ntb, (int)nstrips, (int)nwarps, coef);
     SDFGB_LAUNCHED("jacobi_strip_kernel");
     return SDFGB_OK;
 }
@@ -993,3 +1051,9 @@ extern "C" int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, 
     if (k == 3) return sdfgb::launch_strip<3>(src, dst, M, N, r0, r1, (float)coef, s);
     return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k must be 1, 3, 5 or 7 (got %lld)", (long long)k);
 }
+
+#if SDFGB_JSP_TIMING
+extern "C" int sdfgb_debug_strip_timing(uint64_t* host, int64_t n) {
+    return sdfgb::check_cuda(cudaMemcpyFromSymbol(host, sdfgb::g_sp_timing, (size_t)n * 32), "timing");
+}
+#endif
