@@ -20,6 +20,7 @@
 //   * the canonical c,n,s,w,e order is a compile-time fast path; any other
 //     order of up to 9 neighbours runs the same kernel through a select chain.
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 
 #include "tma.cuh"
@@ -581,87 +582,58 @@ __host__ __device__ constexpr size_t sp_smem(int nrows) {
 constexpr int kSpTimingMax = 1 << 16;
 __device__ uint64_t g_sp_timing[kSpTimingMax * 4];
 #endif
+// How one launch cuts its output rows [ra, rb) of every strip into tiles:
+// nbig tall tiles over [ra, rsplit) and nsmall short ones over [rsplit, rb)
+// (nbigb / nsmallb for the two border-column strips).
+struct StripPlan {
+    int ra, rb, rsplit, nbig, nsmall, nbigb, nsmallb, nstrips, hmax;
+    __host__ __device__ int group(int g) const {
+        return g == 0 ? 2 * nbigb + (nstrips - 2) * nbig : 2 * nsmallb + (nstrips - 2) * nsmall;
+    }
+    __host__ __device__ int total() const { return group(0) + group(1); }
+};
+
+constexpr int kSpSchedSlots = 4096;
+// per-launch work counters (next tile, warps done), zero between launches:
+// the last warp of a launch re-zeroes its pair; launches rotate over slots
+__device__ int g_sp_sched[kSpSchedSlots * 2];
+
 template <int F>
 __global__ void __launch_bounds__(kSpWarps * 32, 4)
 jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* src, const float* dst_in,
-                    float* dst, int M, int N, int ra, int rb, int ntiles, int ntb, int nstrips, int nwarps,
-                    float coef) {
-    // output rows [ra, rb) of the plane (the whole plane, or one band of it)
+                    float* dst, int M, int N, StripPlan plan, int nwarps, int sched_slot, float coef) {
+    // output rows [ra, rb) of the plane (the whole plane, or one band of it).
+    // Persistent warps: each takes tiles from the launch's counter until
+    // none are left, so the tiles' uneven durations balance out and no
+    // block-launch gaps open between waves.
     extern __shared__ __align__(1024) float sp_smem_f[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = blockIdx.x * kSpWarps + warp;
     if (g >= nwarps) return;  // warp-uniform; warps never synchronise with each other
-    // the two border-column strips' warps first (they are the slowest, so
-    // they start in the first wave), then the interior strips, row-tile major
-    // The two border-column strips come first and are cut into ntb >= ntiles
-    // shorter tiles: their fix-ups make a row cost more, so shorter tiles
-    // starting in the first wave keep them off the launch's tail.
-    int strip, tile, nt;
-    {
-        const int nbw = 2 * ntb;  // (the host guarantees nstrips >= 2)
-        if (g < nbw) {
-            strip = (g & 1) ? nstrips - 1 : 0;
-            tile = g >> 1;
-            nt = ntb;
-        } else {
-            const int gi = g - nbw, ni = nstrips - 2;
-            strip = 1 + gi % ni;
-            tile = gi / ni;
-            nt = ntiles;
-        }
-    }
-    // tiles split the rows evenly (every tile >= 16 rows, so only a tile's
-    // checked tail can meet plane row M-1 and its prologue row 0)
-    const int y0 = ra + (int)((int64_t)tile * (rb - ra) / nt), ye = ra + (int)((int64_t)(tile + 1) * (rb - ra) / nt);
-    const int H = (rb - ra + ntiles - 1) / ntiles;  // the tallest tile (smem sizing)
-    const int gx0 = strip * kSpX - kSpPad, gx = gx0 + 4 * lane;
-    const int nrows = (ye - y0) + 2 * F;  // input rows y0-F .. ye-1+F
-    const int RP = sp_rows(H + 2 * F);  // border-column rows per (plane, side), as sized on the host
+    int* sched = g_sp_sched + 2 * sched_slot;
+    const int nstrips = plan.nstrips;
+    const int RP = sp_rows(plan.hmax + 2 * F);  // border-column rows per plane, as sized on the host
     float* ring = sp_smem_f + warp * (kSpStages * kSpStageF + 2 * RP);
     float* bcol = ring + kSpStages * kSpStageF;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sp_smem_f + kSpWarps * (kSpStages * kSpStageF + 2 * RP)) +
                      warp * kSpStages;
-    const int nst = (nrows + 2) / 3;
     if (lane == 0) {
 #pragma unroll
         for (int s = 0; s < kSpStages; ++s) mbar_init(bars + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#pragma unroll
-        for (int s = 0; s < kSpStages; ++s)
-            if (s < nst) {
-                mbar_expect_tx(bars + s, kSpStageF * 4);
-                tma_load_2d(ring + s * kSpStageF, &src_map, bars + s, gx0, y0 - F + 3 * s);
-            }
-    }
-    // a strip holds at most one border column (the host sends planes
-    // narrower than two strips to the one-step kernel)
-    const bool colb = gx0 <= 0 || gx0 + kSpRX - 1 >= N - 1;
-    if (colb) {  // both planes' border column over the strip's input rows
-        // (one float per row, 32 KB apart: eight rows per lane in flight at
-        // once, or the scattered loads' latency stalls this warp ~10 us)
-        const int c = gx0 <= 0 ? 0 : N - 1;
-        for (int i0 = 0; i0 < nrows; i0 += 8 * 32) {
-            float vs[8], vd[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int i = i0 + j * 32 + lane, r = y0 - F + i;
-                const bool in = i < nrows && r >= 0 && r < M;
-                const int64_t o = (int64_t)(in ? r : 0) * N + c;
-                vs[j] = in ? __ldg(src + o) : 0.f;
-                vd[j] = in ? dst_in[o] : 0.f;
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int i = i0 + j * 32 + lane;
-                if (i < nrows) {
-                    bcol[i] = vs[j];
-                    bcol[RP + i] = vd[j];
-                }
-            }
-        }
     }
     __syncwarp();
+#if SDFGB_JSP_TIMING
+    uint64_t t0 = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int ntaken = 0;
+#endif
+    auto grab = [&]() {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(sched, 1);
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
 
 #if SDFGB_JSP_F32X2
     // packed pairs (points 0,1) and (2,3): per point still
@@ -707,6 +679,73 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
         return make_float4(o[0], o[1], o[2], o[3]);
     };
 #endif
+    uint32_t sbase = 0;  // stages this warp has consumed before the current tile (ring slot / parity)
+    for (int t = grab(); t < plan.total(); t = grab()) {
+    // The queue: every strip's tall tiles (rows [ra, rsplit)), then its
+    // short ones ([rsplit, rb)), so the short tiles even out the end of the
+    // launch.  In each group the two border-column strips come first, cut
+    // into up to twice the tiles (their per-row fix-ups cost more); then the
+    // interior strips, row-tile major.  Tiles split their rows evenly,
+    // >= 16 rows each, so only a tile's checked tail can meet plane row M-1
+    // and only its prologue row 0.
+    int strip, tile, nt, lo, hi;
+    {
+        const bool big = t < plan.group(0);
+        const int u = big ? t : t - plan.group(0);
+        const int n = big ? plan.nbig : plan.nsmall, nb = big ? plan.nbigb : plan.nsmallb;
+        lo = big ? plan.ra : plan.rsplit;
+        hi = big ? plan.rsplit : plan.rb;
+        if (u < 2 * nb) {  // (the host guarantees nstrips >= 2)
+            strip = (u & 1) ? nstrips - 1 : 0;
+            tile = u >> 1;
+            nt = nb;
+        } else {
+            const int ui = u - 2 * nb, ni = nstrips - 2;
+            strip = 1 + ui % ni;
+            tile = ui / ni;
+            nt = n;
+        }
+    }
+    const int y0 = lo + (int)((int64_t)tile * (hi - lo) / nt), ye = lo + (int)((int64_t)(tile + 1) * (hi - lo) / nt);
+    const int gx0 = strip * kSpX - kSpPad, gx = gx0 + 4 * lane;
+    const int nrows = (ye - y0) + 2 * F;  // input rows y0-F .. ye-1+F
+    const int nst = (nrows + 2) / 3;
+    __syncwarp();  // the previous tile's last ring reads are done
+    if (lane == 0) {
+        for (int s = 0; s < kSpStages && s < nst; ++s) {
+            const int sl = (int)((sbase + s) % kSpStages);
+            mbar_expect_tx(bars + sl, kSpStageF * 4);
+            tma_load_2d(ring + sl * kSpStageF, &src_map, bars + sl, gx0, y0 - F + 3 * s);
+        }
+    }
+    // a strip holds at most one border column (the host sends planes
+    // narrower than two strips to the one-step kernel)
+    const bool colb = gx0 <= 0 || gx0 + kSpRX - 1 >= N - 1;
+    if (colb) {  // both planes' border column over the strip's input rows
+        // (one float per row, 32 KB apart: eight rows per lane in flight at
+        // once, or the scattered loads' latency stalls this warp ~10 us)
+        const int c = gx0 <= 0 ? 0 : N - 1;
+        for (int i0 = 0; i0 < nrows; i0 += 8 * 32) {
+            float vs[8], vd[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = i0 + j * 32 + lane, r = y0 - F + i;
+                const bool in = i < nrows && r >= 0 && r < M;
+                const int64_t o = (int64_t)(in ? r : 0) * N + c;
+                vs[j] = in ? __ldg(src + o) : 0.f;
+                vd[j] = in ? dst_in[o] : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = i0 + j * 32 + lane;
+                if (i < nrows) {
+                    bcol[i] = vs[j];
+                    bcol[RP + i] = vd[j];
+                }
+            }
+        }
+    }
+    __syncwarp();
     // level k's border row r (0 or M-1) from plane p ^ (k & 1).  gx and N
     // are multiples of 4: a lane's four columns are all inside the plane or
     // all outside; column 0 is a lane's .x, column N-1 a lane's .w
@@ -732,15 +771,15 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
             constexpr int PRO = decltype(pro_tag)::value;
             constexpr int MODE = decltype(mode_tag)::value;
             constexpr int sn = (u + 1) % 3, sc = (u + 2) % 3;
-            const int it = p / 3;
-            const int slot = it % kSpStages, pslot = (it + kSpStages - 1) % kSpStages;
+            const int it = p / 3;  // this tile's stage; the ring runs on across tiles
+            const int slot = (int)((sbase + it) % kSpStages), pslot = (int)((sbase + it + kSpStages - 1) % kSpStages);
             float* stage = ring + slot * kSpStageF;
             const float* prev = ring + pslot * kSpStageF;
             if constexpr (u == 0) {
                 // every lane polls and the loop condition is a warp vote, so
                 // the warp stays provably converged and the shuffles stay
                 // plain SHFLs
-                const uint32_t a = smem_u32(bars + slot), par = (uint32_t)((it / kSpStages) & 1);
+                const uint32_t a = smem_u32(bars + slot), par = (uint32_t)(((sbase + it) / kSpStages) & 1);
                 while (!__all_sync(0xffffffffu, mbar_try_wait(a, par))) {
                 }
             }
@@ -830,16 +869,19 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
             if (p + 2 < nrows) step(I2{}, p + 2, NP{}, M2{});
         }
     };
-#if SDFGB_JSP_TIMING
-    uint64_t t0 = 0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-#endif
-#ifdef SDFGB_JSP_NOCOLB_DEBUG  // timing experiments only: border strips without their fix-ups (wrong results)
-    sweep(std::false_type{});
-#else
     if (colb) sweep(std::true_type{});
     else sweep(std::false_type{});
+    sbase += nst;
+#if SDFGB_JSP_TIMING
+    ntaken += 1 + (colb ? 1000 : 0);
 #endif
+    }  // tiles
+    // the launch's last warp re-zeroes the counters for the next launch on this slot
+    if (lane == 0 && atomicAdd(sched + 1, 1) == nwarps - 1) {
+        sched[0] = 0;
+        sched[1] = 0;
+        __threadfence();
+    }
 #if SDFGB_JSP_TIMING
     uint64_t t1 = 0;
     uint32_t smid;
@@ -849,30 +891,51 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
         g_sp_timing[g * 4 + 0] = t0;
         g_sp_timing[g * 4 + 1] = t1;
         g_sp_timing[g * 4 + 2] = smid;
-        g_sp_timing[g * 4 + 3] = (uint64_t)colb | ((uint64_t)tile << 8) | ((uint64_t)strip << 32);
+        g_sp_timing[g * 4 + 3] = (uint64_t)(ntaken >= 1000) | ((uint64_t)(ntaken % 1000) << 8);
     }
 #endif
 }
 
-// tiles per strip: ~four co-resident waves of warps (4 CTAs x 4 warps per
-// SM) so the edge warps balance out, each tile >= 64 rows
-int strip_tiles(int64_t M, int64_t nstrips) {
-    static int forced = -1;
-    if (forced < 0) {
-        const char* e = getenv("SDFGB_J_STRIP_H");
-        forced = e ? atoi(e) : 0;
-    }
-    const int64_t H = forced > 0 ? forced
-                                 : std::max<int64_t>(64, M / std::max<int64_t>(1, ((int64_t)num_sms() * 64 + nstrips - 1) / nstrips));
-    return (int)std::max<int64_t>(1, std::min<int64_t>(M / 16, (M + H - 1) / H));
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+// Tiles of one launch: tall tiles (SDFGB_J_STRIP_H rows, default 256: the
+// cone recomputation of a tile's first 2F rows is 2 % there) for most rows,
+// then about one short tile (SDFGB_J_STRIP_HS rows, default 32) per
+// resident warp, queued last, so the persistent warps finish together.
+StripPlan strip_plan(int64_t ra, int64_t rb, int64_t nstrips, int64_t resident_warps) {
+    static const int hb = std::max(32, env_int("SDFGB_J_STRIP_H", 256));
+    static const int hs = std::max(32, env_int("SDFGB_J_STRIP_HS", 32));
+    static const int spw = std::max(0, env_int("SDFGB_J_STRIP_SMALL", 1));  // short tiles per warp
+    StripPlan p{};
+    p.ra = (int)ra;
+    p.rb = (int)rb;
+    p.nstrips = (int)nstrips;
+    const int64_t rows = rb - ra;
+    int64_t rs = std::min<int64_t>(rows, (resident_warps * spw + nstrips - 1) / nstrips * hs);
+    int64_t nbig = (rows - rs) / hb;
+    if (nbig == 0) rs = rows;  // too few rows for a tall tile: all short
+    p.rsplit = (int)(rb - rs);
+    p.nbig = (int)nbig;
+    p.nsmall = (int)std::max<int64_t>(1, std::min<int64_t>(rs / hs, rs / 16));
+    if (rs < 16) p.nsmall = 1;  // a band of 8..15 rows: one tile
+    p.nbigb = (int)std::min<int64_t>(2 * nbig, (rows - rs) / 16);
+    p.nsmallb = (int)std::max<int64_t>(1, std::min<int64_t>(2 * p.nsmall, rs / 16));
+    const int64_t hbig = nbig ? (rows - rs + nbig - 1) / nbig : 0;
+    p.hmax = (int)std::max<int64_t>(hbig, (rs + p.nsmall - 1) / p.nsmall);
+    return p;
 }
 
 template <int F>
 int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra, int64_t rb, float coef,
                  cudaStream_t s) {
     const int64_t nstrips = (N + kSpX - 1) / kSpX;
-    const int ntiles = strip_tiles(rb - ra, nstrips);
-    const size_t smem = sp_smem((int)((rb - ra + ntiles - 1) / ntiles) + 2 * F);
+    // persistent: one co-resident wave of warps (4 CTAs x 4 warps per SM)
+    const int64_t resident = (int64_t)num_sms() * 4 * kSpWarps;
+    const StripPlan plan = strip_plan(ra, rb, nstrips, resident);
+    const size_t smem = sp_smem(plan.hmax + 2 * F);
     static size_t attr = 0;
     if (smem > attr) {
         SDFGB_CUDA(cudaFuncSetAttribute(jacobi_strip_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -882,12 +945,19 @@ int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra,
     CUtensorMap map;
     SDFGB_TRY(encode_tiled_2d(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, src, M, N, kSpRX, 3,
                               CU_TENSOR_MAP_SWIZZLE_NONE));
-    // border strips: twice the tiles (rows per tile >= 16)
-    const int ntb = (int)std::max<int64_t>(ntiles, std::min<int64_t>(2 * ntiles, (rb - ra) / 16));
-    const int64_t nwarps = 2 * ntb + (nstrips - 2) * ntiles;
+    static int per_sm = 0;
+    static size_t per_sm_smem = 0;
+    if (!per_sm || per_sm_smem != smem) {
+        per_sm_smem = smem;
+        SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_strip_kernel<F>, kSpWarps * 32, smem));
+        per_sm = std::max(per_sm, 1);
+    }
+    const int64_t nwarps = std::min<int64_t>(plan.total(), (int64_t)num_sms() * per_sm * kSpWarps);
     const unsigned blocks = (unsigned)((nwarps + kSpWarps - 1) / kSpWarps);
-    jacobi_strip_kernel<F><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, (int)ra, (int)rb,
-                                                               ntiles, ntb, (int)nstrips, (int)nwarps, coef);
+    static std::atomic<int> launches{0};
+    const int slot = launches.fetch_add(1) & (kSpSchedSlots - 1);
+    jacobi_strip_kernel<F><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, plan, (int)nwarps,
+                                                               slot, coef);
     SDFGB_LAUNCHED("jacobi_strip_kernel");
     return SDFGB_OK;
 }

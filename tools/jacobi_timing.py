@@ -30,7 +30,8 @@ dur = end - start
 colb = (t[:, 3] & 0xff).astype(bool)
 print(f"warps {len(t)}  launch span {end.max():.1f} us  warp duration median {np.median(dur):.1f} "
       f"p10 {np.percentile(dur, 10):.1f} p90 {np.percentile(dur, 90):.1f} max {dur.max():.1f} us")
-print(f"border-column warps: median {np.median(dur[colb]):.1f} us ({colb.sum()} warps); others {np.median(dur[~colb]):.1f}")
+ntile = ((t[:, 3] >> 8) & 0xffffff).astype(int)
+print(f"warps that took border tiles: {colb.sum()}; tiles per warp min {ntile.min()} median {np.median(ntile):.0f} max {ntile.max()}")
 print("end-time percentiles (us):", " ".join(f"p{q}={np.percentile(end, q):.1f}" for q in (50, 90, 99, 100)))
 sm = t[:, 2].astype(int)
 busy = np.array([dur[sm == i].sum() for i in range(sm.max() + 1)])

@@ -23,11 +23,12 @@ if [ "${1:-}" = "build" ]; then
   wait
   exit 0
 fi
-# run [H ...]: also sweep the strip height (SDFGB_J_STRIP_H) per library
+# run [H[/HS] ...]: also sweep the tall / short tile heights (SDFGB_J_STRIP_H / _HS) per library
 shift
 for f in $OUT/lib_*.so; do
-  for H in ${@:-0}; do
-    SDFGB_J_STRIP_H=$H SDFGB_LIB=$f timeout 300 python bench.py --motif jacobi2d --steps 3 --warmup 3 --no-e2e --no-cpu \
-      | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); m=d['motifs']['jacobi2d']; print('$(basename $f) H=$H', m['ms'], 'ms/1000 steps', m['ok'])"
+  for HH in ${@:-256/32}; do
+    H=${HH%%/*}; HS=${HH##*/}
+    SDFGB_J_STRIP_H=$H SDFGB_J_STRIP_HS=$HS SDFGB_LIB=$f timeout 300 python bench.py --motif jacobi2d --steps 3 --warmup 3 --no-e2e --no-cpu \
+      | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); m=d['motifs']['jacobi2d']; print('$(basename $f) H=$H HS=$HS', m['ms'], 'ms/1000 steps', m['ok'])"
   done
 done
