@@ -33,7 +33,7 @@ namespace sdfgb {
 namespace {
 
 #ifndef SDFGB_H_BLOCK
-#define SDFGB_H_BLOCK 512
+#define SDFGB_H_BLOCK 1024  // one CTA per SM: 13.3 -> 13.0 us at 4096^2 (profiles/r2_hist_variants.txt)
 #endif
 #ifndef SDFGB_H_UNROLL
 #define SDFGB_H_UNROLL 4
