@@ -155,6 +155,12 @@ int sdfgb_jacobi2d_block_f32(const float* src, float* dst, int64_t M, int64_t N,
  * needs N >= 128 and at least 8 interior rows. */
 int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k,
                             int64_t r0, int64_t r1, double coef, void* stream);
+/* Host-only introspection of the strip kernel's tile queue for output rows
+ * [r0, r1) of an M x N plane and `resident` persistent warps: tiles[3t..3t+2]
+ * = (strip, y0, ye) of entry t (at most max_tiles written); returns the
+ * number of entries.  Used by the CPU tests. */
+int64_t sdfgb_debug_strip_tiles(int64_t M, int64_t N, int64_t r0, int64_t r1, int64_t resident,
+                                int32_t* tiles, int64_t max_tiles);
 
 /* GEMM after MapReduceFusion (library.py:461-554): C = A(MxK) * B(KxN),
  * row-major fp32, fp32-accurate through 3xTF32 on tcgen05 tensor cores.

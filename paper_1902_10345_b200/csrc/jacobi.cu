@@ -591,6 +591,26 @@ struct StripPlan {
         return g == 0 ? 2 * nbigb + (nstrips - 2) * nbig : 2 * nsmallb + (nstrips - 2) * nsmall;
     }
     __host__ __device__ int total() const { return group(0) + group(1); }
+    // queue entry t -> strip and output rows [y0, ye)
+    __host__ __device__ void tile(int t, int& strip, int& y0, int& ye) const {
+        const bool big = t < group(0);
+        const int u = big ? t : t - group(0);
+        const int n = big ? nbig : nsmall, nb = big ? nbigb : nsmallb;
+        const int lo = big ? ra : rsplit, hi = big ? rsplit : rb;
+        int tl, nt;
+        if (u < 2 * nb) {  // (the host guarantees nstrips >= 2)
+            strip = (u & 1) ? nstrips - 1 : 0;
+            tl = u >> 1;
+            nt = nb;
+        } else {
+            const int ui = u - 2 * nb, ni = nstrips - 2;
+            strip = 1 + ui % ni;
+            tl = ui / ni;
+            nt = n;
+        }
+        y0 = lo + (int)((int64_t)tl * (hi - lo) / nt);
+        ye = lo + (int)((int64_t)(tl + 1) * (hi - lo) / nt);
+    }
 };
 
 constexpr int kSpSchedSlots = 4096;
@@ -688,25 +708,8 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
     // interior strips, row-tile major.  Tiles split their rows evenly,
     // >= 16 rows each, so only a tile's checked tail can meet plane row M-1
     // and only its prologue row 0.
-    int strip, tile, nt, lo, hi;
-    {
-        const bool big = t < plan.group(0);
-        const int u = big ? t : t - plan.group(0);
-        const int n = big ? plan.nbig : plan.nsmall, nb = big ? plan.nbigb : plan.nsmallb;
-        lo = big ? plan.ra : plan.rsplit;
-        hi = big ? plan.rsplit : plan.rb;
-        if (u < 2 * nb) {  // (the host guarantees nstrips >= 2)
-            strip = (u & 1) ? nstrips - 1 : 0;
-            tile = u >> 1;
-            nt = nb;
-        } else {
-            const int ui = u - 2 * nb, ni = nstrips - 2;
-            strip = 1 + ui % ni;
-            tile = ui / ni;
-            nt = n;
-        }
-    }
-    const int y0 = lo + (int)((int64_t)tile * (hi - lo) / nt), ye = lo + (int)((int64_t)(tile + 1) * (hi - lo) / nt);
+    int strip, y0, ye;
+    plan.tile(t, strip, y0, ye);
     const int gx0 = strip * kSpX - kSpPad, gx = gx0 + 4 * lane;
     const int nrows = (ye - y0) + 2 * F;  // input rows y0-F .. ye-1+F
     const int nst = (nrows + 2) / 3;
@@ -1127,3 +1130,18 @@ extern "C" int sdfgb_debug_strip_timing(uint64_t* host, int64_t n) {
     return sdfgb::check_cuda(cudaMemcpyFromSymbol(host, sdfgb::g_sp_timing, (size_t)n * 32), "timing");
 }
 #endif
+
+// The tile queue of one strip-kernel launch over output rows [r0, r1) of an
+// M x N plane with `resident` persistent warps: tiles[3 t + {0,1,2}] =
+// (strip, y0, ye) of queue entry t, for up to max_tiles entries.  Returns
+// the number of entries (host only: the CPU tests check that the queue
+// covers every strip's rows exactly once, in tiles of >= 16 rows).
+extern "C" int64_t sdfgb_debug_strip_tiles(int64_t M, int64_t N, int64_t r0, int64_t r1, int64_t resident,
+                                           int32_t* tiles, int64_t max_tiles) {
+    (void)M;
+    const int64_t nstrips = (N + sdfgb::kSpX - 1) / sdfgb::kSpX;
+    const sdfgb::StripPlan plan = sdfgb::strip_plan(r0, r1, nstrips, resident);
+    const int total = plan.total();
+    for (int t = 0; t < total && t < max_tiles; ++t) plan.tile(t, tiles[3 * t], tiles[3 * t + 1], tiles[3 * t + 2]);
+    return total;
+}
