@@ -906,11 +906,12 @@ int env_int(const char* name, int dflt) {
 
 // Tiles of one launch: tall tiles (SDFGB_J_STRIP_H rows, default 256: the
 // cone recomputation of a tile's first 2F rows is 2 % there) for most rows,
-// then about one short tile (SDFGB_J_STRIP_HS rows, default 32) per
-// resident warp, queued last, so the persistent warps finish together.
+// then about one short tile (SDFGB_J_STRIP_HS rows, default 16) per
+// resident warp, queued last, so the persistent warps finish together
+// (profiles/r2_jacobi_persistent.txt).
 StripPlan strip_plan(int64_t ra, int64_t rb, int64_t nstrips, int64_t resident_warps) {
     static const int hb = std::max(32, env_int("SDFGB_J_STRIP_H", 256));
-    static const int hs = std::max(32, env_int("SDFGB_J_STRIP_HS", 32));
+    static const int hs = std::max(16, env_int("SDFGB_J_STRIP_HS", 16));
     static const int spw = std::max(0, env_int("SDFGB_J_STRIP_SMALL", 1));  // short tiles per warp
     StripPlan p{};
     p.ra = (int)ra;
@@ -924,10 +925,11 @@ StripPlan strip_plan(int64_t ra, int64_t rb, int64_t nstrips, int64_t resident_w
     p.nbig = (int)nbig;
     p.nsmall = (int)std::max<int64_t>(1, std::min<int64_t>(rs / hs, rs / 16));
     if (rs < 16) p.nsmall = 1;  // a band of 8..15 rows: one tile
+    if (rs == 0) p.nsmall = 0;  // no short tiles at all (SDFGB_J_STRIP_SMALL=0)
     p.nbigb = (int)std::min<int64_t>(2 * nbig, (rows - rs) / 16);
-    p.nsmallb = (int)std::max<int64_t>(1, std::min<int64_t>(2 * p.nsmall, rs / 16));
+    p.nsmallb = rs ? (int)std::max<int64_t>(1, std::min<int64_t>(2 * p.nsmall, rs / 16)) : 0;
     const int64_t hbig = nbig ? (rows - rs + nbig - 1) / nbig : 0;
-    p.hmax = (int)std::max<int64_t>(hbig, (rs + p.nsmall - 1) / p.nsmall);
+    p.hmax = (int)std::max<int64_t>(hbig, p.nsmall ? (rs + p.nsmall - 1) / p.nsmall : 0);
     return p;
 }
 

@@ -26,9 +26,9 @@ fi
 # run [H[/HS] ...]: also sweep the tall / short tile heights (SDFGB_J_STRIP_H / _HS) per library
 shift
 for f in $OUT/lib_*.so; do
-  for HH in ${@:-256/32}; do
-    H=${HH%%/*}; HS=${HH##*/}
-    SDFGB_J_STRIP_H=$H SDFGB_J_STRIP_HS=$HS SDFGB_LIB=$f timeout 300 python bench.py --motif jacobi2d --steps 3 --warmup 3 --no-e2e --no-cpu \
-      | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); m=d['motifs']['jacobi2d']; print('$(basename $f) H=$H HS=$HS', m['ms'], 'ms/1000 steps', m['ok'])"
+  for HH in ${@:-256/32/1}; do
+    IFS=/ read H HS SM <<< "$HH"
+    SDFGB_J_STRIP_H=$H SDFGB_J_STRIP_HS=$HS SDFGB_J_STRIP_SMALL=${SM:-1} SDFGB_LIB=$f timeout 300 python bench.py --motif jacobi2d --steps 3 --warmup 3 --no-e2e --no-cpu \
+      | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); m=d['motifs']['jacobi2d']; print('$(basename $f) H=$H HS=$HS SMALL=${SM:-1}', m['ms'], 'ms/1000 steps', m['ok'])"
   done
 done
