@@ -547,6 +547,9 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* dst_in,
 #ifndef SDFGB_JSP_F32X2
 #define SDFGB_JSP_F32X2 0
 #endif
+#ifndef SDFGB_JSP_L0REG
+#define SDFGB_JSP_L0REG 1  // level 0 kept in the register window (1 LDS per row instead of 3; 19.43 -> 19.2 ms per J1 loop)
+#endif
 __device__ __forceinline__ uint64_t pk2(float lo, float hi) {
     uint64_t r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
@@ -793,11 +796,19 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
                 const float* b = q >= 0 ? stage + q * kSpRX : prev + (q + 3) * kSpRX;
                 return *reinterpret_cast<const float4*>(b + 4 * lane);
             };
+#if SDFGB_JSP_L0REG
+            // the new row only; rows p-2 and p-1 are still in the register window
+            w[0][u] = *reinterpret_cast<const float4*>(stage + u * kSpRX + 4 * lane);
+#endif
 #pragma unroll
             for (int k = 1; k < F; ++k) {
                 if (MODE != 1 || PRO >= 2 * k) {
+#if SDFGB_JSP_L0REG
+                    w[k][u] = calc(w[k - 1][sn], w[k - 1][sc], w[k - 1][u]);
+#else
                     w[k][u] = k == 1 ? calc(l0(u - 2), l0(u - 1), l0(u))
                                      : calc(w[k - 1][sn], w[k - 1][sc], w[k - 1][u]);
+#endif
                     if constexpr (COLB) {  // this level's border column value (plane p ^ (k & 1))
                         const float bk = bcol[(k & 1) * RP + p - k];
                         if (cw) w[k][u].x = bk;
@@ -834,6 +845,17 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
                     if (part && gx + 3 >= 1 && gx + 3 <= N - 2) d[3] = o.w;
                 }
             }
+#if SDFGB_JSP_L0REG
+            if constexpr (u == 2) {  // this stage's three rows are in registers: refill it
+                __syncwarp();
+                const int nx = it + kSpStages;
+                if (lane == 0 && nx < nst) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(bars + slot, kSpStageF * 4);
+                    tma_load_2d(stage, &src_map, bars + slot, gx0, y0 - F + 3 * nx);
+                }
+            }
+#else
             if constexpr (u == 2) {  // the previous stage is consumed (its last reads fed level 1): refill it
                 __syncwarp();
                 const int nx = it - 1 + kSpStages;
@@ -844,6 +866,7 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
                                 y0 - F + 3 * nx);
                 }
             }
+#endif
         };
         using I0 = std::integral_constant<int, 0>;
         using I1 = std::integral_constant<int, 1>;
