@@ -618,8 +618,11 @@ struct StripPlan {
 
 constexpr int kSpSchedSlots = 4096;
 // per-launch work counters (next tile, warps done), zero between launches:
-// the last warp of a launch re-zeroes its pair; launches rotate over slots
+// the last warp of a launch re-zeroes its pair; launches (of every F, from
+// every host thread) rotate over the slots, so concurrent launches on
+// different streams use different counters
 __device__ int g_sp_sched[kSpSchedSlots * 2];
+std::atomic<int> g_sp_launches{0};
 
 template <int F>
 __global__ void __launch_bounds__(kSpWarps * 32, 4)
@@ -982,8 +985,7 @@ int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra,
     }
     const int64_t nwarps = std::min<int64_t>(plan.total(), (int64_t)num_sms() * per_sm * kSpWarps);
     const unsigned blocks = (unsigned)((nwarps + kSpWarps - 1) / kSpWarps);
-    static std::atomic<int> launches{0};
-    const int slot = launches.fetch_add(1) & (kSpSchedSlots - 1);
+    const int slot = g_sp_launches.fetch_add(1) & (kSpSchedSlots - 1);
     jacobi_strip_kernel<F><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, plan, (int)nwarps,
                                                                slot, coef);
     SDFGB_LAUNCHED("jacobi_strip_kernel");
