@@ -477,9 +477,6 @@ def bench_query(args, dist, P):
     return res
 
 
-GATHER_CEILING_MS = 0.999  # 2^28 random 4 B gathers + streamed int4/float4: profiles/r1r_gather_ceiling.txt
-
-
 def bench_spmv(args, dist, P):
     import torch
     from paper_1902_10345_b200 import device, _lib
@@ -505,6 +502,20 @@ def bench_spmv(args, dist, P):
             device.spmv(rowptr, col, val, x, b)
 
     ms = time_steps(step, args.steps, args.warmup, dist)
+    # the bound that binds: every x[col[j]] is a random 4 B gather costing a
+    # 32 B L2 sector.  Its ceiling is measured live on the same arrays with
+    # the library's gather probe (col/val streamed, x gathered, no rows).
+    L = _lib.load()
+    xg = x if not multi else _dev(xh)
+    sink = torch.zeros(1, device="cuda")
+    nl = (hi - lo) * nz
+
+    def probe(k):
+        _lib.check(L.sdfgb_probe_gather_f32(ctypes.c_void_p(xg.data_ptr()), ctypes.c_void_p(col.data_ptr()),
+                                            ctypes.c_void_p(val.data_ptr()), nl, ctypes.c_void_p(sink.data_ptr()),
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    pms = time_steps(probe, args.steps, args.warmup, dist)
+    del xg
     # check: one clean step, every row, against a float64 gather-sum (1e-5)
     b.zero_()
     step(0)
@@ -521,19 +532,14 @@ def bench_spmv(args, dist, P):
     per = by / (dist.world if args.scaling == "strong" else 1)
     res = {"value": _scale(dist, args) * by / ms / 1e6, "unit": "GB/s", "ms_per_step": ms, "bytes_per_unit": by,
            "launches_per_step": 1, "roofline": roof("hbm", per / ms / 1e6, P, "spmv_hw_vec4_kernel"),
-           # the bound that binds: every x[col[j]] is a random 4 B gather that
-           # costs a 32 B L2 sector; the measured ceiling of exactly that
-           # access pattern (tools/micro/gather_bw.cu) is the second roofline
-           "roofline2": {"bound": "l2_gather", "achieved": nnz / (dist.world if args.scaling == "strong" else 1)
-                         / ms / 1e6, "peak": nnz / GATHER_CEILING_MS / 1e6, "unit": "Ggather/s",
-                         "frac": GATHER_CEILING_MS * nnz / (dist.world if args.scaling == "strong" else 1) / nnz / ms,
-                         "peak_note": "2^28 random fp32 gathers + streamed col/val in 0.999 ms "
-                                      "(profiles/r1r_gather_ceiling.txt)"},
+           "roofline2": {"bound": "l2_gather", "achieved": nl / ms / 1e6, "peak": nl / pms / 1e6,
+                         "unit": "Ggather/s", "frac": pms / ms, "probe_ms": pms,
+                         "peak_note": "gather_probe_kernel on this SpMV's own col/val/x, timed in this run "
+                                      f"({pms:.3f} ms for {nl} gathers; round 1: 0.999 ms, "
+                                      "profiles/r1r_gather_ceiling.txt)"},
            "l2": "matrix 2 GiB > L2 (x, 16 MiB, is L2-resident by design)", "check": check,
            "config": {"workload": "CSR SpMV 2^22 x 2^22, 64 nnz/row fp32/int32", "rows": [lo, hi], "nnz": nnz}}
     if args.e2e:
-        L = _lib.load()
-        nl = (hi - lo) * nz
         hrow = pinned(hi - lo + 1, torch.int64)
         hrow.copy_(rowptr.long().cpu())
         hcol = pinned(nl, torch.int64)

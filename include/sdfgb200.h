@@ -117,6 +117,12 @@ int sdfgb_query_f64(const double* col, int64_t n, int op, double thr,
 /* CSR SpMV: data-dependent inner map over [rowptr[i], rowptr[i+1]) with the
  * indirection x[col[j]] and WCR sum into b[i] (gallery.py:152-213):
  *     b[i] += sum_j val[j] * x[col[j]]               i in [0, H) */
+/* Measurement probe (not a motif): SpMV's memory pattern without its rows --
+ * col/val (nnz % 4 == 0, 16 B aligned) streamed, x[col[j]] gathered, products
+ * summed into *sink.  bench.py times it on the SpMV's own arrays: the live
+ * L2-gather ceiling the SpMV kernel is measured against. */
+int sdfgb_probe_gather_f32(const float* x, const int32_t* col, const float* val, int64_t nnz,
+                           float* sink, void* stream);
 int sdfgb_spmv_csr_f32(const int32_t* rowptr, const int32_t* col, const float* val,
                        const float* x, float* b, int64_t H, void* stream);
 int sdfgb_spmv_csr_f64(const int64_t* rowptr, const int64_t* col, const double* val,

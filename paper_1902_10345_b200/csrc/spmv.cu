@@ -165,8 +165,40 @@ int launch_spmv(const I* rowptr, const I* col, const T* val, const T* x, T* b, i
     return SDFGB_OK;
 }
 
+// Measurement probe (not a motif): the SpMV's memory pattern without its
+// row structure -- col/val streamed as int4/float4 with evict_first, one
+// random x gather per nonzero with evict_last, the products summed into a
+// sink.  bench.py times it on the same arrays as the SpMV to measure the
+// L2-gather ceiling live (the bound the SpMV kernel runs against).
+__global__ void __launch_bounds__(kSpmvBlock)
+gather_probe_kernel(const float* __restrict__ x, const int32_t* __restrict__ col, const float* __restrict__ val,
+                    int64_t n4, float* __restrict__ sink) {
+    const uint64_t first = policy_evict_first(), last = policy_evict_last();
+    float acc = 0.f;
+    for (int64_t i = (int64_t)blockIdx.x * kSpmvBlock + threadIdx.x; i < n4; i += (int64_t)gridDim.x * kSpmvBlock) {
+        const int4 c = ldg_stream_i4(col + 4 * i, first);
+        const float4 v = ldg_stream_f4(val + 4 * i, first);
+        acc += v.x * ldg_keep(x + c.x, last) + v.y * ldg_keep(x + c.y, last) + v.z * ldg_keep(x + c.z, last) +
+               v.w * ldg_keep(x + c.w, last);
+    }
+    if (acc == -1.2345e-30f) sink[0] = acc;  // keeps the loads alive
+}
+
 }  // namespace
 }  // namespace sdfgb
+
+extern "C" int sdfgb_probe_gather_f32(const float* x, const int32_t* col, const float* val, int64_t nnz, float* sink,
+                                      void* stream) {
+    if (nnz < 0 || (nnz % 4) != 0 || (nnz > 0 && (!x || !col || !val || !sink)) ||
+        (reinterpret_cast<uintptr_t>(col) & 15) || (reinterpret_cast<uintptr_t>(val) & 15))
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "probe_gather: nnz % 4 == 0 and 16 B aligned col/val");
+    if (nnz == 0) return SDFGB_OK;
+    const int64_t blocks = (int64_t)sdfgb::num_sms() * 8;  // the SpMV kernel's residency (8 x 256 threads per SM)
+    sdfgb::gather_probe_kernel<<<(unsigned)blocks, sdfgb::kSpmvBlock, 0, sdfgb::as_stream(stream)>>>(
+        x, col, val, nnz / 4, sink);
+    SDFGB_LAUNCHED("gather_probe_kernel");
+    return SDFGB_OK;
+}
 
 extern "C" int sdfgb_spmv_csr_f32(const int32_t* rowptr, const int32_t* col, const float* val,
                                   const float* x, float* b, int64_t H, void* stream) {

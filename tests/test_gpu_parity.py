@@ -591,3 +591,23 @@ def test_host_matmul_pipelined_panels(M, N, K):
     for k in range(K):
         seq = seq + A[:, k:k + 1] * B[k:k + 1, :]
     np.testing.assert_array_equal(C64, seq)
+
+
+def test_gather_probe_runs_and_checks_arguments():
+    """The bench's live L2-gather ceiling (sdfgb_probe_gather_f32): runs on a
+    CSR-shaped stream and rejects unaligned / ragged inputs."""
+    import ctypes
+    from paper_1902_10345_b200 import _lib
+    from paper_1902_10345_b200.errors import CodegenError
+    L = _lib.load()
+    x = torch.rand(1 << 16, device=DEV)
+    col = torch.randint(0, 1 << 16, (1 << 20,), device=DEV, dtype=torch.int32)
+    val = torch.rand(1 << 20, device=DEV)
+    sink = torch.zeros(1, device=DEV)
+    p = lambda t, off=0: ctypes.c_void_p(t.data_ptr() + off)  # noqa: E731
+    _lib.check(L.sdfgb_probe_gather_f32(p(x), p(col), p(val), col.numel(), p(sink), None))
+    torch.cuda.synchronize()
+    with pytest.raises(CodegenError):
+        _lib.check(L.sdfgb_probe_gather_f32(p(x), p(col), p(val), 6, p(sink), None))
+    with pytest.raises(CodegenError):
+        _lib.check(L.sdfgb_probe_gather_f32(p(x), p(col, 4), p(val), 8, p(sink), None))
