@@ -7,8 +7,12 @@ import pytest
 
 import oracle
 
+import os
+
 DEV = "cuda"
 OPS = ["<", "<=", ">", ">=", "==", "!="]
+# SDFGB_FUZZ_SCALE=k runs k times the seeds (long campaigns on the box)
+SCALE = max(1, int(os.environ.get("SDFGB_FUZZ_SCALE", "1")))
 
 
 def t(a):
@@ -17,7 +21,7 @@ def t(a):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(12 * SCALE))
 def test_query_fuzz(seed, cuda_ok):
     import torch
     from paper_1902_10345_b200 import device
@@ -48,7 +52,7 @@ def test_query_fuzz(seed, cuda_ok):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(12 * SCALE))
 def test_histogram_fuzz(seed, cuda_ok):
     import torch
     from paper_1902_10345_b200 import device
@@ -73,7 +77,7 @@ def test_histogram_fuzz(seed, cuda_ok):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(8 * SCALE))
 def test_spmv_fuzz(seed, cuda_ok):
     """ragged rows (empty, short, > 64 nnz), unaligned row starts, duplicate columns"""
     from paper_1902_10345_b200 import device
@@ -100,7 +104,7 @@ def test_spmv_fuzz(seed, cuda_ok):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(6 * SCALE))
 def test_jacobi_fuzz(seed, cuda_ok):
     """square sizes around the tile and vector widths, T around the temporal
     block lengths: bit-exact against the fp32 restatement"""
@@ -117,7 +121,7 @@ def test_jacobi_fuzz(seed, cuda_ok):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(6 * SCALE))
 def test_matmul_host_entry_fuzz(seed, cuda_ok):
     """the reference-facing matmul entries on random shapes (K % 4 != 0 pads,
     one-row / one-column panels): 3xTF32 within 1e-5 of |A||B|, float64
@@ -143,3 +147,40 @@ def test_matmul_host_entry_fuzz(seed, cuda_ok):
             for k in range(K):
                 seq = seq + A[:, k:k + 1] * B[k:k + 1, :]
             np.testing.assert_array_equal(C64, seq)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(8 * SCALE))
+def test_jacobi_strip_fuzz(seed, cuda_ok):
+    """rectangular planes wide enough for the strip kernel (N >= 128), rows
+    around its tile heights (16-row short tiles, 256-row tall tiles, border
+    strips cut twice as fine), T around the 7/5/3 blocks; plus a random
+    edge/interior band split of one launch: bit-exact against the fp32
+    restatement / the whole-plane launch"""
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(9000 + seed)
+    M = int(rng.integers(16, 1200))
+    N = int(rng.integers(32, 420)) * 4
+    T = int(rng.choice([4, 7, 8, 9, 13, 15, 22]))
+    A = rng.random((2, M, N), dtype=np.float32)
+    ref = A.copy()
+    for tt in range(T):
+        src, dst = ref[tt % 2], ref[(tt + 1) % 2]
+        acc = src[1:-1, 1:-1] + src[0:-2, 1:-1]
+        acc = acc + src[2:, 1:-1]
+        acc = acc + src[1:-1, 0:-2]
+        acc = acc + src[1:-1, 2:]
+        dst[1:-1, 1:-1] = np.float32(0.2) * acc
+    At = t(A)
+    device.jacobi2d_rect(At, T)
+    np.testing.assert_array_equal(At.cpu().numpy(), ref, err_msg=f"M={M} N={N} T={T}")
+    if M >= 48:
+        k = int(rng.choice([3, 5, 7]))
+        e0 = int(rng.integers(9, M // 3))
+        e1 = int(rng.integers(2 * M // 3, M - 9))
+        whole, banded = t(A), t(A)
+        device.jacobi2d_block(whole[0], whole[1], k)
+        for r0, r1 in ((0, e0), (e1, M), (e0, e1)):
+            device.jacobi2d_band(banded[0], banded[1], k, r0, r1)
+        np.testing.assert_array_equal(banded.cpu().numpy(), whole.cpu().numpy(),
+                                      err_msg=f"bands M={M} N={N} k={k} cuts={e0},{e1}")
