@@ -334,6 +334,9 @@ __device__ __forceinline__ void st_pred(double* base, uint32_t idx, double v, ui
 #ifndef SDFGB_Q_MINB
 #define SDFGB_Q_MINB 1
 #endif
+#ifndef SDFGB_Q_ROLL
+#define SDFGB_Q_ROLL 1
+#endif
 constexpr int64_t kPieceBytes = (int64_t)SDFGB_Q_PIECE_MB << 20;  // upper bound; pieces are equalised
 
 template <typename T>
@@ -373,6 +376,39 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
         // ---- A: count this warp's chunks [w0, w1)
         uint32_t cnt = 0;
         int64_t q = w0;
+#if SDFGB_Q_ROLL
+        // a rolling ring of 8 chunk loads per lane: each consumed vector is
+        // replaced at once by the load 8 chunks ahead, so 8 stay in flight
+        // (a batch of 8 loaded then counted leaves HBM idle between batches)
+        const int64_t qfull = [&] {
+            int64_t e = w1;
+            while (e > w0 && ps + e * CH > n) --e;  // chunks wholly inside the column
+            return e;
+        }();
+        if (q + 8 <= qfull) {
+            V x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = ldg_hint(col + ps + (q + j) * CH + lane * VN, keep);
+            for (; q + 8 <= qfull; q += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const V v = x[j];
+                    if (q + 8 + j < qfull) x[j] = ldg_hint(col + ps + (q + 8 + j) * CH + lane * VN, keep);
+#pragma unroll
+                    for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(v, cc), thr) ? 1u : 0u;
+                }
+            }
+            // the loads issued past the last full group were exactly the rest
+            // of [q, qfull): count them from the ring
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (q + j < qfull) {
+#pragma unroll
+                    for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x[j], cc), thr) ? 1u : 0u;
+                }
+            q = qfull;
+        }
+#else
         // 8 chunk loads in flight per lane before any is consumed
         for (; q + 8 <= w1 && ps + (q + 8) * CH <= n; q += 8) {
             V x[8];
@@ -383,6 +419,7 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
 #pragma unroll
                 for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x[j], cc), thr) ? 1u : 0u;
         }
+#endif
         for (; q < w1; ++q) {
             const int64_t e0 = ps + q * CH + lane * VN;
             if (e0 + VN <= n) {
