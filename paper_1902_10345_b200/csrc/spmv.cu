@@ -19,6 +19,9 @@ namespace sdfgb {
 namespace {
 
 constexpr int kSpmvBlock = 256;
+#ifndef SDFGB_SPMV_PF
+#define SDFGB_SPMV_PF 1  // next row bounds and this row's b loaded a row ahead (1.094 -> 1.086 ms at S1)
+#endif
 
 template <typename I, typename T>
 __global__ void __launch_bounds__(kSpmvBlock)
@@ -111,9 +114,24 @@ spmv_hw_vec4_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restric
     const int64_t nhw = ((int64_t)gridDim.x * kSpmvBlock) >> 4;
     const uint64_t pstream = policy_evict_first(), pkeep = policy_evict_last();
     auto ldg_na = [&](const float* p) { return ldg_keep(p, pkeep); };
+#if SDFGB_SPMV_PF
+    // the next row's bounds and this row's b are loaded a row ahead, so a
+    // row's chain is col/val -> gathers only (not rowptr -> col/val ->
+    // gathers -> b)
+    int64_t rbn = hw < H ? (int64_t)rowptr[hw] : 0, ren = hw < H ? (int64_t)rowptr[hw + 1] : 0;
+    for (int64_t r = hw; r < H; r += nhw) {
+        const int64_t rb = rbn, re = ren;
+        const float bold = hl == 0 ? b[r] : 0.f;
+        if (r + nhw < H) {
+            rbn = rowptr[r + nhw];
+            ren = rowptr[r + nhw + 1];
+        }
+        float s = 0.f;
+#else
     for (int64_t r = hw; r < H; r += nhw) {
         const int64_t rb = rowptr[r], re = rowptr[r + 1];
         float s = 0.f;
+#endif
         if ((rb & 3) == 0) {
             for (int64_t j = rb + 4 * hl; j < re; j += 64) {
                 if (j + 3 < re) {
@@ -134,7 +152,11 @@ spmv_hw_vec4_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restric
         }
 #pragma unroll
         for (int d = 8; d; d >>= 1) s += __shfl_xor_sync(hmask, s, d, 16);
+#if SDFGB_SPMV_PF
+        if (hl == 0) b[r] = bold + s;
+#else
         if (hl == 0) b[r] += s;
+#endif
     }
 }
 
