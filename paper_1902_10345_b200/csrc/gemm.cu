@@ -52,6 +52,19 @@ __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float(r);
 }
 
+#ifndef SDFGB_GEMM_RAW_AHI
+#define SDFGB_GEMM_RAW_AHI 1  // 4096^3: 0.592 -> 0.584 ms, same error class (profiles/r2_gemm_variants.txt)
+#endif
+// A's hi part read straight from A (the tensor core keeps the top 19 bits of
+// a kind::tf32 operand, i.e. truncates): only lo = a - trunc_tf32(a) is written
+__global__ void split_lo_kernel(const float4* __restrict__ A, float4* __restrict__ lo, int64_t n4) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 a = A[i];
+        auto l = [](float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); };
+        lo[i] = make_float4(l(a.x), l(a.y), l(a.z), l(a.w));
+    }
+}
+
 __global__ void split_rows_kernel(const float* __restrict__ A, float* __restrict__ hi,
                                   float* __restrict__ lo, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -790,10 +803,17 @@ int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, c
 // C = A x B with B already split (gemm_split_b); Ahi / Alo hold M x K each
 int gemm_f32_presplit(const float* A, const float* Bhi, const float* Blo, float* C, int64_t M, int64_t N,
                       int64_t K, float* Ahi, float* Alo, cudaStream_t s) {
-    split_rows_kernel<<<num_sms() * 8, 256, 0, s>>>(A, Ahi, Alo, M * K);
-    SDFGB_LAUNCHED("split_rows_kernel");
     CUtensorMap mAhi, mAlo, mBhi, mBlo;
-    SDFGB_TRY(make_kmajor_map(&mAhi, Ahi, M, K));
+    if (SDFGB_GEMM_RAW_AHI && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Alo)) & 15) == 0) {
+        split_lo_kernel<<<num_sms() * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(A), reinterpret_cast<float4*>(Alo),
+                                                      M * K / 4);
+        SDFGB_LAUNCHED("split_lo_kernel");
+        SDFGB_TRY(make_kmajor_map(&mAhi, A, M, K));
+    } else {
+        split_rows_kernel<<<num_sms() * 8, 256, 0, s>>>(A, Ahi, Alo, M * K);
+        SDFGB_LAUNCHED("split_rows_kernel");
+        SDFGB_TRY(make_kmajor_map(&mAhi, Ahi, M, K));
+    }
     SDFGB_TRY(make_kmajor_map(&mAlo, Alo, M, K));
     if (K <= kFlushK && gemm_use_pair()) {
         SDFGB_TRY(make_kmajor_map(&mBhi, Bhi, N, K, BHALF));
