@@ -729,7 +729,8 @@ int host_matmul(const double* A, const double* B, double* C, int64_t M, int64_t 
         host::narrow_rn(B + off, p, len);
         return SDFGB_OK;
     }, kNoCompute));
-    SDFGB_TRY(gemm_split_b(fB, Bhi, Blo, Kp, N, s));  // once for all panels
+    GemmB bops;
+    SDFGB_TRY(gemm_split_b(fB, Bhi, Blo, Kp, N, s, &bops));  // once for all panels
     DownQueue dq(ss);
     const int64_t rows_per_slot = std::max<int64_t>(1, (int64_t)(slot_bytes() / ((size_t)Kp * 4)));
 
@@ -739,7 +740,7 @@ int host_matmul(const double* A, const double* B, double* C, int64_t M, int64_t 
             host::narrow_rows_rn(A + (r0 + off / Kp) * K, p, len / Kp, K, Kp);
             return SDFGB_OK;
         }, kNoCompute, rows_per_slot * Kp));
-        SDFGB_TRY(gemm_f32_presplit(fA + r0 * Kp, Bhi, Blo, fC + r0 * N, rows, N, Kp, Ahi, Alo, s));
+        SDFGB_TRY(gemm_f32_presplit(fA + r0 * Kp, bops, fC + r0 * N, rows, N, Kp, Ahi, Alo, s));
         SDFGB_TRY(dq.after_compute());
         const int64_t per = (int64_t)(slot_bytes() / 4);
         for (int64_t o = 0; o < rows * N; o += per) {

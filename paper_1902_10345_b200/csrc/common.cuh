@@ -23,9 +23,16 @@ int num_sms();
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // internal building blocks of the host entries (capi.cu), not exported
-int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, cudaStream_t s);
-int gemm_f32_presplit(const float* A, const float* Bhi, const float* Blo, float* C, int64_t M, int64_t N,
-                      int64_t K, float* Ahi, float* Alo, cudaStream_t s);
+// B's operands after the split: hi / lo K-major transposed ([N][K]), or (mn)
+// B itself and its lo part, row-major [K][N], read MN-major by the pair kernel
+struct GemmB {
+    const float* hi;
+    const float* lo;
+    bool mn;
+};
+int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, cudaStream_t s, GemmB* out);
+int gemm_f32_presplit(const float* A, const GemmB& b, float* C, int64_t M, int64_t N, int64_t K, float* Ahi,
+                      float* Alo, cudaStream_t s);
 int spmv_csr_f64_i32(const int32_t* rowptr, const int32_t* col, const double* val, const double* x, double* b,
                      int64_t H, cudaStream_t s);
 

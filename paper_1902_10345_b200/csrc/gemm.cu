@@ -6,9 +6,14 @@
 // Only this motif is a dense contraction, so only it goes to the tensor pipe.
 //
 // fp32 accuracy from TF32 tensor cores via the 3xTF32 split:
-//     A = Ahi + Alo, Ahi = rna_tf32(A), Alo = A - Ahi (exact in fp32)
-//     C ~= Ahi*Bhi + Ahi*Blo + Alo*Bhi        (Alo*Blo ~ 2^-22 dropped)
+//     A = Ahi + Alo, Ahi = tf32(A), Alo = A - Ahi (exact in fp32)
+//     C ~= Ahi*Bhi + Ahi*Blo + Alo*Bhi        (Alo*Blo ~ 2^-20 dropped)
 // 1xTF32 would miss the 1e-4 tolerance (6.8e-4 at K=4096).
+// The tensor core keeps the top 19 bits of a kind::tf32 operand (it
+// truncates), so the pair kernel reads A and B themselves as the hi
+// operands -- A K-major, B MN-major straight from its row-major [K][N]
+// layout -- and the pre-pass writes only Alo and Blo = x - trunc_tf32(x)
+// (round 2; the older kernels below still take rna-split, K-major B^T).
 //
 // v1 structure (one 128x128 C tile per CTA, 256 threads):
 //   * split pre-pass writes Ahi/Alo (M x K) and Bt_hi/Bt_lo (N x K), all
@@ -39,6 +44,16 @@ namespace {
 __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
            (2ull << 61);
+}
+// UMMA shared-memory descriptor, MN-major SWIZZLE_128B: atoms of 32 MN-contiguous
+// fp32 (128 B) x 8 K rows (1 KB); LBO = byte stride between MN atoms, SBO =
+// byte stride between 8-row K groups (cute::UMMA::make_umma_desc<Major::MN>)
+#ifndef SDFGB_BMN_LAYOUT
+#define SDFGB_BMN_LAYOUT 1  // descriptor layout type: 1 = SWIZZLE_128B_BASE32B (MN-major tf32), 2 = SWIZZLE_128B
+#endif
+__device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)SDFGB_BMN_LAYOUT << 61);
 }
 // instruction descriptor kind::tf32, fp32 accumulate, A/B K-major
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
@@ -386,6 +401,18 @@ constexpr int BTILE2 = BHALF * BK * 4;                       // 8 KB
 constexpr int STAGE2_BYTES = 2 * TILE_BYTES + 2 * BTILE2;    // 48 KB: Ahi, Alo, Bhi half, Blo half
 constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256;
 
+#ifndef SDFGB_BMN_LBO
+#define SDFGB_BMN_LBO 4096  // bytes between 32-column MN atoms (one 32 x 32 TMA box)
+#endif
+#ifndef SDFGB_BMN_SBO
+#define SDFGB_BMN_SBO 512  // bytes between 4-row K groups (128 B rows)
+#endif
+#ifndef SDFGB_BMN_KSTEP
+#define SDFGB_BMN_KSTEP 1024  // descriptor start advance per K = 8 MMA
+#endif
+// BMN: B's hi / lo come MN-major straight from row-major [K][N] buffers (B itself
+// and its lo part): TMA boxes of 32 N x 32 K, the MMA's B descriptor MN-major
+template <bool BMN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, SDFGB_GEMM_PAIR_MINB)
 gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                         const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
@@ -450,13 +477,23 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_c
                 const uint32_t lbar = smem_u32(&full[s]) & 0xFEFFFFFFu;
                 tma_load_2d_pair(st + 0 * TILE_BYTES, &mAhi, lbar, kb * BK, m0);
                 tma_load_2d_pair(st + 1 * TILE_BYTES, &mAlo, lbar, kb * BK, m0);
-                tma_load_2d_pair(st + 2 * TILE_BYTES, &mBhi, lbar, kb * BK, n0 + (int)rank * BHALF);
-                tma_load_2d_pair(st + 2 * TILE_BYTES + BTILE2, &mBlo, lbar, kb * BK, n0 + (int)rank * BHALF);
+                if constexpr (BMN) {  // two 32-column MN atoms per half
+#pragma unroll
+                    for (int h = 0; h < BHALF / 32; ++h) {
+                        tma_load_2d_pair(st + 2 * TILE_BYTES + h * 32 * BK * 4, &mBhi, lbar,
+                                         n0 + (int)rank * BHALF + 32 * h, kb * BK);
+                        tma_load_2d_pair(st + 2 * TILE_BYTES + BTILE2 + h * 32 * BK * 4, &mBlo, lbar,
+                                         n0 + (int)rank * BHALF + 32 * h, kb * BK);
+                    }
+                } else {
+                    tma_load_2d_pair(st + 2 * TILE_BYTES, &mBhi, lbar, kb * BK, n0 + (int)rank * BHALF);
+                    tma_load_2d_pair(st + 2 * TILE_BYTES + BTILE2, &mBlo, lbar, kb * BK, n0 + (int)rank * BHALF);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {  // the leader issues the pair's MMAs
-            constexpr uint32_t idesc = idesc_tf32(2 * BM, BN);
+            constexpr uint32_t idesc = idesc_tf32(2 * BM, BN) | (BMN ? (1u << 16) : 0u);  // bit 16: B MN-major
             for (int kb = 0; kb < KB; ++kb) {
                 const int s = kb % STAGES2;
                 const uint32_t ph = (kb / STAGES2) & 1;
@@ -470,8 +507,13 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_c
                     const uint32_t off = k * 32;
                     const uint64_t ahi = sw128_kmajor_desc(base + 0 * TILE_BYTES + off);
                     const uint64_t alo = sw128_kmajor_desc(base + 1 * TILE_BYTES + off);
-                    const uint64_t bhi = sw128_kmajor_desc(base + 2 * TILE_BYTES + off);
-                    const uint64_t blo = sw128_kmajor_desc(base + 2 * TILE_BYTES + BTILE2 + off);
+                    // MN-major B: the k-th K=8 slice is the k-th 1 KB row group of every atom
+                    const uint64_t bhi = BMN ? sw128_mnmajor_desc(base + 2 * TILE_BYTES + k * SDFGB_BMN_KSTEP,
+                                                                  SDFGB_BMN_LBO, SDFGB_BMN_SBO)
+                                             : sw128_kmajor_desc(base + 2 * TILE_BYTES + off);
+                    const uint64_t blo = BMN ? sw128_mnmajor_desc(base + 2 * TILE_BYTES + BTILE2 + k * SDFGB_BMN_KSTEP,
+                                                                  SDFGB_BMN_LBO, SDFGB_BMN_SBO)
+                                             : sw128_kmajor_desc(base + 2 * TILE_BYTES + BTILE2 + off);
                     tc_mma_tf32_pair(dacc, alo, bhi, idesc, !(first && k == 0));
                     tc_mma_tf32_pair(dacc, ahi, blo, idesc, 1u);
                     tc_mma_tf32_pair(dacc, ahi, bhi, idesc, 1u);
@@ -787,7 +829,19 @@ namespace sdfgb {
 
 // B (K x N, row-major) -> Bt_hi / Bt_lo (N x K, K-major): the 3xTF32 split of
 // the right operand, done once per B (the host entry's row panels share it)
-int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, cudaStream_t s) {
+#ifndef SDFGB_GEMM_BMN
+#define SDFGB_GEMM_BMN 1  // the pair kernel reads B's hi / lo MN-major (no transpose in the pre-pass)
+#endif
+int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, cudaStream_t s, GemmB* out) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(Blo)) & 15) == 0;
+    if (SDFGB_GEMM_BMN && K <= kFlushK && gemm_use_pair() && N % 4 == 0 && aligned) {
+        // MN-major: B's hi is B itself (tensor-core truncation), only lo is written, untransposed
+        split_lo_kernel<<<num_sms() * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(B), reinterpret_cast<float4*>(Blo),
+                                                      K * N / 4);
+        SDFGB_LAUNCHED("split_lo_kernel");
+        *out = {B, Blo, true};
+        return SDFGB_OK;
+    }
     if (N % 4 == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0) {  // K % 4 == 0 already
         dim3 tg((unsigned)((N + 63) / 64), (unsigned)((K + 63) / 64));
         split_transpose64_kernel<<<tg, 256, 0, s>>>(B, Bhi, Blo, K, N);
@@ -797,12 +851,15 @@ int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, c
         split_transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(B, Bhi, Blo, K, N);
         SDFGB_LAUNCHED("split_transpose_kernel");
     }
+    *out = {Bhi, Blo, false};
     return SDFGB_OK;
 }
 
 // C = A x B with B already split (gemm_split_b); Ahi / Alo hold M x K each
-int gemm_f32_presplit(const float* A, const float* Bhi, const float* Blo, float* C, int64_t M, int64_t N,
-                      int64_t K, float* Ahi, float* Alo, cudaStream_t s) {
+int gemm_f32_presplit(const float* A, const GemmB& b, float* C, int64_t M, int64_t N, int64_t K, float* Ahi,
+                      float* Alo, cudaStream_t s) {
+    const float* Bhi = b.hi;
+    const float* Blo = b.lo;
     CUtensorMap mAhi, mAlo, mBhi, mBlo;
     if (SDFGB_GEMM_RAW_AHI && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Alo)) & 15) == 0) {
         split_lo_kernel<<<num_sms() * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(A), reinterpret_cast<float4*>(Alo),
@@ -816,21 +873,36 @@ int gemm_f32_presplit(const float* A, const float* Bhi, const float* Blo, float*
     }
     SDFGB_TRY(make_kmajor_map(&mAlo, Alo, M, K));
     if (K <= kFlushK && gemm_use_pair()) {
-        SDFGB_TRY(make_kmajor_map(&mBhi, Bhi, N, K, BHALF));
-        SDFGB_TRY(make_kmajor_map(&mBlo, Blo, N, K, BHALF));
         static std::once_flag attr2;
         static cudaError_t attr2_err = cudaSuccess;
         std::call_once(attr2, [] {
-            attr2_err = cudaFuncSetAttribute(gemm_3xtf32_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             GEMM2_SMEM);
+            attr2_err = cudaFuncSetAttribute(gemm_3xtf32_pair_kernel<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM2_SMEM);
+            if (attr2_err == cudaSuccess)
+                attr2_err = cudaFuncSetAttribute(gemm_3xtf32_pair_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM2_SMEM);
         });
         SDFGB_CUDA(attr2_err);
         const int64_t pairs = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
-        gemm_3xtf32_pair_kernel<<<(unsigned)(2 * pairs), GEMM_THREADS, GEMM2_SMEM, s>>>(mAhi, mAlo, mBhi, mBlo, C,
-                                                                                     (int)M, (int)N, (int)K);
+        if (b.mn) {  // row-major [K][N] B operands, 32 x 32 boxes (one 128 B swizzle span of N)
+            // MN-major tf32 operands take the "128 B swizzle, 32 B atomicity" smem layout
+            // (CUTLASS: Layout_MN_SW128_32B_Atom, the only one it allows for them)
+            constexpr CUtensorMapSwizzle sw = SDFGB_BMN_LAYOUT == 1 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                                                     : CU_TENSOR_MAP_SWIZZLE_128B;
+            SDFGB_TRY(encode_tiled_2d(&mBhi, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Bhi, K, N, 32, BK, sw));
+            SDFGB_TRY(encode_tiled_2d(&mBlo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Blo, K, N, 32, BK, sw));
+            gemm_3xtf32_pair_kernel<true><<<(unsigned)(2 * pairs), GEMM_THREADS, GEMM2_SMEM, s>>>(
+                mAhi, mAlo, mBhi, mBlo, C, (int)M, (int)N, (int)K);
+        } else {
+            SDFGB_TRY(make_kmajor_map(&mBhi, Bhi, N, K, BHALF));
+            SDFGB_TRY(make_kmajor_map(&mBlo, Blo, N, K, BHALF));
+            gemm_3xtf32_pair_kernel<false><<<(unsigned)(2 * pairs), GEMM_THREADS, GEMM2_SMEM, s>>>(
+                mAhi, mAlo, mBhi, mBlo, C, (int)M, (int)N, (int)K);
+        }
         SDFGB_LAUNCHED("gemm_3xtf32_pair_kernel");
         return SDFGB_OK;
     }
+    if (b.mn) return set_error(SDFGB_ERR_INVALID, "gemm: MN-major B needs the pair kernel");
     SDFGB_TRY(make_kmajor_map(&mBhi, Bhi, N, K));
     SDFGB_TRY(make_kmajor_map(&mBlo, Blo, N, K));
     static std::once_flag attr;
@@ -877,8 +949,9 @@ extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t 
     float* Alo = reinterpret_cast<float*>(w + r((size_t)M * K * 4));
     float* Bhi = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4));
     float* Blo = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4) + r((size_t)N * K * 4));
-    SDFGB_TRY(gemm_split_b(B, Bhi, Blo, K, N, s));
-    return gemm_f32_presplit(A, Bhi, Blo, C, M, N, K, Ahi, Alo, s);
+    GemmB bops;
+    SDFGB_TRY(gemm_split_b(B, Bhi, Blo, K, N, s, &bops));
+    return gemm_f32_presplit(A, bops, C, M, N, K, Ahi, Alo, s);
 }
 
 extern "C" int sdfgb_gemm_f32_simt(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
