@@ -175,6 +175,14 @@ size_t sdfgb_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int sdfgb_gemm_f32(const float* A, const float* B, float* C,
                    int64_t M, int64_t N, int64_t K,
                    void* ws, size_t ws_bytes, void* stream);
+/* The same with flags.  SDFGB_GEMM_B_SPLIT: B's split operands are already in
+ * ws from an earlier call with the same B (same K, N) -- row pieces of one
+ * product (the multi-GPU A-piece pipeline) split B once.  B's part of the
+ * workspace does not depend on M. */
+#define SDFGB_GEMM_B_SPLIT 1
+int sdfgb_gemm_f32_ex(const float* A, const float* B, float* C,
+                      int64_t M, int64_t N, int64_t K,
+                      void* ws, size_t ws_bytes, int flags, void* stream);
 /* SIMT fp32 FFMA GEMM (k-sequential per element) used as the on-device
  * cross-check of the tensor-core path in tests. */
 int sdfgb_gemm_f32_simt(const float* A, const float* B, float* C,

@@ -20,6 +20,7 @@ OK, ERR_INVALID, ERR_CUDA, ERR_OOB, ERR_WORKSPACE = 0, 1, 2, 3, 4
 PREC_FP32, PREC_NATIVE = 0, 1
 CMP = {"<": 0, "<=": 1, ">": 2, ">=": 3, "==": 4, "!=": 5}
 QUERY_ORDERED = 0x100  # include/sdfgb200.h: OR into op for input-order survivors
+GEMM_B_SPLIT = 1  # include/sdfgb200.h: sdfgb_gemm_f32_ex flag, B already split in the workspace
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -68,6 +69,7 @@ SIGNATURES = {
     "sdfgb_probe_gather_f32": (_INT, [_P, _P, _P, _I64, _P, _P]),
     "sdfgb_gemm_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
     "sdfgb_gemm_f32": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _SZ, _P]),
+    "sdfgb_gemm_f32_ex": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P, _SZ, _INT, _P]),
     "sdfgb_gemm_f32_simt": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "sdfgb_gemm_f64": (_INT, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "sdfgb_host_histogram": (_INT, [_P, _P, _I64, _I64, _I64, _F64, _F64, _INT]),

@@ -31,6 +31,7 @@ struct GemmB {
     bool mn;
 };
 int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, cudaStream_t s, GemmB* out);
+GemmB gemm_b_operands(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N);  // after gemm_split_b
 int gemm_f32_presplit(const float* A, const GemmB& b, float* C, int64_t M, int64_t N, int64_t K, float* Ahi,
                       float* Alo, cudaStream_t s);
 int spmv_csr_f64_i32(const int32_t* rowptr, const int32_t* col, const double* val, const double* x, double* b,

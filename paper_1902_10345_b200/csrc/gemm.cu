@@ -832,9 +832,18 @@ namespace sdfgb {
 #ifndef SDFGB_GEMM_BMN
 #define SDFGB_GEMM_BMN 1  // the pair kernel reads B's hi / lo MN-major (no transpose in the pre-pass)
 #endif
-int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, cudaStream_t s, GemmB* out) {
+// the pair kernel reads B MN-major (no transpose) when it runs and B / Blo are aligned
+static bool gemm_b_mn(const float* B, const float* Blo, int64_t K, int64_t N) {
     const bool aligned = ((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(Blo)) & 15) == 0;
-    if (SDFGB_GEMM_BMN && K <= kFlushK && gemm_use_pair() && N % 4 == 0 && aligned) {
+    return SDFGB_GEMM_BMN && K <= kFlushK && gemm_use_pair() && N % 4 == 0 && aligned;
+}
+
+GemmB gemm_b_operands(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N) {
+    return gemm_b_mn(B, Blo, K, N) ? GemmB{B, Blo, true} : GemmB{Bhi, Blo, false};
+}
+
+int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, cudaStream_t s, GemmB* out) {
+    if (gemm_b_mn(B, Blo, K, N)) {
         // MN-major: B's hi is B itself (tensor-core truncation), only lo is written, untransposed
         split_lo_kernel<<<num_sms() * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(B), reinterpret_cast<float4*>(Blo),
                                                       K * N / 4);
@@ -928,8 +937,8 @@ int gemm_f32_presplit(const float* A, const GemmB& b, float* C, int64_t M, int64
 
 }  // namespace sdfgb
 
-extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
-                              void* ws, size_t ws_bytes, void* stream) {
+extern "C" int sdfgb_gemm_f32_ex(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
+                                 void* ws, size_t ws_bytes, int flags, void* stream) {
     using namespace sdfgb;
     if (M < 0 || N < 0 || K < 0 || (M * N > 0 && !C))
         return set_error(SDFGB_ERR_INVALID, "gemm: bad arguments");
@@ -943,15 +952,25 @@ extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t 
         return set_error(SDFGB_ERR_INVALID, "gemm: K must be a multiple of 4 (TMA row stride)");
     if (!A || !B || !ws || ws_bytes < sdfgb_gemm_workspace_bytes(M, N, K))
         return set_error(SDFGB_ERR_WORKSPACE, "gemm: workspace too small");
+    // workspace: B's split first (its place does not depend on M, so row
+    // pieces of one product can share it), then A's
     auto r = [](size_t b) { return (b + 255) / 256 * 256; };
     uint8_t* w = static_cast<uint8_t*>(ws);
-    float* Ahi = reinterpret_cast<float*>(w);
-    float* Alo = reinterpret_cast<float*>(w + r((size_t)M * K * 4));
-    float* Bhi = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4));
-    float* Blo = reinterpret_cast<float*>(w + 2 * r((size_t)M * K * 4) + r((size_t)N * K * 4));
+    float* Bhi = reinterpret_cast<float*>(w);
+    float* Blo = reinterpret_cast<float*>(w + r((size_t)N * K * 4));
+    float* Ahi = reinterpret_cast<float*>(w + 2 * r((size_t)N * K * 4));
+    float* Alo = reinterpret_cast<float*>(w + 2 * r((size_t)N * K * 4) + r((size_t)M * K * 4));
     GemmB bops;
-    SDFGB_TRY(gemm_split_b(B, Bhi, Blo, K, N, s, &bops));
+    if (flags & SDFGB_GEMM_B_SPLIT)
+        bops = gemm_b_operands(B, Bhi, Blo, K, N);  // split by an earlier call with this B and workspace
+    else
+        SDFGB_TRY(gemm_split_b(B, Bhi, Blo, K, N, s, &bops));
     return gemm_f32_presplit(A, bops, C, M, N, K, Ahi, Alo, s);
+}
+
+extern "C" int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
+                              void* ws, size_t ws_bytes, void* stream) {
+    return sdfgb_gemm_f32_ex(A, B, C, M, N, K, ws, ws_bytes, 0, stream);
 }
 
 extern "C" int sdfgb_gemm_f32_simt(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,

@@ -44,6 +44,8 @@ int sdfgb_jacobi2d_block_f32(const float* src, float* dst, int64_t M, int64_t N,
                              void* stream);
 int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k, int64_t r0, int64_t r1,
                             double coef, void* stream);
+int sdfgb_gemm_f32_ex(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, void* ws,
+                      size_t ws_bytes, int flags, void* stream);
 int sdfgb_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K, void* ws,
                    size_t ws_bytes, void* stream);
 }
@@ -381,8 +383,9 @@ extern "C" int sdfgb_gemm_f32_mgpu(const float* A_piece, int64_t a_rows, const f
     for (int i = 0; i < Q; ++i) {
         const int q = (qi + i) % Q;
         if (q != qi) SDFGB_CUDA(cudaStreamWaitEvent(s, landed[q], 0));
-        SDFGB_TRY(sdfgb_gemm_f32(A_panel + q * a_rows * K, B_panel, C_block + q * a_rows * nq, a_rows, nq, K, ws,
-                                 ws_bytes, stream));
+        // B is split once (first piece); the later pieces reuse it from ws
+        SDFGB_TRY(sdfgb_gemm_f32_ex(A_panel + q * a_rows * K, B_panel, C_block + q * a_rows * nq, a_rows, nq, K, ws,
+                                    ws_bytes, i ? SDFGB_GEMM_B_SPLIT : 0, stream));
     }
     return ss.join();
 }

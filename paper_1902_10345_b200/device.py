@@ -142,15 +142,18 @@ def gemm_workspace(M, N, K, device=None):
     return torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
 
 
-def gemm(A, B, C, ws, stream=None):
-    """C = A @ B (fp32, 3xTF32 tcgen05)."""
+def gemm(A, B, C, ws, stream=None, b_split=False):
+    """C = A @ B (fp32, 3xTF32 tcgen05).  ``b_split``: B's split operands
+    are already in ``ws`` from an earlier call with this B (row pieces of
+    one product split B once)."""
     import torch
     L = _lib.load()
     for t, n in ((A, "A"), (B, "B"), (C, "C")):
         _require(t, torch.float32, n)
     M, K = A.shape
     N = B.shape[1]
-    _lib.check(L.sdfgb_gemm_f32(_p(A), _p(B), _p(C), M, N, K, _p(ws), ws.numel(), _stream(stream)))
+    _lib.check(L.sdfgb_gemm_f32_ex(_p(A), _p(B), _p(C), M, N, K, _p(ws), ws.numel(),
+                                   _lib.GEMM_B_SPLIT if b_split else 0, _stream(stream)))
 
 
 def gemm_f64(A, B, C, stream=None):

@@ -68,13 +68,17 @@ class DeviceBackend:
     def jacobi_band(self, src, dst, k, r0, r1, coef):
         self.d.jacobi2d_band(src, dst, k, r0, r1, coef)
 
-    def gemm(self, A, B, C):
+    def gemm(self, A, B, C, reuse_b=False, ws_rows=None):
+        """C = A @ B.  Row pieces of one product pass ws_rows (the tallest
+        piece, so they share one workspace) and reuse_b after the first, so
+        B is split once."""
         M, K = A.shape
         N = B.shape[1]
-        key = ("g", M, N, K, A.device)
+        rows = max(M, ws_rows or 0)
+        key = ("g", rows, N, K, A.device)
         if key not in self._ws:
-            self._ws[key] = self.d.gemm_workspace(M, N, K, A.device)
-        self.d.gemm(A, B, C, self._ws[key])
+            self._ws[key] = self.d.gemm_workspace(rows, N, K, A.device)
+        self.d.gemm(A, B, C, self._ws[key], b_split=reuse_b)
 
 
 def _rank_world(pg):
@@ -499,11 +503,14 @@ def gemm(pg, grid: GemmGrid, A_piece, B_piece, C_block, backend, pipeline=True):
             torch.empty((b - a, K), dtype=A_piece.dtype, device=A_piece.device) for q, (a, b) in enumerate(rows)]
     works = [pg.broadcast(bufs[q], src=grid.i * grid.Q + q, group=grid.row_group, async_op=True)
              for q in range(grid.Q)]
+    tallest = max(b - a for a, b in rows)
+    first = True
     for q in [grid.j] + [q for q in range(grid.Q) if q != grid.j]:
         works[q].wait()
         a, b = rows[q]
-        if b > a:
-            backend.gemm(bufs[q], Bp, C_block[a:b])
+        if b > a:  # B is split by the first piece's call, reused by the others
+            backend.gemm(bufs[q], Bp, C_block[a:b], reuse_b=not first, ws_rows=tallest)
+            first = False
 
 
 def _gather_rows(pg, outs, mine, me, ranks, group):

@@ -611,3 +611,22 @@ def test_gather_probe_runs_and_checks_arguments():
         _lib.check(L.sdfgb_probe_gather_f32(p(x), p(col), p(val), 6, p(sink), None))
     with pytest.raises(CodegenError):
         _lib.check(L.sdfgb_probe_gather_f32(p(x), p(col, 4), p(val), 8, p(sink), None))
+
+
+@pytest.mark.parametrize("M,N,K", [(384, 256, 512), (300, 130, 96)])
+def test_gemm_row_pieces_split_b_once(M, N, K):
+    """sdfgb_gemm_f32_ex with SDFGB_GEMM_B_SPLIT: row pieces of one product
+    (the multi-GPU A-piece pipeline) sharing one workspace split B once and
+    give the whole product bit for bit (MN-major and transposed B paths)."""
+    from paper_1902_10345_b200 import device
+    g = torch.Generator(device=DEV).manual_seed(M + N)
+    A = torch.rand(M, K, device=DEV, generator=g)
+    B = torch.rand(K, N, device=DEV, generator=g)
+    whole = torch.empty(M, N, device=DEV)
+    device.gemm(A, B, whole, device.gemm_workspace(M, N, K, DEV))
+    ws = device.gemm_workspace(M - 100, N, K, DEV)  # sized for the tallest piece
+    pieces = torch.empty(M, N, device=DEV)
+    device.gemm(A[:100].contiguous(), B, pieces[:100], ws)
+    device.gemm(A[100:].contiguous(), B, pieces[100:], ws, b_split=True)
+    torch.cuda.synchronize()
+    assert torch.equal(pieces, whole)

@@ -70,7 +70,7 @@ class OracleBackend:
         r0, r1 = max(r0, 1), min(r1, dst.shape[0] - 1)
         dst[r0:r1] = tmp[r0:r1]
 
-    def gemm(self, A, B, C):
+    def gemm(self, A, B, C, reuse_b=False, ws_rows=None):
         C.copy_(torch.from_numpy(oracle.matmul(A.numpy(), B.numpy()).astype(np.float32)))
 
 
