@@ -318,82 +318,113 @@ __device__ __forceinline__ void st_pred(double* base, uint32_t idx, double v, ui
 
 // ---------------------------------------------------------------------------
 // Piece kernel (the default for 16 B-aligned columns).  The column is cut
-// into L2-sized pieces (64 MB); for each piece every co-resident CTA
-//   A  counts its contiguous chunk range warp by warp (HBM read, L2
-//      evict_last), keeping the per-warp counts in smem;
-//   -- one grid-wide barrier (cooperative groups) per piece --
-//   B  reads the G CTA counts (one block-wide load) for its offset, then
-//      every warp re-reads its slice from L2 (evict_first) and compacts it in
-//      order: per lane one 16 B vector per 32*VN-element chunk, byte-packed
-//      chunk counts, one 32-bit shuffle scan per 4 chunks, predicated stores.
-// No CTA ever polls another: the only cross-CTA synchronisation is one grid
-// barrier per 64 MB, and HBM sees each input byte once.
+// into equal pieces of at most 32 MB, and each co-resident CTA owns the same
+// contiguous chunk range of every piece, cut into NW warp ranges.  Two warp
+// roles run as a pipeline, one piece apart:
+//   A  (counter warps)    count piece i's warp ranges from HBM (L2
+//      evict_last, a rolling ring of 8 vector loads per lane), then publish
+//      the CTA's total as an epoch-tagged word cnts[i*G + c];
+//   B  (compactor warps)  read piece i-1's G CTA totals (spinning only on
+//      words not yet published) for the CTA's offset, then re-read each warp
+//      range from L2 (evict_first, two 4-chunk register sets so the next
+//      loads are in flight) and compact it in order: byte-packed chunk
+//      counts, one 32-bit shuffle scan per 4 chunks, predicated stores.
+// So HBM reads of piece i overlap the survivor writes of piece i-1, two
+// pieces (64 MB) are L2-resident at a time, HBM sees each input byte once,
+// and no grid-wide barrier is needed (the cooperative launch only guarantees
+// that every CTA is resident).  One CTA barrier per step hands the per-warp
+// counts from the counters to the compactors.
 #ifndef SDFGB_Q_PIECE_MB
-#define SDFGB_Q_PIECE_MB 64
+#define SDFGB_Q_PIECE_MB 32
 #endif
 #ifndef SDFGB_Q_MINB
 #define SDFGB_Q_MINB 1
 #endif
-#ifndef SDFGB_Q_ROLL
-#define SDFGB_Q_ROLL 1
+#ifndef SDFGB_Q_RING
+#define SDFGB_Q_RING 8  // chunk loads in flight per counter lane
 #endif
 constexpr int64_t kPieceBytes = (int64_t)SDFGB_Q_PIECE_MB << 20;  // upper bound; pieces are equalised
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 template <typename T>
 __device__ __forceinline__ typename Vec16<T>::type ldg_hint(const T* p, uint64_t pol) {
     return ldg_pol(reinterpret_cast<const typename Vec16<T>::type*>(p), pol);
 }
 
+#ifndef SDFGB_Q_PBLOCK
+#define SDFGB_Q_PBLOCK 512
+#endif
+constexpr int kQPBlock = SDFGB_Q_PBLOCK;
+
+#ifndef SDFGB_Q_TIMING
+#define SDFGB_Q_TIMING 0  // debug: per-CTA role timestamps (sdfgb_debug_query_timing)
+#endif
+#if SDFGB_Q_TIMING
+__device__ unsigned long long g_qtime[64][4][1024];  // [iteration][A0,A1,B0,B1][CTA]
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 template <typename T, int OP>
-__global__ void __launch_bounds__(kQBlock, SDFGB_Q_MINB)
+__global__ void __launch_bounds__(kQPBlock, SDFGB_Q_MINB)
 query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ out,
-                   unsigned long long* __restrict__ count, unsigned long long* __restrict__ cnts) {
+                   unsigned long long* __restrict__ count, unsigned long long* __restrict__ cnts, uint32_t epoch) {
     using V = typename Vec16<T>::type;
     constexpr int VN = Vec16<T>::n;
-    constexpr int NW = kQBlock / 32;
+    // two roles of NW warps each, counters (A) and compactors (B), over the
+    // same NW warp ranges of the CTA's chunks
+    constexpr int NW = kQPBlock / 64;
     constexpr int CH = 32 * VN;  // elements per warp chunk
     // equal pieces of at most kPieceBytes, multiples of a chunk
     const int64_t npieces = (n * (int64_t)sizeof(T) + kPieceBytes - 1) / kPieceBytes;
     const int64_t PIECE = ((n + npieces - 1) / npieces + CH - 1) / CH * CH;
-    __shared__ uint32_t s_wcnt[NW];
+    __shared__ uint32_t s_wcnt[2][NW];  // per-warp counts of the two pieces in flight
     __shared__ int64_t s_lo[NW], s_to[NW];
 
-    cg::grid_group grid = cg::this_grid();
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const bool counter = tid < NW * 32;
+    const int warp = (tid >> 5) - (counter ? 0 : NW);  // index within the role
+    const int rtid = tid - (counter ? 0 : NW * 32);
     const int64_t G = gridDim.x, c = blockIdx.x;
     const uint64_t keep = make_policy(true), drop = make_policy(false);
-    int64_t base = 0;
-    int64_t p = 0;
-    for (int64_t ps = 0; ps < n; ps += PIECE, ++p) {
+    // warp range r's chunks [w0, w1) of piece p (starting at element ps)
+    auto geom = [&](int64_t p, int r, int64_t& ps, int64_t& w0, int64_t& w1) {
+        ps = p * PIECE;
         const int64_t pl = n - ps < PIECE ? n - ps : PIECE;
         const int64_t nch = (pl + CH - 1) / CH;
         const int64_t per_cta = (nch + G - 1) / G;
         const int64_t cs = c * per_cta < nch ? c * per_cta : nch;
         const int64_t ce = cs + per_cta < nch ? cs + per_cta : nch;
         const int64_t per_w = (ce - cs + NW - 1) / NW;
-        const int64_t w0 = cs + warp * per_w < ce ? cs + warp * per_w : ce;
-        const int64_t w1 = w0 + per_w < ce ? w0 + per_w : ce;
-        // ---- A: count this warp's chunks [w0, w1)
+        w0 = cs + r * per_w < ce ? cs + r * per_w : ce;
+        w1 = w0 + per_w < ce ? w0 + per_w : ce;
+    };
+    // ---- A(p): count, publish this CTA's count of piece p (epoch-tagged)
+    auto phaseA = [&](int64_t p) {
+        int64_t ps, w0, w1;
+        geom(p, warp, ps, w0, w1);
+        // a rolling ring of R chunk loads per lane: each consumed vector is
+        // replaced at once by the load R chunks ahead, so R stay in flight
+        // (a batch loaded then counted leaves HBM idle between batches)
+        constexpr int R = SDFGB_Q_RING;
         uint32_t cnt = 0;
         int64_t q = w0;
-#if SDFGB_Q_ROLL
-        // a rolling ring of 8 chunk loads per lane: each consumed vector is
-        // replaced at once by the load 8 chunks ahead, so 8 stay in flight
-        // (a batch of 8 loaded then counted leaves HBM idle between batches)
-        const int64_t qfull = [&] {
-            int64_t e = w1;
-            while (e > w0 && ps + e * CH > n) --e;  // chunks wholly inside the column
-            return e;
-        }();
-        if (q + 8 <= qfull) {
-            V x[8];
+        int64_t qfull = w1;
+        while (qfull > w0 && ps + qfull * CH > n) --qfull;  // chunks wholly inside the column
+        if (q + R <= qfull) {
+            V x[R];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = ldg_hint(col + ps + (q + j) * CH + lane * VN, keep);
-            for (; q + 8 <= qfull; q += 8) {
+            for (int j = 0; j < R; ++j) x[j] = ldg_hint(col + ps + (q + j) * CH + lane * VN, keep);
+            for (; q + R <= qfull; q += R) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < R; ++j) {
                     const V v = x[j];
-                    if (q + 8 + j < qfull) x[j] = ldg_hint(col + ps + (q + 8 + j) * CH + lane * VN, keep);
+                    if (q + R + j < qfull) x[j] = ldg_hint(col + ps + (q + R + j) * CH + lane * VN, keep);
 #pragma unroll
                     for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(v, cc), thr) ? 1u : 0u;
                 }
@@ -401,25 +432,13 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
             // the loads issued past the last full group were exactly the rest
             // of [q, qfull): count them from the ring
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < R; ++j)
                 if (q + j < qfull) {
 #pragma unroll
                     for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x[j], cc), thr) ? 1u : 0u;
                 }
             q = qfull;
         }
-#else
-        // 8 chunk loads in flight per lane before any is consumed
-        for (; q + 8 <= w1 && ps + (q + 8) * CH <= n; q += 8) {
-            V x[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = ldg_hint(col + ps + (q + j) * CH + lane * VN, keep);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-#pragma unroll
-                for (int cc = 0; cc < VN; ++cc) cnt += pred<OP>(vget<V, T>(x[j], cc), thr) ? 1u : 0u;
-        }
-#endif
         for (; q < w1; ++q) {
             const int64_t e0 = ps + q * CH + lane * VN;
             if (e0 + VN <= n) {
@@ -431,21 +450,30 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
                 for (int cc = 0; cc < VN; ++cc) cnt += (e0 + cc < n && pred<OP>(col[e0 + cc], thr)) ? 1u : 0u;
             }
         }
-#pragma unroll
-        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-        if (lane == 0) s_wcnt[warp] = cnt;
-        __syncthreads();
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) s_wcnt[p & 1][warp] = cnt;
+        named_bar(1, NW * 32);  // the counters only
         if (tid == 0) {
             uint32_t t = 0;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) t += s_wcnt[w];
-            cnts[p * G + c] = t;
+            for (int w = 0; w < NW; ++w) t += s_wcnt[p & 1][w];
+            st_relaxed(cnts + p * G + c, pack_status(epoch, kFlagAgg, t));
         }
-        grid.sync();
-        // ---- B: this CTA's offset inside the piece, then per-warp compaction
+    };
+    int64_t base = 0;
+    // ---- B(p): this CTA's offset inside piece p (waits only for counts not
+    // yet published -- by now every CTA has moved on to piece p+1), then
+    // per-warp compaction from L2
+    auto phaseB = [&](int64_t p) {
+        int64_t ps, w0, w1;
+        geom(p, warp, ps, w0, w1);
         int64_t lo = 0, to = 0;
-        for (int64_t q = tid; q < G; q += kQBlock) {
-            const int64_t v = (int64_t)__ldcg(cnts + p * G + q);
+        for (int64_t q = rtid; q < G; q += NW * 32) {
+            uint64_t w;
+            do {
+                w = ld_relaxed(cnts + p * G + q);
+            } while ((uint32_t)(w >> 44) != epoch);
+            const int64_t v = (int64_t)(w & kValueMask);
             to += v;
             lo += q < c ? v : 0;
         }
@@ -458,28 +486,23 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
             s_lo[warp] = lo;
             s_to[warp] = to;
         }
-        __syncthreads();
+        named_bar(2, NW * 32);  // the compactors only
         int64_t cta_off = 0, piece_total = 0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
             cta_off += s_lo[w];
             piece_total += s_to[w];
         }
-        uint32_t wc = lane < warp ? s_wcnt[lane] : 0u;
+        uint32_t wc = lane < warp ? s_wcnt[p & 1][lane] : 0u;
 #pragma unroll
         for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
         T* wout = out + (base + cta_off + wc);
         uint32_t run = 0;
-        for (int64_t q0 = w0; q0 < w1; q0 += 8) {
-            V x[8];
-            uint32_t bits = 0, pk[2] = {0u, 0u};
-            const bool full = q0 + 8 <= w1 && ps + (q0 + 8) * CH <= n;
-            if (full) {  // 8 loads in flight per lane
+        // compact 4 chunks from x (loaded, or loaded here when !full)
+        auto emit4 = [&](V (&x)[4], bool full, int64_t q0) {
+            uint32_t bits = 0, pk = 0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) x[j] = ldg_hint(col + ps + (q0 + j) * CH + lane * VN, drop);
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 4; ++j) {
                 const int64_t e0 = ps + (q0 + j) * CH + lane * VN;
                 uint32_t m = 0;
                 if (full) {
@@ -499,36 +522,72 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
                     }
                 }
                 bits |= m << (j * VN);
-                pk[j >> 2] |= (uint32_t)__popc(m) << (8 * (j & 3));
+                pk |= (uint32_t)__popc(m) << (8 * j);
             }
+            uint32_t incl = pk;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t incl = pk[h];
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (lane >= d) incl += o;
-                }
-                const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-                const uint32_t excl = incl - pk[h];
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    const int j = 4 * h + jj;
-                    uint32_t at = run + ((excl >> (8 * jj)) & 0xffu);
-#pragma unroll
-                    for (int cc = 0; cc < VN; ++cc) {
-                        const uint32_t pp = (bits >> (j * VN + cc)) & 1u;
-                        st_pred(wout, at, vget<V, T>(x[j], cc), pp);
-                        at += pp;
-                    }
-                    run += (tot >> (8 * jj)) & 0xffu;
-                }
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += o;
             }
+            const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+            const uint32_t excl = incl - pk;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t at = run + ((excl >> (8 * j)) & 0xffu);
+#pragma unroll
+                for (int cc = 0; cc < VN; ++cc) {
+                    const uint32_t pp = (bits >> (j * VN + cc)) & 1u;
+                    st_pred(wout, at, vget<V, T>(x[j], cc), pp);
+                    at += pp;
+                }
+                run += (tot >> (8 * j)) & 0xffu;
+            }
+        };
+        auto load4 = [&](V (&x)[4], int64_t q0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = ldg_hint(col + ps + (q0 + j) * CH + lane * VN, drop);
+        };
+        // whole chunks inside the column: two 4-chunk register sets, the
+        // next one's L2 loads in flight while the current one is compacted
+        int64_t qf = w1;
+        while (qf > w0 && ps + qf * CH > n) --qf;
+        int64_t q0 = w0;
+        V xa[4], xb[4];
+        if (q0 + 4 <= qf) load4(xa, q0);
+        for (;;) {
+            if (q0 + 4 > qf) break;
+            if (q0 + 8 <= qf) load4(xb, q0 + 4);
+            emit4(xa, true, q0);
+            q0 += 4;
+            if (q0 + 4 > qf) break;
+            if (q0 + 8 <= qf) load4(xa, q0 + 4);
+            emit4(xb, true, q0);
+            q0 += 4;
         }
+        for (; q0 < w1; q0 += 4) emit4(xa, false, q0);
         base += piece_total;
-        __syncthreads();  // s_wcnt / s_lo reuse
+    };
+    // Warp-specialised pipeline: while the counters stream piece i from HBM
+    // into L2, the compactors write piece i-1's survivors, so HBM reads and
+    // writes overlap.  The counts of piece i-1 were published by every CTA
+    // during the previous step; the only CTA-wide barrier is the one per
+    // step that hands s_wcnt over between the roles.
+    for (int64_t i = 0; i <= npieces; ++i) {
+#if SDFGB_Q_TIMING
+        if ((tid == 0 || tid == NW * 32) && i < 64) g_qtime[i][counter ? 0 : 2][c] = gtime();
+#endif
+        if (counter) {
+            if (i < npieces) phaseA(i);
+        } else if (i > 0) {
+            phaseB(i - 1);
+        }
+#if SDFGB_Q_TIMING
+        if ((tid == 0 || tid == NW * 32) && i < 64) g_qtime[i][counter ? 1 : 3][c] = gtime();
+#endif
+        named_bar(3, kQPBlock);  // counters + compactors
     }
-    if (c == 0 && tid == 0) atomicAdd(count, (unsigned long long)base);
+    if (c == 0 && tid == NW * 32) atomicAdd(count, (unsigned long long)base);
 }
 
 // ---------------------------------------------------------------------------
@@ -885,11 +944,13 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
         auto pk = query_piece_kernel_for<T>(kop);
         static int pocc[2][8] = {};
         int& po = pocc[sizeof(T) == 8][kop];
-        if (po == 0) SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&po, pk, kQBlock, 0));
+        if (po == 0) SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&po, pk, kQPBlock, 0));
         const int64_t G = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(po, 1) * num_sms(), (int64_t)kTBlock));
         auto* cnts = W->status;
-        void* args[] = {(void*)&col, (void*)&n, (void*)&tt, (void*)&out, (void*)&C, (void*)&cnts};
-        SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)pk, dim3((unsigned)G), dim3(kQBlock), args, 0, s));
+        uint32_t ep = epoch;
+        // cooperative: every CTA co-resident (B waits on all CTAs' counts)
+        void* args[] = {(void*)&col, (void*)&n, (void*)&tt, (void*)&out, (void*)&C, (void*)&cnts, (void*)&ep};
+        SDFGB_CUDA(cudaLaunchCooperativeKernel((const void*)pk, dim3((unsigned)G), dim3(kQPBlock), args, 0, s));
         return SDFGB_OK;
     }
     auto kern = vec ? query_kernel_for<T, true>(kop) : query_kernel_for<T, false>(kop);
@@ -908,13 +969,20 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
 }  // namespace
 }  // namespace sdfgb
 
+#if SDFGB_Q_TIMING
+extern "C" int sdfgb_debug_query_timing(void* host) {
+    return cudaMemcpyFromSymbol(host, sdfgb::g_qtime, sizeof(sdfgb::g_qtime)) == cudaSuccess ? 0 : 1;
+}
+#endif
 extern "C" size_t sdfgb_query_workspace_bytes(int64_t n, int elem_bytes) {
-    // one status word per (round, CTA) slot of the register-path kernel:
-    // rounds * G <= segments + G - 1; the piece kernel needs pieces * G
-    // count slots, fewer than that
+    // one status word per (round, CTA) slot of the register-path kernel
+    // (rounds * G <= segments + G - 1) or per (piece, CTA) of the piece
+    // kernel (G <= kTBlock), whichever is more
     const int64_t seg = elem_bytes == 8 ? sdfgb::seg_elems<double>() : sdfgb::seg_elems<float>();
     const int64_t segs = (n + seg - 1) / seg;
-    return offsetof(sdfgb::QueryWs, status) + (size_t)(segs + sdfgb::kTBlock) * 8;
+    const int64_t pieces = (n * (int64_t)elem_bytes + sdfgb::kPieceBytes - 1) / sdfgb::kPieceBytes;
+    const int64_t slots = std::max<int64_t>(segs + sdfgb::kTBlock, pieces * sdfgb::kTBlock);
+    return offsetof(sdfgb::QueryWs, status) + (size_t)slots * 8;
 }
 extern "C" int sdfgb_query_f32(const float* col, int64_t n, int op, double thr, float* out_vals,
                                int64_t* count, void* ws, size_t ws_bytes, void* stream) {

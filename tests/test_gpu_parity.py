@@ -254,6 +254,27 @@ def test_query_f64(ordered):
     np.testing.assert_array_equal(got, rout)
 
 
+@pytest.mark.parametrize("dtype,thr", [(np.float32, 0.0), (np.float32, 0.03), (np.float32, 0.5),
+                                       (np.float32, 1.0), (np.float64, 0.5)])
+def test_query_ordered_many_pieces(dtype, thr):
+    """FIFO order across several 64 MB pieces (the piece kernel's counts of
+    piece p+1 are published while piece p is compacted); a ragged tail and
+    0 / 3 / 50 / 100 % selectivity exercise the per-warp stage carry"""
+    from paper_1902_10345_b200 import device
+    n = (160 << 20) // np.dtype(dtype).itemsize + 12345
+    col = np.random.default_rng(int(thr * 100) + n).random(n).astype(dtype)
+    out = torch.full((n,), -1.0, dtype=torch.from_numpy(col[:1]).dtype, device=DEV)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    ws = device.query_workspace(n, col.itemsize, DEV)
+    for rep in range(2):
+        out.fill_(-1.0)
+        cnt.zero_()
+        device.query(t(col), thr, out, cnt, ws, "<", ordered=True)
+        rout, rcnt = oracle.query(col, thr, np.full(n, -1.0, dtype), np.zeros(1, np.int64), "<")
+        assert cnt.item() == rcnt[0]
+        np.testing.assert_array_equal(out.cpu().numpy(), rout)
+
+
 def test_query_mixed_modes_share_workspace():
     """ordered and unordered launches alternate on one workspace; the
     unordered kernel's counter/ticket must be left zeroed every time"""
