@@ -775,20 +775,26 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
         // valid once p >= 2k; level F (p >= 2F) is output row y0 + p - 2F.
         // MODE 0: steady state; 1: prologue (PRO = p, compile time); 2: tail
         // (rows may reach M-1)
+        // stage state carried from step to step (no per-row division or
+        // modulo): `it` = this tile's stage (p / 3), `slot` its ring slot,
+        // `par` its mbarrier parity; the ring runs on across tiles
+        int it = 0, slot = (int)(sbase % kSpStages);
+        uint32_t par = (uint32_t)((sbase / kSpStages) & 1);
+        // output row y0 + p - 2F of this lane, advanced by one row per step
+        float* drow = dst + (int64_t)(y0 - 2 * F) * N + gx;
         auto step = [&](auto u_tag, int p, auto pro_tag, auto mode_tag) {
             constexpr int u = decltype(u_tag)::value;  // p mod 3
             constexpr int PRO = decltype(pro_tag)::value;
             constexpr int MODE = decltype(mode_tag)::value;
             constexpr int sn = (u + 1) % 3, sc = (u + 2) % 3;
-            const int it = p / 3;  // this tile's stage; the ring runs on across tiles
-            const int slot = (int)((sbase + it) % kSpStages), pslot = (int)((sbase + it + kSpStages - 1) % kSpStages);
+            const int pslot = slot == 0 ? kSpStages - 1 : slot - 1;
             float* stage = ring + slot * kSpStageF;
             const float* prev = ring + pslot * kSpStageF;
             if constexpr (u == 0) {
                 // every lane polls and the loop condition is a warp vote, so
                 // the warp stays provably converged and the shuffles stay
                 // plain SHFLs
-                const uint32_t a = smem_u32(bars + slot), par = (uint32_t)(((sbase + it) / kSpStages) & 1);
+                const uint32_t a = smem_u32(bars + slot);
                 while (!__all_sync(0xffffffffu, mbar_try_wait(a, par))) {
                 }
             }
@@ -831,7 +837,7 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
                 bool keep = lane >= kSpPad / 4 && lane < (kSpPad + kSpX) / 4;
                 if constexpr (MODE == 1) keep = keep && r >= 1;
                 if constexpr (MODE == 2) keep = keep && r <= M - 2;
-                float* d = dst + (int64_t)r * N + gx;
+                float* d = drow;
                 if constexpr (!COLB) {
                     if (keep) *reinterpret_cast<float4*>(d) = o;
                 } else {
@@ -870,6 +876,14 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
                 }
             }
 #endif
+            if constexpr (u == 2) {  // next stage
+                ++it;
+                if (++slot == kSpStages) {
+                    slot = 0;
+                    par ^= 1u;
+                }
+            }
+            drow += N;
         };
         using I0 = std::integral_constant<int, 0>;
         using I1 = std::integral_constant<int, 1>;
