@@ -275,6 +275,23 @@ def test_query_ordered_many_pieces(dtype, thr):
         np.testing.assert_array_equal(out.cpu().numpy(), rout)
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("pieces,delta", [(1, -1), (1, 1), (2, 0), (2, 129), (3, -517)])
+def test_query_ordered_piece_boundaries(dtype, pieces, delta):
+    """sizes at and around whole multiples of the FIFO kernel's 32 MB piece:
+    equalised pieces, the last CTA's short range and the column's ragged
+    tail all meet the per-piece count words"""
+    from paper_1902_10345_b200 import device
+    n = pieces * (32 << 20) // np.dtype(dtype).itemsize + delta
+    col = np.random.default_rng(n).random(n).astype(dtype)
+    out = torch.full((n,), -1.0, dtype=torch.from_numpy(col[:1]).dtype, device=DEV)
+    cnt = torch.full((1,), 3, dtype=torch.int64, device=DEV)
+    device.query(t(col), 0.7, out, cnt, device.query_workspace(n, col.itemsize, DEV), ">=", ordered=True)
+    rout, rcnt = oracle.query(col, 0.7, np.full(n, -1.0, dtype), np.array([3], np.int64), ">=")
+    assert cnt.item() == rcnt[0]
+    np.testing.assert_array_equal(out.cpu().numpy(), rout)
+
+
 def test_query_mixed_modes_share_workspace():
     """ordered and unordered launches alternate on one workspace; the
     unordered kernel's counter/ticket must be left zeroed every time"""
