@@ -292,6 +292,28 @@ def test_query_ordered_piece_boundaries(dtype, pieces, delta):
     np.testing.assert_array_equal(out.cpu().numpy(), rout)
 
 
+@pytest.mark.parametrize("ordered", [False, True])
+def test_query_beyond_int32_elements(ordered):
+    """2^31 + 12345 elements (8.6 GB in, up to 8.6 GB out): element counts,
+    offsets and chunk indices past 32 bits.  Checked through properties
+    (the count; the survivors equal the masked column, in FIFO order or as
+    a sorted multiset)"""
+    from paper_1902_10345_b200 import device
+    n = (1 << 31) + 12345
+    g = torch.Generator(device=DEV).manual_seed(7)
+    col = torch.rand(n, device=DEV, generator=g)
+    out = torch.empty(n, device=DEV)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    device.query(col, 0.25, out, cnt, device.query_workspace(n, 4, DEV), "<", ordered=ordered)
+    sel = col[col < 0.25]
+    k = sel.numel()
+    assert cnt.item() == k
+    if ordered:
+        assert torch.equal(out[:k], sel)
+    else:
+        assert torch.equal(torch.sort(out[:k]).values, torch.sort(sel).values)
+
+
 def test_query_mixed_modes_share_workspace():
     """ordered and unordered launches alternate on one workspace; the
     unordered kernel's counter/ticket must be left zeroed every time"""
@@ -420,6 +442,20 @@ def test_full_histogram_4096():
     ref, _ = oracle.histogram(img, np.zeros(256, np.int64))
     np.testing.assert_array_equal(h.cpu().numpy(), ref)
     assert int(h.sum()) == img.size
+
+
+def test_histogram_beyond_int32_elements():
+    """2^31 + 999 pixels (8.6 GB): per-bin counts past 32 bits of element
+    index, checked against torch.bincount of the same binning"""
+    from paper_1902_10345_b200 import device
+    n = (1 << 31) + 999
+    g = torch.Generator(device=DEV).manual_seed(3)
+    img = torch.rand(n, device=DEV, generator=g)
+    h = torch.zeros(256, dtype=torch.int64, device=DEV)
+    oob = torch.zeros(1, dtype=torch.int64, device=DEV)
+    device.hist(img, h, oob)
+    ref = torch.bincount((img * 256.0).to(torch.int64), minlength=256)
+    assert torch.equal(h, ref) and oob.item() == 0 and int(h.sum()) == n
 
 
 def test_full_query_2pow26():
