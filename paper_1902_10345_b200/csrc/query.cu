@@ -318,27 +318,32 @@ __device__ __forceinline__ void st_pred(double* base, uint32_t idx, double v, ui
 
 // ---------------------------------------------------------------------------
 // Piece kernel (the default for 16 B-aligned columns).  The column is cut
-// into equal pieces of at most 32 MB, and each co-resident CTA owns the same
+// into equal pieces of at most 16 MB, and each co-resident CTA owns the same
 // contiguous chunk range of every piece, cut into NW warp ranges.  Two warp
-// roles run as a pipeline, one piece apart:
-//   A  (counter warps)    count piece i's warp ranges from HBM (L2
+// roles run as a pipeline:
+//   A  (counter warps)    count piece p's warp ranges from HBM (L2
 //      evict_last, a rolling ring of 8 vector loads per lane), then publish
-//      the CTA's total as an epoch-tagged word cnts[i*G + c];
-//   B  (compactor warps)  read piece i-1's G CTA totals (spinning only on
-//      words not yet published) for the CTA's offset, then re-read each warp
-//      range from L2 (evict_first, two 4-chunk register sets so the next
-//      loads are in flight) and compact it in order: byte-packed chunk
-//      counts, one 32-bit shuffle scan per 4 chunks, predicated stores.
-// So HBM reads of piece i overlap the survivor writes of piece i-1, two
-// pieces (64 MB) are L2-resident at a time, HBM sees each input byte once,
-// and no grid-wide barrier is needed (the cooperative launch only guarantees
-// that every CTA is resident).  One CTA barrier per step hands the per-warp
-// counts from the counters to the compactors.
+//      the CTA's total as an epoch-tagged word cnts[p*G + c] and the
+//      per-warp counts in a shared-memory slot (full mbarrier);
+//   B  (compactor warps)  read piece p's G CTA totals (spinning only on
+//      words not yet published) for the CTA's offset, take the per-warp
+//      counts from the slot (empty mbarrier), then re-read each warp range
+//      from L2 (evict_first, two 4-chunk register sets so the next loads are
+//      in flight) and compact it in order: byte-packed chunk counts, one
+//      32-bit shuffle scan per 4 chunks, predicated stores.
+// So HBM reads of one piece overlap the survivor writes of earlier ones, the
+// counters run up to SDFGB_Q_SLOTS pieces ahead (so at most ~4 pieces are
+// L2-resident), HBM sees each input byte once, and there is no grid-wide or
+// per-step CTA barrier (the cooperative launch only guarantees that every
+// CTA is resident).
 #ifndef SDFGB_Q_PIECE_MB
-#define SDFGB_Q_PIECE_MB 32
+#define SDFGB_Q_PIECE_MB 16
 #endif
 #ifndef SDFGB_Q_MINB
 #define SDFGB_Q_MINB 1
+#endif
+#ifndef SDFGB_Q_SLOTS
+#define SDFGB_Q_SLOTS 3  // per-warp count slots between the roles: counters run up to 3 pieces ahead
 #endif
 #ifndef SDFGB_Q_RING
 #define SDFGB_Q_RING 8  // chunk loads in flight per counter lane
@@ -363,7 +368,7 @@ constexpr int kQPBlock = SDFGB_Q_PBLOCK;
 #define SDFGB_Q_TIMING 0  // debug: per-CTA role timestamps (sdfgb_debug_query_timing)
 #endif
 #if SDFGB_Q_TIMING
-__device__ unsigned long long g_qtime[64][4][1024];  // [iteration][A0,A1,B0,B1][CTA]
+__device__ unsigned long long g_qtime[64][4][1024];  // [piece][A0,A1,B0,B1][CTA]
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -383,13 +388,28 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
     // equal pieces of at most kPieceBytes, multiples of a chunk
     const int64_t npieces = (n * (int64_t)sizeof(T) + kPieceBytes - 1) / kPieceBytes;
     const int64_t PIECE = ((n + npieces - 1) / npieces + CH - 1) / CH * CH;
-    __shared__ uint32_t s_wcnt[2][NW];  // per-warp counts of the two pieces in flight
-    __shared__ int64_t s_lo[NW], s_to[NW];
+    constexpr int SL = SDFGB_Q_SLOTS;
+    __shared__ uint32_t s_wcnt[SL][NW];  // per-warp counts of the pieces in flight
+    __shared__ __align__(8) uint64_t s_full[SL], s_empty[SL];
+    __shared__ int64_t s_lo[2][NW], s_to[2][NW];
 
     const int tid = threadIdx.x, lane = tid & 31;
     const bool counter = tid < NW * 32;
     const int warp = (tid >> 5) - (counter ? 0 : NW);  // index within the role
     const int rtid = tid - (counter ? 0 : NW * 32);
+    if (tid == 0) {
+        for (int k = 0; k < SL; ++k) {
+            mbar_init(&s_full[k], 1);
+            mbar_init(&s_empty[k], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto wait_bar = [&](uint64_t* b, uint32_t par) {
+        while (!__all_sync(0xffffffffu, mbar_try_wait(smem_u32(b), par))) {
+        }
+    };
+#define SLOT(p) ((int)((p) % SL))
     const int64_t G = gridDim.x, c = blockIdx.x;
     const uint64_t keep = make_policy(true), drop = make_policy(false);
     // warp range r's chunks [w0, w1) of piece p (starting at element ps)
@@ -451,13 +471,16 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
             }
         }
         cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0) s_wcnt[p & 1][warp] = cnt;
+        // the slot's previous piece (p - SL) has been read by every compactor warp
+        if (p >= SL) wait_bar(&s_empty[SLOT(p)], (uint32_t)((p / SL - 1) & 1));
+        if (lane == 0) s_wcnt[SLOT(p)][warp] = cnt;
         named_bar(1, NW * 32);  // the counters only
         if (tid == 0) {
             uint32_t t = 0;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) t += s_wcnt[p & 1][w];
+            for (int w = 0; w < NW; ++w) t += s_wcnt[SLOT(p)][w];
             st_relaxed(cnts + p * G + c, pack_status(epoch, kFlagAgg, t));
+            mbar_arrive(&s_full[SLOT(p)]);
         }
     };
     int64_t base = 0;
@@ -482,18 +505,23 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
             lo += __shfl_xor_sync(0xffffffffu, lo, d);
             to += __shfl_xor_sync(0xffffffffu, to, d);
         }
+        int64_t* slo = s_lo[p & 1];  // double-buffered: a fast warp may reach the next piece
+        int64_t* sto = s_to[p & 1];
         if (lane == 0) {
-            s_lo[warp] = lo;
-            s_to[warp] = to;
+            slo[warp] = lo;
+            sto[warp] = to;
         }
         named_bar(2, NW * 32);  // the compactors only
         int64_t cta_off = 0, piece_total = 0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-            cta_off += s_lo[w];
-            piece_total += s_to[w];
+            cta_off += slo[w];
+            piece_total += sto[w];
         }
-        uint32_t wc = lane < warp ? s_wcnt[p & 1][lane] : 0u;
+        wait_bar(&s_full[SLOT(p)], (uint32_t)((p / SL) & 1));
+        uint32_t wc = lane < warp ? s_wcnt[SLOT(p)][lane] : 0u;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[SLOT(p)]);
 #pragma unroll
         for (int d = 16; d; d >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, d);
         T* wout = out + (base + cta_off + wc);
@@ -573,19 +601,19 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
     // writes overlap.  The counts of piece i-1 were published by every CTA
     // during the previous step; the only CTA-wide barrier is the one per
     // step that hands s_wcnt over between the roles.
-    for (int64_t i = 0; i <= npieces; ++i) {
+    // The roles hand the per-warp counts over through SL shared-memory slots
+    // (full / empty mbarriers), so each runs at its own pace: the counters
+    // stream piece p from HBM into L2 while the compactors write the
+    // survivors of an earlier piece, up to SL pieces behind.
+    for (int64_t p = 0; p < npieces; ++p) {
 #if SDFGB_Q_TIMING
-        if ((tid == 0 || tid == NW * 32) && i < 64) g_qtime[i][counter ? 0 : 2][c] = gtime();
+        if ((tid == 0 || tid == NW * 32) && p < 64) g_qtime[p][counter ? 0 : 2][c] = gtime();
 #endif
-        if (counter) {
-            if (i < npieces) phaseA(i);
-        } else if (i > 0) {
-            phaseB(i - 1);
-        }
+        if (counter) phaseA(p);
+        else phaseB(p);
 #if SDFGB_Q_TIMING
-        if ((tid == 0 || tid == NW * 32) && i < 64) g_qtime[i][counter ? 1 : 3][c] = gtime();
+        if ((tid == 0 || tid == NW * 32) && p < 64) g_qtime[p][counter ? 1 : 3][c] = gtime();
 #endif
-        named_bar(3, kQPBlock);  // counters + compactors
     }
     if (c == 0 && tid == NW * 32) atomicAdd(count, (unsigned long long)base);
 }

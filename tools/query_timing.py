@@ -1,7 +1,7 @@
 """Per-CTA role timestamps of the FIFO query piece kernel, from a library
 built with -DSDFGB_Q_TIMING=1 (tools/lib_variants.sh query.cu
-"qt:-DSDFGB_Q_TIMING=1", then SDFGB_LIB=...lib_qt.so): per pipeline step i,
-the counters' A(i) and the compactors' B(i-1) span (2^26 fp32, x < 0.5)."""
+"qt:-DSDFGB_Q_TIMING=1", then SDFGB_LIB=...lib_qt.so): per piece p, the
+counters' A(p) and the compactors' B(p) span (2^26 fp32, x < 0.5)."""
 import ctypes
 import sys
 
@@ -31,6 +31,6 @@ for i in range(64):
     if t[i, 0, 0] == 0:
         break
     a0, a1, b0, b1 = [(t[i, k, :G] - t0) / 1e3 for k in range(4)]
-    print(f"step {i}: A {np.median(a1 - a0):6.1f} us (max {np.max(a1 - a0):6.1f})   "
+    print(f"piece {i}: A {np.median(a1 - a0):6.1f} us (max {np.max(a1 - a0):6.1f})   "
           f"B {np.median(b1 - b0):6.1f} (max {np.max(b1 - b0):6.1f})   "
           f"[start {min(a0.min(), b0.min()):6.1f} .. end {max(a1.max(), b1.max()):6.1f}]")
