@@ -24,12 +24,10 @@
 #include <atomic>
 #include <cmath>
 
-#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "tma.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace sdfgb {
 namespace {
@@ -968,7 +966,7 @@ int launch_query(const T* col, int64_t n, int op, double thr, T* out, int64_t* c
         return SDFGB_OK;
     }
     if (vec && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-        // piece kernel: co-resident CTAs, one grid barrier per 64 MB piece
+        // piece kernel: co-resident CTAs (the compactors wait on every CTA's counts)
         auto pk = query_piece_kernel_for<T>(kop);
         static int pocc[2][8] = {};
         int& po = pocc[sizeof(T) == 8][kop];
