@@ -373,6 +373,27 @@ __device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t adesc
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u)
         : "memory");
 }
+// the same MMA with an A-collector hint: FILL keeps the A tile in the
+// tensor core's operand collector, LASTUSE reads it from there (no second
+// shared-memory read of A) and releases it
+enum { kCollFill = 1, kCollLastUse = 2 };
+template <int COLL>
+__device__ __forceinline__ void tc_mma_tf32_pair_c(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                   uint32_t accumulate) {
+    if constexpr (COLL == kCollFill) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::tf32.collector::a::fill [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::tf32.collector::a::lastuse [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
+}
 __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on this offset in both CTAs
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -381,6 +402,9 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on th
         : "memory");
 }
 
+#ifndef SDFGB_GEMM_AREUSE
+#define SDFGB_GEMM_AREUSE 1  // A-collector reuse between the two A-hi MMAs of a K = 8 step
+#endif
 #ifndef SDFGB_GEMM_PAIR_GROUP
 #define SDFGB_GEMM_PAIR_GROUP 8  // tile rows per rasterisation group (sweep: 4 / 8 / 16 / 32)
 #endif
@@ -514,9 +538,16 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_c
                     const uint64_t blo = BMN ? sw128_mnmajor_desc(base + 2 * TILE_BYTES + BTILE2 + k * SDFGB_BMN_KSTEP,
                                                                   SDFGB_BMN_LBO, SDFGB_BMN_SBO)
                                              : sw128_kmajor_desc(base + 2 * TILE_BYTES + BTILE2 + off);
+#if SDFGB_GEMM_AREUSE
+                    // A hi feeds two MMAs from one shared-memory read
+                    tc_mma_tf32_pair_c<kCollFill>(dacc, ahi, blo, idesc, !(first && k == 0));
+                    tc_mma_tf32_pair_c<kCollLastUse>(dacc, ahi, bhi, idesc, 1u);
+                    tc_mma_tf32_pair(dacc, alo, bhi, idesc, 1u);
+#else
                     tc_mma_tf32_pair(dacc, alo, bhi, idesc, !(first && k == 0));
                     tc_mma_tf32_pair(dacc, ahi, blo, idesc, 1u);
                     tc_mma_tf32_pair(dacc, ahi, bhi, idesc, 1u);
+#endif
                 }
                 tc_commit_pair(&empty[s]);
             }
