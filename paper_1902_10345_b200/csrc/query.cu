@@ -615,6 +615,7 @@ query_piece_kernel(const T* __restrict__ col, int64_t n, T thr, T* __restrict__ 
     }
     if (c == 0 && tid == NW * 32) atomicAdd(count, (unsigned long long)base);
 }
+#undef SLOT
 
 // ---------------------------------------------------------------------------
 // Unordered push kernel (the default).  A Map's iterations are concurrent and
