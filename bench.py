@@ -609,14 +609,19 @@ def bench_jacobi(args, dist, P):
         slab0 = MG.jacobi_slab(rows, g0, Ng)
         del rows
         slab = MG.JacobiSlab(slab0.A.clone(), slab0.g0, slab0.rows, slab0.Ng, slab0.top, slab0.bot)
+        # opt-in: the ghost exchange fused into the edge-band kernels over
+        # NVLink (multigpu.PeerJacobi) instead of NCCL send/recv
+        jp2p = os.environ.get("SDFGB_BENCH_JACOBI_P2P", "0") == "1"
+        peer = MG.PeerJacobi(dist.pg, slab) if jp2p else None
     else:
         lo, hi = 0, N
         A = _dev(A0h)
         A0 = A.clone()
+        jp2p = False
 
     def step(k):
         if multi:
-            MG.jacobi(dist.pg, slab, T, be)
+            MG.jacobi(dist.pg, slab, T, be, p2p=peer)
         else:
             device.jacobi2d(A, T)
 
@@ -628,7 +633,7 @@ def bench_jacobi(args, dist, P):
         R = _jacobi_restated(torch.from_numpy(A0h).cuda(), T)
         if multi:
             chk = MG.JacobiSlab(slab0.A.clone(), slab0.g0, slab0.rows, slab0.Ng, slab0.top, slab0.bot)
-            MG.jacobi(dist.pg, chk, T, be)
+            MG.jacobi(dist.pg, chk, T, be, p2p=MG.PeerJacobi(dist.pg, chk) if jp2p else None)
             got = chk.A[:, chk.top:chk.top + (hi - lo)]
         else:
             got = A0.clone()
@@ -662,7 +667,9 @@ def bench_jacobi(args, dist, P):
                         "traffic": tb, "traffic_note": tnote},
            "l2": "2 x 256 MiB planes > L2", "check": check,
            "config": {"workload": "Jacobi-2D 8192^2 fp32, T=1000 (whole time loop per step)", "rows": [lo, hi],
-                      "T": T},
+                      "T": T, **({"exchange": "edge bands stored into the neighbours' ghost rows over NVLink"
+                                  if jp2p else "ncclSend/Recv of the edge bands under the interior band"}
+                                 if multi else {})},
            "steps": steps, "warmup": 1}
     if args.e2e and not multi:
         L = _lib.load()

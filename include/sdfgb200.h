@@ -161,6 +161,14 @@ int sdfgb_jacobi2d_block_f32(const float* src, float* dst, int64_t M, int64_t N,
  * needs N >= 128 and at least 8 interior rows. */
 int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k,
                             int64_t r0, int64_t r1, double coef, void* stream);
+/* The same band, its output rows r in [m0, m1) also stored at
+ * mirror + (r - m0) * N: a neighbour rank's ghost rows in peer memory
+ * (NVLink), so an edge band and its ghost-row transfer are one kernel
+ * (multigpu.jacobi with PeerJacobi).  k == 1 runs the one-step kernel and
+ * then copies those rows. */
+int sdfgb_jacobi2d_band_mirror_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k,
+                                   int64_t r0, int64_t r1, double coef, float* mirror, int64_t m0,
+                                   int64_t m1, void* stream);
 /* Host-only introspection of the strip kernel's tile queue for output rows
  * [r0, r1) of an M x N plane and `resident` persistent warps: tiles[3t..3t+2]
  * = (strip, y0, ye) of entry t (at most max_tiles written); returns the
@@ -202,6 +210,12 @@ int sdfgb_nccl_available(void);
 /* Kernels on the current device may access memory on device `peer` (the
  * P2P entries' peer mappings); already-enabled is success. */
 int sdfgb_enable_peer_access(int peer);
+/* Stream-ordered cross-rank flags for kernels that write peer memory:
+ * signal stores `value` into `flag` (system-scope release) after all work
+ * queued before it on the stream; wait holds the stream until `flag` (this
+ * device's memory) reaches `value`.  Flags only grow. */
+int sdfgb_flag_signal(int* flag, int value, void* stream);
+int sdfgb_flag_wait(const int* flag, int value, void* stream);
 int sdfgb_nccl_unique_id(void* id_out /* 128 bytes */);
 int sdfgb_nccl_comm_init(void** comm_out, int nranks, const void* id, int rank);
 int sdfgb_nccl_comm_destroy(void* comm);

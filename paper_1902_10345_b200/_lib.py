@@ -65,6 +65,9 @@ SIGNATURES = {
     "sdfgb_jacobi2d_rect_f32": (_INT, [_P, _I64, _I64, _I64, _F64, _P, _P, _INT, _P]),
     "sdfgb_jacobi2d_block_f32": (_INT, [_P, _P, _I64, _I64, _I64, _F64, _P]),
     "sdfgb_jacobi2d_band_f32": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _I64, _F64, _P]),
+    "sdfgb_jacobi2d_band_mirror_f32": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _I64, _F64, _P, _I64, _I64, _P]),
+    "sdfgb_flag_signal": (_INT, [_P, _INT, _P]),
+    "sdfgb_flag_wait": (_INT, [_P, _INT, _P]),
     "sdfgb_debug_strip_tiles": (_I64, [_I64, _I64, _I64, _I64, _I64, _P, _I64]),
     "sdfgb_probe_gather_f32": (_INT, [_P, _P, _P, _I64, _P, _P]),
     "sdfgb_gemm_workspace_bytes": (_SZ, [_I64, _I64, _I64]),

@@ -788,6 +788,35 @@ extern "C" int sdfgb_enable_peer_access(int peer) {
     return check_cuda(e, "cudaDeviceEnablePeerAccess");
 }
 
+// Cross-rank ordering for kernels that write peer memory: signal stores
+// `value` into a flag (usually a peer rank's, over NVLink) once everything
+// queued before it on the stream is done and visible system-wide; wait
+// holds the stream until a (local) flag reaches `value`.  Flags only grow.
+__global__ void flag_signal_kernel(int* flag, int value) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+__global__ void flag_wait_kernel(const int* flag, int value) {
+    int v;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v >= value) break;
+        __nanosleep(256);
+    }
+}
+extern "C" int sdfgb_flag_signal(int* flag, int value, void* stream) {
+    if (!flag) return set_error(SDFGB_ERR_INVALID, "flag_signal: null flag");
+    flag_signal_kernel<<<1, 1, 0, as_stream(stream)>>>(flag, value);
+    SDFGB_LAUNCHED("flag_signal_kernel");
+    return SDFGB_OK;
+}
+extern "C" int sdfgb_flag_wait(const int* flag, int value, void* stream) {
+    if (!flag) return set_error(SDFGB_ERR_INVALID, "flag_wait: null flag");
+    flag_wait_kernel<<<1, 1, 0, as_stream(stream)>>>(flag, value);
+    SDFGB_LAUNCHED("flag_wait_kernel");
+    return SDFGB_OK;
+}
+
 extern "C" int sdfgb_host_alloc(void** ptr, size_t bytes) {
     return check_cuda(cudaHostAlloc(ptr, std::max<size_t>(bytes, 1), cudaHostAllocPortable), "cudaHostAlloc");
 }

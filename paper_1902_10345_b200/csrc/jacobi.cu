@@ -570,6 +570,8 @@ __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
 }
 constexpr int kSpWarps = 4, kSpStages = 6, kSpRX = 128, kSpPad = 8, kSpX = kSpRX - 2 * kSpPad;
 constexpr int kSpStageF = 3 * kSpRX;  // floats per stage (3 rows)
+// the strip kernel needs >= 2 strips (each holds at most one border column)
+inline bool strip_ok(int64_t N) { return N > kSpX + kSpPad + 4; }
 // per warp: the TMA ring, then [plane 0/1][rows] of its border column
 // (rows rounded to 16: every warp's ring stays 128 B aligned for TMA)
 __host__ __device__ constexpr int sp_rows(int nrows) { return (nrows + 15) / 16 * 16; }
@@ -624,10 +626,14 @@ constexpr int kSpSchedSlots = 4096;
 __device__ int g_sp_sched[kSpSchedSlots * 2];
 std::atomic<int> g_sp_launches{0};
 
-template <int F>
+// MIRROR: output rows [mr0, mr1) are also stored moff elements further on --
+// into a neighbour rank's ghost rows over NVLink (peer memory), so a slab's
+// edge band and its ghost-row transfer are one kernel (multigpu.jacobi, p2p)
+template <int F, bool MIRROR = false>
 __global__ void __launch_bounds__(kSpWarps * 32, 4)
 jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* src, const float* dst_in,
-                    float* dst, int M, int N, StripPlan plan, int nwarps, int sched_slot, float coef) {
+                    float* dst, int M, int N, StripPlan plan, int nwarps, int sched_slot, float coef,
+                    int64_t moff, int mr0, int mr1) {
     // output rows [ra, rb) of the plane (the whole plane, or one band of it).
     // Persistent warps: each takes tiles from the launch's counter until
     // none are left, so the tiles' uneven durations balance out and no
@@ -840,6 +846,9 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
                 float* d = drow;
                 if constexpr (!COLB) {
                     if (keep) *reinterpret_cast<float4*>(d) = o;
+                    if constexpr (MIRROR) {
+                        if (keep && r >= mr0 && r < mr1) *reinterpret_cast<float4*>(d + moff) = o;
+                    }
                 } else {
                     // predicated stores only (no lane-divergent branch, which
                     // would wrap the next shuffles in warp re-convergence):
@@ -852,6 +861,15 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
                     if (part && gx + 1 >= 1 && gx + 1 <= N - 2) d[1] = o.y;
                     if (part && gx + 2 >= 1 && gx + 2 <= N - 2) d[2] = o.z;
                     if (part && gx + 3 >= 1 && gx + 3 <= N - 2) d[3] = o.w;
+                    if constexpr (MIRROR) {
+                        float* m = d + moff;
+                        const bool mk = r >= mr0 && r < mr1;
+                        if (full && mk) *reinterpret_cast<float4*>(m) = o;
+                        if (mk && part && gx >= 1 && gx <= N - 2) m[0] = o.x;
+                        if (mk && part && gx + 1 >= 1 && gx + 1 <= N - 2) m[1] = o.y;
+                        if (mk && part && gx + 2 >= 1 && gx + 2 <= N - 2) m[2] = o.z;
+                        if (mk && part && gx + 3 >= 1 && gx + 3 <= N - 2) m[3] = o.w;
+                    }
                 }
             }
 #if SDFGB_JSP_L0REG
@@ -973,9 +991,9 @@ StripPlan strip_plan(int64_t ra, int64_t rb, int64_t nstrips, int64_t resident_w
     return p;
 }
 
-template <int F>
+template <int F, bool MIRROR = false>
 int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra, int64_t rb, float coef,
-                 cudaStream_t s) {
+                 cudaStream_t s, int64_t moff = 0, int mr0 = 0, int mr1 = 0) {
     const int64_t nstrips = (N + kSpX - 1) / kSpX;
     // persistent: one co-resident wave of warps (4 CTAs x 4 warps per SM)
     const int64_t resident = (int64_t)num_sms() * 4 * kSpWarps;
@@ -983,7 +1001,7 @@ int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra,
     const size_t smem = sp_smem(plan.hmax + 2 * F);
     static size_t attr = 0;
     if (smem > attr) {
-        SDFGB_CUDA(cudaFuncSetAttribute(jacobi_strip_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SDFGB_CUDA(cudaFuncSetAttribute(jacobi_strip_kernel<F, MIRROR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
         attr = smem;
     }
@@ -994,14 +1012,15 @@ int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra,
     static size_t per_sm_smem = 0;
     if (!per_sm || per_sm_smem != smem) {
         per_sm_smem = smem;
-        SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_strip_kernel<F>, kSpWarps * 32, smem));
+        SDFGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_strip_kernel<F, MIRROR>,
+                                                                 kSpWarps * 32, smem));
         per_sm = std::max(per_sm, 1);
     }
     const int64_t nwarps = std::min<int64_t>(plan.total(), (int64_t)num_sms() * per_sm * kSpWarps);
     const unsigned blocks = (unsigned)((nwarps + kSpWarps - 1) / kSpWarps);
     const int slot = g_sp_launches.fetch_add(1) & (kSpSchedSlots - 1);
-    jacobi_strip_kernel<F><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, plan, (int)nwarps,
-                                                               slot, coef);
+    jacobi_strip_kernel<F, MIRROR><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, plan,
+                                                                       (int)nwarps, slot, coef, moff, mr0, mr1);
     SDFGB_LAUNCHED("jacobi_strip_kernel");
     return SDFGB_OK;
 }
@@ -1156,7 +1175,7 @@ extern "C" int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, 
         sdfgb::parse_terms(di, dj, 5, terms, canon);
         return sdfgb::launch_step<float>(src, dst, N, M, 0, r0, r1, (float)coef, terms, true, s);
     }
-    if (N <= sdfgb::kSpX + sdfgb::kSpPad + 4)
+    if (!sdfgb::strip_ok(N))
         return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k > 1 bands need N >= 128 (strip kernel)");
     if (r1 - r0 < 8)  // a strip tile needs >= 8 rows (its prologue never meets plane row M-1)
         return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k > 1 bands are at least 8 interior rows");
@@ -1164,6 +1183,42 @@ extern "C" int sdfgb_jacobi2d_band_f32(const float* src, float* dst, int64_t M, 
     if (k == 5) return sdfgb::launch_strip<5>(src, dst, M, N, r0, r1, (float)coef, s);
     if (k == 3) return sdfgb::launch_strip<3>(src, dst, M, N, r0, r1, (float)coef, s);
     return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band: k must be 1, 3, 5 or 7 (got %lld)", (long long)k);
+}
+
+// The band, with its output rows r in [m0, m1) also stored at
+// mirror + (r - m0) * N (a neighbour's ghost rows in peer memory): compute
+// and ghost transfer in one kernel.  k == 1 runs the one-step kernel and
+// then copies those rows.
+extern "C" int sdfgb_jacobi2d_band_mirror_f32(const float* src, float* dst, int64_t M, int64_t N, int64_t k,
+                                              int64_t r0, int64_t r1, double coef, float* mirror, int64_t m0,
+                                              int64_t m1, void* stream) {
+    if (!mirror || m0 > m1) return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band_mirror: bad mirror");
+    if (k == 1) {
+        SDFGB_TRY(sdfgb_jacobi2d_band_f32(src, dst, M, N, 1, r0, r1, coef, stream));
+        const int64_t a = std::max<int64_t>({r0, m0, 1}), b = std::min<int64_t>({r1, m1, M - 1});
+        if (b <= a) return SDFGB_OK;
+        return sdfgb::check_cuda(cudaMemcpyAsync(mirror + (a - m0) * N, dst + a * N, (size_t)((b - a) * N) * 4,
+                                                 cudaMemcpyDeviceToDevice, sdfgb::as_stream(stream)),
+                                 "jacobi2d_band_mirror copy");
+    }
+    if (M < 16 || N < 16 || (N % 4) != 0 || !src || !dst || (reinterpret_cast<uintptr_t>(src) & 15) != 0 ||
+        (reinterpret_cast<uintptr_t>(dst) & 15) != 0 || (reinterpret_cast<uintptr_t>(mirror) & 15) != 0 ||
+        r0 < 0 || r1 > M || r0 > r1)
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band_mirror: bad arguments");
+    const int64_t moff = (int64_t)(mirror - (dst + m0 * N));  // elements from a dst row to its mirror
+    r0 = std::max<int64_t>(r0, 1);
+    r1 = std::min<int64_t>(r1, M - 1);
+    if (r1 <= r0) return SDFGB_OK;
+    cudaStream_t s = sdfgb::as_stream(stream);
+    if (!sdfgb::strip_ok(N))
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band_mirror: k > 1 bands need N >= 128 (strip kernel)");
+    if (r1 - r0 < 8)
+        return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band_mirror: k > 1 bands are at least 8 interior rows");
+    const int a = (int)std::max<int64_t>(m0, 0), b = (int)std::min<int64_t>(m1, M);
+    if (k == 7) return sdfgb::launch_strip<7, true>(src, dst, M, N, r0, r1, (float)coef, s, moff, a, b);
+    if (k == 5) return sdfgb::launch_strip<5, true>(src, dst, M, N, r0, r1, (float)coef, s, moff, a, b);
+    if (k == 3) return sdfgb::launch_strip<3, true>(src, dst, M, N, r0, r1, (float)coef, s, moff, a, b);
+    return sdfgb::set_error(SDFGB_ERR_INVALID, "jacobi2d_band_mirror: k must be 1, 3, 5 or 7 (got %lld)", (long long)k);
 }
 
 #if SDFGB_JSP_TIMING

@@ -129,6 +129,29 @@ def jacobi2d_band(src, dst, k, r0, r1, coef=0.2, stream=None):
                                          _stream(stream)))
 
 
+def jacobi2d_band_mirror(src, dst, k, r0, r1, mirror_ptr, m0, m1, coef=0.2, stream=None):
+    """jacobi2d_band, its output rows r in [m0, m1) also stored at
+    mirror_ptr + (r - m0) rows (a raw device address: a neighbour's ghost
+    rows in peer memory)."""
+    L = _lib.load()
+    M, N = src.shape[-2], src.shape[-1]
+    _lib.check(L.sdfgb_jacobi2d_band_mirror_f32(_p(src), _p(dst), M, N, int(k), int(r0), int(r1), float(coef),
+                                                ctypes.c_void_p(int(mirror_ptr)), int(m0), int(m1),
+                                                _stream(stream)))
+
+
+def flag_signal(flag_ptr, value, stream=None):
+    """Stream-ordered: store ``value`` into the int32 flag at ``flag_ptr``
+    (system-scope release) after the work queued before it."""
+    _lib.check(_lib.load().sdfgb_flag_signal(ctypes.c_void_p(int(flag_ptr)), int(value), _stream(stream)))
+
+
+def flag_wait(flag_ptr, value, stream=None):
+    """Stream-ordered: hold the stream until the int32 flag at ``flag_ptr``
+    reaches ``value``."""
+    _lib.check(_lib.load().sdfgb_flag_wait(ctypes.c_void_p(int(flag_ptr)), int(value), _stream(stream)))
+
+
 def jacobi2d_step(src, dst, N, rows, g0, r0, r1, coef=0.2, terms=JACOBI5, stream=None):
     L = _lib.load()
     di, dj = _terms(terms)

@@ -335,7 +335,7 @@ def jacobi_slab(A_global_rows, g0, Ng, ghost=GHOST):
 
 
 def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1)),
-           overlap=True):
+           overlap=True, p2p: "PeerJacobi" = None):
     """T steps of the guard loop (loops.py:31-61) over row blocks with
     ghost zones: the single-GPU temporal-blocking schedule (odd blocks of
     7/5/3 steps, then one final step so the other plane ends at state T-1)
@@ -348,7 +348,11 @@ def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (
     first computes the owned rows within EDGE of a neighbour -- the rows the
     neighbours' ghost zones need -- then posts the exchange of those rows
     and computes the interior band while it is in flight; the next block
-    waits for it.  Non-canonical stencil orders take one step per block."""
+    waits for it.  Non-canonical stencil orders take one step per block.
+
+    With ``p2p`` (a :class:`PeerJacobi`, device backend) the exchange is
+    fused into the edge-band kernels over NVLink instead
+    (:func:`jacobi_p2p_blocks`)."""
     rank, world = _rank_world(pg)
     A = slab.A
     canon = tuple(map(tuple, terms)) == ((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1))
@@ -360,6 +364,13 @@ def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (
     # other parity and never exchanged again
     _ghost_exchange(pg, A[1], slab, rank, world)
     _ghost_exchange(pg, A[0], slab, rank, world)
+    if p2p is not None and band:
+        for _ in jacobi_p2p_blocks(slab, p2p, T, coef):
+            pass
+        import torch
+        torch.cuda.current_stream().synchronize()
+        pg.barrier()  # no neighbour still writes into this rank's planes
+        return
     t = 0
     pending = None
     while t < T:
@@ -397,6 +408,122 @@ def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (
 
 
 EDGE = 16  # edge-band rows computed before the exchange (>= GHOST; the strip kernel's minimum band)
+
+
+class PeerJacobi:
+    """The neighbour slabs' planes and flag words mapped into this process
+    (CUDA IPC handles exchanged once through ``pg``), for the fused ghost
+    exchange of :func:`jacobi` (``p2p=``): the edge-band kernels store the
+    rows a neighbour's ghost zone needs straight into that neighbour's
+    planes over NVLink (sdfgb_jacobi2d_band_mirror_f32), and int32 flag words
+    order the ranks (sdfgb_flag_signal / sdfgb_flag_wait) -- no collective.
+
+    flags (this rank's, written by its neighbours): [0] blocks whose ghost
+    rows the rank above has delivered, [1] the same from the rank below,
+    [2] blocks the rank above has finished, [3] blocks the rank below has
+    finished.  Counts only grow (``base`` carries them across calls)."""
+
+    def __init__(self, pg=None, slab: "JacobiSlab" = None, _local=None):
+        import torch
+        self.base = 0
+        self.up = self.down = None
+        if _local is not None:  # one-process construction (tests): see pair()
+            return
+        from torch.multiprocessing.reductions import reduce_tensor
+        rank, world = _rank_world(pg)
+        self.flags = torch.zeros(4, dtype=torch.int32, device=slab.A.device)
+        mine = (reduce_tensor(slab.A), reduce_tensor(self.flags), slab.top, slab.rows, slab.bot)
+        allh = [None] * world
+        pg.all_gather_object(allh, mine)
+        mapped = []
+        for r in (rank - 1, rank + 1):
+            if 0 <= r < world:
+                (af, aa), (ff, fa), top, rows, bot = allh[r]
+                nb = {"A": af(*aa), "flags": ff(*fa), "top": top, "rows": rows, "bot": bot}
+                mapped += [nb["A"], nb["flags"]]
+            else:
+                nb = None
+            if r == rank - 1:
+                self.up = nb
+            else:
+                self.down = nb
+        _peer_access(mapped)
+
+    @classmethod
+    def pair(cls, upper: "JacobiSlab", lower: "JacobiSlab"):
+        """Two vertically adjacent slabs in ONE process (tests: their blocks
+        are then driven in turn on one stream, see jacobi_p2p_blocks)."""
+        import torch
+        a, b = cls(_local=True), cls(_local=True)
+        for p, s in ((a, upper), (b, lower)):
+            p.flags = torch.zeros(4, dtype=torch.int32, device=s.A.device)
+        a.down = {"A": lower.A, "flags": b.flags, "top": lower.top, "rows": lower.rows, "bot": lower.bot}
+        b.up = {"A": upper.A, "flags": a.flags, "top": upper.top, "rows": upper.rows, "bot": upper.bot}
+        return a, b
+
+
+def jacobi_p2p_blocks(slab: "JacobiSlab", peer: PeerJacobi, T, coef=0.2, stream=None):
+    """The canonical-stencil schedule of :func:`jacobi` with the fused ghost
+    exchange, one temporal block per ``next()`` (a generator, so a test can
+    interleave two slabs of one process on one stream).  Block b (k steps,
+    src = A[t % 2] -> dst):
+
+      1. wait until both neighbours delivered block b-1's ghost rows into
+         src (flags[0], flags[1] >= b) and finished block b-1 -- the last
+         reader of the ghost rows this block overwrites in their dst
+         (flags[2], flags[3] >= b);
+      2. the edge bands (EDGE rows at each neighbour), their first / last
+         GHOST rows stored into the neighbour's dst ghost rows as well;
+      3. signal the neighbours: ghost rows of block b delivered;
+      4. the interior band;
+      5. signal the neighbours: block b finished.
+    Ghost rows of both planes must hold the initial state (one exchange
+    before the first block, as jacobi() does)."""
+    from . import device
+    A = slab.A
+    top, rows, bot = slab.top, slab.rows, slab.bot
+    lo, hi = top, top + rows
+    e0 = lo + EDGE if top else lo
+    e1 = hi - EDGE if bot else hi
+    up, down = peer.up, peer.down
+    fl = peer.flags
+    t, b = 0, 0
+    while t < T:
+        if T - t > 1:
+            k = min(GHOST, T - 1 - t)
+            k -= (k % 2 == 0)
+        else:
+            k = 1
+        src, dst = A[t % 2], A[(t + 1) % 2]
+        n = peer.base + b  # blocks before this one
+        if b > 0:
+            if up is not None:
+                device.flag_wait(fl.data_ptr(), n, stream)
+                device.flag_wait(fl.data_ptr() + 8, n, stream)
+            if down is not None:
+                device.flag_wait(fl.data_ptr() + 4, n, stream)
+                device.flag_wait(fl.data_ptr() + 12, n, stream)
+        plane = (t + 1) % 2
+        if up is not None:  # my rows [lo, lo + GHOST) -> the rank above's bottom ghost rows
+            ua = up["A"][plane]
+            dst_ptr = ua.data_ptr() + (up["top"] + up["rows"]) * ua.shape[-1] * ua.element_size()
+            device.jacobi2d_band_mirror(src, dst, k, lo, e0, dst_ptr, lo, lo + GHOST, coef, stream)
+        if down is not None:  # my rows [hi - GHOST, hi) -> the rank below's top ghost rows
+            da = down["A"][plane]
+            device.jacobi2d_band_mirror(src, dst, k, e1, hi, da.data_ptr(), hi - GHOST, hi, coef, stream)
+        if up is not None:
+            device.flag_signal(up["flags"].data_ptr() + 4, n + 1, stream)   # its [1]: from below
+        if down is not None:
+            device.flag_signal(down["flags"].data_ptr(), n + 1, stream)     # its [0]: from above
+        device.jacobi2d_band(src, dst, k, e0, e1, coef, stream)
+        if up is not None:
+            device.flag_signal(up["flags"].data_ptr() + 12, n + 1, stream)  # its [3]: below finished
+        if down is not None:
+            device.flag_signal(down["flags"].data_ptr() + 8, n + 1, stream)  # its [2]: above finished
+        t += k
+        b += 1
+        yield b
+    peer.base += b
 
 
 def _ghost_exchange(pg, plane, slab: JacobiSlab, rank, world, wait=True):

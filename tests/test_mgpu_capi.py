@@ -273,3 +273,62 @@ def test_query_p2p_gather_two_processes_one_gpu(cuda_ok):
         assert totals == [sel.size, sel.size]
         assert count == 3 + 2 * sel.size
     np.testing.assert_array_equal(np.sort(res[0][3]), sel)
+
+
+def _numpy_jacobi(A, T):
+    ref = A.copy()
+    for s in range(T):
+        src, dst = ref[s % 2], ref[(s + 1) % 2]
+        acc = src[1:-1, 1:-1] + src[:-2, 1:-1]
+        acc = acc + src[2:, 1:-1]
+        acc = acc + src[1:-1, :-2]
+        acc = acc + src[1:-1, 2:]
+        dst[1:-1, 1:-1] = np.float32(0.2) * acc
+    return ref
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T", [1, 2, 9, 23])
+@pytest.mark.parametrize("nslabs", [2, 3])
+def test_jacobi_fused_p2p_exchange_slabs_in_turn(T, nslabs):
+    """multigpu.jacobi's fused ghost exchange (edge-band kernels storing the
+    neighbours' ghost rows, sdfgb_jacobi2d_band_mirror_f32, ordered by
+    sdfgb_flag_signal / _wait) on slabs of ONE device: every slab's blocks
+    are queued in turn on one stream, so each flag wait is already satisfied
+    when it runs (no kernel ever waits on another).  Bit-exact against the
+    one-plane numpy restatement."""
+    import torch
+    from paper_1902_10345_b200 import multigpu as MG
+    rng = np.random.default_rng(100 + T + nslabs)
+    Ng, N = 64 * nslabs + 37, 260
+    A = np.zeros((2, Ng, N), dtype=np.float32)
+    A[:, 1:-1, 1:-1] = rng.random((Ng - 2, N - 2), dtype=np.float32)
+    ref = _numpy_jacobi(A, T)
+    cuts = [round(i * Ng / nslabs) for i in range(nslabs + 1)]
+    At = t(A)
+    slabs = [MG.jacobi_slab(At[:, a:b], a, Ng) for a, b in zip(cuts, cuts[1:])]
+    # the initial ghost rows of both planes (what jacobi()'s first exchange does)
+    for up, lo in zip(slabs, slabs[1:]):
+        up.A[:, up.top + up.rows:] = lo.A[:, lo.top:lo.top + up.bot]
+        lo.A[:, :lo.top] = up.A[:, up.top + up.rows - lo.top:up.top + up.rows]
+    peers = [MG.PeerJacobi(_local=True) for _ in slabs]
+    for p, s in zip(peers, slabs):
+        p.flags = torch.zeros(4, dtype=torch.int32, device=DEV)
+    for i in range(nslabs - 1):
+        a, b = peers[i], peers[i + 1]
+        s_lo, s_up = slabs[i + 1], slabs[i]
+        a.down = {"A": s_lo.A, "flags": b.flags, "top": s_lo.top, "rows": s_lo.rows, "bot": s_lo.bot}
+        b.up = {"A": s_up.A, "flags": a.flags, "top": s_up.top, "rows": s_up.rows, "bot": s_up.bot}
+    gens = [MG.jacobi_p2p_blocks(s, p, T) for s, p in zip(slabs, peers)]
+    live = list(gens)
+    while live:
+        for g in list(live):
+            try:
+                next(g)
+            except StopIteration:
+                live.remove(g)
+    torch.cuda.synchronize()
+    got = np.concatenate([s.A[:, s.top:s.top + s.rows].cpu().numpy() for s in slabs], axis=1)
+    np.testing.assert_array_equal(got[T % 2], ref[T % 2])
+    np.testing.assert_array_equal(got[(T + 1) % 2][1:-1, 1:-1], ref[(T + 1) % 2][1:-1, 1:-1])
+    assert all(int(p.flags.max()) > 0 for p in peers) or T == 0
