@@ -535,6 +535,10 @@ class Lowering:
         self.devfns: list[str] = []
         self.kcount = 0
         self.tcount = 0
+        # bounds-check hoisting (top_map): accesses recorded while a map body
+        # is emitted, and the mode that emits it without per-access checks
+        self.track = None
+        self.unchecked = False
         self.scoped: dict = {}  # transient -> (state, top entry): thread-sliced per-iteration scratch
         self.private = self._find_private()
         self.consumed = set()
@@ -575,6 +579,10 @@ class Lowering:
         access, interpreter.py:216-233; the C path does not)."""
         d = self.g.data[data]
         return " && ".join(f"(uint64_t)({i}) < (uint64_t)({env.emit(dim)})" for i, dim in zip(idx, d.dims))
+
+    def _track(self, data: str, subset, width: int) -> None:
+        if self.track is not None:
+            self.track.append((data, [r.begin for r in subset]) if width == 1 else None)
 
     def size_expr(self, data: str, env: Env) -> str:
         d = self.g.data[data]
@@ -1005,9 +1013,13 @@ class Lowering:
                 aread[c] = (v, f"({self.size_expr(m.data, env)} - ({self.origin(m.data, m.subset, env)}))")
             else:
                 pt = point(m.subset)
-                out.append(f"{ind2}const {CT[d.basetype]} {v} = ({self.in_bounds(m.data, pt, env)}) ? "
-                           f"{self.cname(m.data)}[{self.flat(m.data, pt, env)}] : "
-                           f"(gen_fail(g_err, 6), ({CT[d.basetype]})0);")
+                self._track(m.data, m.subset, width)
+                if self.unchecked:
+                    out.append(f"{ind2}const {CT[d.basetype]} {v} = {self.cname(m.data)}[{self.flat(m.data, pt, env)}];")
+                else:
+                    out.append(f"{ind2}const {CT[d.basetype]} {v} = ({self.in_bounds(m.data, pt, env)}) ? "
+                               f"{self.cname(m.data)}[{self.flat(m.data, pt, env)}] : "
+                               f"(gen_fail(g_err, 6), ({CT[d.basetype]})0);")
             names[c] = v
         commits = []
         wcounts = []  # (edge, C count of subscript writes) for the report
@@ -1075,8 +1087,10 @@ class Lowering:
                 sub = m.subset if m.data == target.data or m.reindex is None else m.reindex
                 pt = point(sub)
                 lv = f"{self.cname(target.data)}[{self.flat(target.data, pt, env)}]"
-                ok = self.in_bounds(target.data, pt, env)
-                guard = f"{guard}if (!({ok})) gen_fail(g_err, 6); else "
+                self._track(target.data, sub, width)
+                if not self.unchecked:
+                    ok = self.in_bounds(target.data, pt, env)
+                    guard = f"{guard}if (!({ok})) gen_fail(g_err, 6); else "
                 if m.wcr is None:
                     out.append(f"{ind2}{guard}{lv} = {v};")
                 else:
@@ -1197,29 +1211,49 @@ class Lowering:
                         f"n{k} = g_rlen(b{k}, {denv.emit(r.end)}, s{k});")
             lens.append(f"n{k}")
         body.append(f"    const int64_t total = {' * '.join(lens)};")
-        body.append("    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total; "
-                    "f += (int64_t)gridDim.x * blockDim.x) {")
-        body.append("        int64_t rem = f;")
+        head = ["    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total; "
+                "f += (int64_t)gridDim.x * blockDim.x) {", "        int64_t rem = f;"]
         more = {}
         for k in reversed(range(len(n.params))):
             v = f"p_{_ident(n.params[k])}_{n.id}"
             # the outermost index needs no modulo: rem < n0 once the inner ones are divided out
             idx = "rem" if k == 0 else f"(rem % n{k})"
-            body.append(f"        const int64_t {v} = b{k} + {idx} * s{k};")
+            head.append(f"        const int64_t {v} = b{k} + {idx} * s{k};")
             if k:
-                body.append(f"        rem /= n{k};")
+                head.append(f"        rem /= n{k};")
             more[n.params[k]] = v
         penv = denv.child(more)
-        self.instance_counts(st, n, penv, "        ", body)
+        loop = list(head)
+        self.instance_counts(st, n, penv, "        ", loop)
         # private transients: fresh, zeroed per iteration
-        for name in sorted(self.private):
-            if self._owned_by(name, st, parent, n.id):
-                d = self.g.data[name]
-                body.append(f"        {CT[d.basetype]} {self.cname(name)}[{self.static_size(d)}] = {{}};")
+        owned = [name for name in sorted(self.private) if self._owned_by(name, st, parent, n.id)]
+        for name in owned:
+            d = self.g.data[name]
+            loop.append(f"        {CT[d.basetype]} {self.cname(name)}[{self.static_size(d)}] = {{}};")
+        hoist = (not dynamic and not scoped and not owned and self.rep is None
+                 and all(st.nodes[i].kind in ("tasklet", "map_exit") for i in st.topological_order()
+                         if parent[i] == n.id and i != n.id))
         inner: list = []
+        self.track = [] if hoist else None
         self.emit_scope(st, parent, n.id, penv, "        ", inner, True)
-        body += inner
-        body.append("    }")
+        track, self.track = self.track, None
+        safe = self._corner_checks(n, denv, track) if hoist else None
+        if safe:
+            # every access of the body is affine in the map parameters: its
+            # extremes are at the corners of the iteration box, so one check
+            # of the corners per thread replaces the per-access checks
+            unchecked: list = []
+            self.unchecked = True
+            try:
+                self.emit_scope(st, parent, n.id, penv, "        ", unchecked, True)
+            finally:
+                self.unchecked = False
+            body.append(f"    const bool g_safe = {safe};")
+            body.append("    if (g_safe) {")
+            body += head + unchecked + ["    }", "    } else {"]
+            body += loop + inner + ["    }", "    }"]
+        else:
+            body += loop + inner + ["    }"]
         k = self.new_kernel(body, f"{st.name}_map{n.id}")
         self.finish_counts(st, n.id, host_env, "    ", out, host=True)
 
@@ -1243,6 +1277,25 @@ class Lowering:
         out.append("      if (tot > 0) {")
         grow("(int64_t)gen_blocks(tot) * 256")
         out.append(f"      {k}<<<gen_blocks(tot), 256, 0, st>>>({self.kargs()}); GEN_CHECK(); }} }}")
+
+    def _corner_checks(self, n, denv: Env, track) -> Optional[str]:
+        """The in-bounds condition of every recorded access at every corner
+        of the map's iteration box (params at their first / last value), or
+        None when an access is not affine in the parameters."""
+        from itertools import product
+        params = list(n.params)
+        pset = set(params)
+        if not track or any(t is None or not all(_affine_in(b, pset) for b in t[1]) for t in track):
+            return None
+        conds = []
+        for combo in product((0, 1), repeat=len(params)):
+            cenv = denv.child({p: (f"(b{k})" if c == 0 else f"(b{k} + (n{k} - 1) * s{k})")
+                               for k, (p, c) in enumerate(zip(params, combo))})
+            for data, begins in track:
+                c = self.in_bounds(data, [cenv.emit(b) for b in begins], cenv)
+                if c not in conds:
+                    conds.append(c)
+        return " && ".join(f"({c})" for c in conds)
 
     def top_consume(self, st: State, parent: dict, n, out: list) -> None:
         """A consume scope (codegen.py:526-543: P workers popping until the
@@ -1601,6 +1654,20 @@ class Lowering:
 
 def _is_one(e) -> bool:
     return isinstance(e, X.Num) and e.value == 1
+
+
+def _affine_in(e, params: set) -> bool:
+    """e is affine in the symbols ``params`` (other symbols are uniform)."""
+    if isinstance(e, (X.Num, X.Sym)):
+        return True
+    if isinstance(e, X.Neg):
+        return _affine_in(e.arg, params)
+    if isinstance(e, X.Bin) and e.op in ("+", "-"):
+        return _affine_in(e.left, params) and _affine_in(e.right, params)
+    if isinstance(e, X.Bin) and e.op == "*":
+        lf, rf = X.free_symbols(e.left) & params, X.free_symbols(e.right) & params
+        return (not lf and _affine_in(e.right, params)) or (not rf and _affine_in(e.left, params))
+    return not (X.free_symbols(e) & params)
 
 
 def _subscripts(code: ast.Module):

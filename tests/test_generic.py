@@ -56,6 +56,27 @@ def test_lowers(name):
     assert "__global__" in lw.source or "__device__" in lw.source
 
 
+def test_affine_map_bodies_check_their_corners_once():
+    """the laplace map's accesses are affine in its parameter: the kernel
+    checks the iteration box's corners once and runs an unchecked loop when
+    they are in bounds, the per-access checked loop (gen_fail) otherwise"""
+    src = lower(load(_doc("gal_laplace"))).source
+    k = src[src.index("gen_laplace_k0_body_map"):]
+    k = k[:k.index("\n}\n")]
+    assert "const bool g_safe = " in k and "if (g_safe) {" in k
+    fast, slow = k.split("} else {")
+    assert "gen_fail" not in fast.split("if (g_safe) {")[1] and "gen_fail" in slow
+
+
+def test_affine_in():
+    from paper_1902_10345_b200 import expr as X
+    from paper_1902_10345_b200.lower import _affine_in
+    P = {"i", "j"}
+    for text, ok in (("i + 1", True), ("2 * i - j + N", True), ("N * i", True), ("(t % 2) * N + i", True),
+                     ("i * j", False), ("i // 2", False), ("i % N", False), ("min(i, N)", False), ("N // 2 + i", True)):
+        assert _affine_in(X.parse_expr(text), P) is ok, text
+
+
 def test_consume_scope_is_a_work_queue_kernel():
     src = lower(load(_doc("gal_fibonacci"))).source
     assert "stream_push_q" in src and "gen_queue_reset" in src
