@@ -450,16 +450,17 @@ class PeerJacobi:
         _peer_access(mapped)
 
     @classmethod
-    def pair(cls, upper: "JacobiSlab", lower: "JacobiSlab"):
-        """Two vertically adjacent slabs in ONE process (tests: their blocks
-        are then driven in turn on one stream, see jacobi_p2p_blocks)."""
+    def chain(cls, slabs):
+        """Vertically adjacent slabs of ONE process (tests: their blocks are
+        then driven in turn on one stream, see jacobi_p2p_blocks)."""
         import torch
-        a, b = cls(_local=True), cls(_local=True)
-        for p, s in ((a, upper), (b, lower)):
+        peers = [cls(_local=True) for _ in slabs]
+        for p, s in zip(peers, slabs):
             p.flags = torch.zeros(4, dtype=torch.int32, device=s.A.device)
-        a.down = {"A": lower.A, "flags": b.flags, "top": lower.top, "rows": lower.rows, "bot": lower.bot}
-        b.up = {"A": upper.A, "flags": a.flags, "top": upper.top, "rows": upper.rows, "bot": upper.bot}
-        return a, b
+        for (a, up), (b, lo) in zip(zip(peers, slabs), zip(peers[1:], slabs[1:])):
+            a.down = {"A": lo.A, "flags": b.flags, "top": lo.top, "rows": lo.rows, "bot": lo.bot}
+            b.up = {"A": up.A, "flags": a.flags, "top": up.top, "rows": up.rows, "bot": up.bot}
+        return peers
 
 
 def jacobi_p2p_blocks(slab: "JacobiSlab", peer: PeerJacobi, T, coef=0.2, stream=None):

@@ -311,14 +311,7 @@ def test_jacobi_fused_p2p_exchange_slabs_in_turn(T, nslabs):
     for up, lo in zip(slabs, slabs[1:]):
         up.A[:, up.top + up.rows:] = lo.A[:, lo.top:lo.top + up.bot]
         lo.A[:, :lo.top] = up.A[:, up.top + up.rows - lo.top:up.top + up.rows]
-    peers = [MG.PeerJacobi(_local=True) for _ in slabs]
-    for p, s in zip(peers, slabs):
-        p.flags = torch.zeros(4, dtype=torch.int32, device=DEV)
-    for i in range(nslabs - 1):
-        a, b = peers[i], peers[i + 1]
-        s_lo, s_up = slabs[i + 1], slabs[i]
-        a.down = {"A": s_lo.A, "flags": b.flags, "top": s_lo.top, "rows": s_lo.rows, "bot": s_lo.bot}
-        b.up = {"A": s_up.A, "flags": a.flags, "top": s_up.top, "rows": s_up.rows, "bot": s_up.bot}
+    peers = MG.PeerJacobi.chain(slabs)
     gens = [MG.jacobi_p2p_blocks(s, p, T) for s, p in zip(slabs, peers)]
     live = list(gens)
     while live:
