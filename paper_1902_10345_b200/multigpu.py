@@ -367,8 +367,9 @@ def jacobi(pg, slab: JacobiSlab, T, backend, coef=0.2, terms=((0, 0), (-1, 0), (
     if p2p is not None and band:
         for _ in jacobi_p2p_blocks(slab, p2p, T, coef):
             pass
-        import torch
-        torch.cuda.current_stream().synchronize()
+        if A.is_cuda:
+            import torch
+            torch.cuda.current_stream().synchronize()
         pg.barrier()  # no neighbour still writes into this rank's planes
         return
     t = 0
@@ -423,23 +424,35 @@ class PeerJacobi:
     [2] blocks the rank above has finished, [3] blocks the rank below has
     finished.  Counts only grow (``base`` carries them across calls)."""
 
-    def __init__(self, pg=None, slab: "JacobiSlab" = None, _local=None):
+    def __init__(self, pg=None, slab: "JacobiSlab" = None, _local=None, ops=None):
         import torch
         self.base = 0
         self.up = self.down = None
-        if _local is not None:  # one-process construction (tests): see pair()
+        self.ops = ops if ops is not None else DeviceP2POps()
+        if _local is not None:  # one-process construction (tests): see chain()
             return
-        from torch.multiprocessing.reductions import reduce_tensor
+        import io
+        import pickle
+        from multiprocessing.reduction import ForkingPickler
+        import torch.multiprocessing  # noqa: F401  (registers the tensor reductions)
+
+        def export(t):
+            # CUDA: an IPC handle; CPU (tests): a shared-memory segment
+            if not t.is_cuda:
+                t.share_memory_()
+            buf = io.BytesIO()
+            ForkingPickler(buf, pickle.HIGHEST_PROTOCOL).dump(t)
+            return buf.getvalue()
         rank, world = _rank_world(pg)
         self.flags = torch.zeros(4, dtype=torch.int32, device=slab.A.device)
-        mine = (reduce_tensor(slab.A), reduce_tensor(self.flags), slab.top, slab.rows, slab.bot)
+        mine = (export(slab.A), export(self.flags), slab.top, slab.rows, slab.bot)
         allh = [None] * world
         pg.all_gather_object(allh, mine)
         mapped = []
         for r in (rank - 1, rank + 1):
             if 0 <= r < world:
-                (af, aa), (ff, fa), top, rows, bot = allh[r]
-                nb = {"A": af(*aa), "flags": ff(*fa), "top": top, "rows": rows, "bot": bot}
+                a, f, top, rows, bot = allh[r]
+                nb = {"A": pickle.loads(a), "flags": pickle.loads(f), "top": top, "rows": rows, "bot": bot}
                 mapped += [nb["A"], nb["flags"]]
             else:
                 nb = None
@@ -447,7 +460,8 @@ class PeerJacobi:
                 self.up = nb
             else:
                 self.down = nb
-        _peer_access(mapped)
+        if slab.A.is_cuda:
+            _peer_access(mapped)
 
     @classmethod
     def chain(cls, slabs):
@@ -461,6 +475,27 @@ class PeerJacobi:
             a.down = {"A": lo.A, "flags": b.flags, "top": lo.top, "rows": lo.rows, "bot": lo.bot}
             b.up = {"A": up.A, "flags": a.flags, "top": up.top, "rows": up.rows, "bot": up.bot}
         return peers
+
+
+class DeviceP2POps:
+    """The device side of the fused exchange (libsdfgb200); a test can swap
+    in host implementations of the same four operations."""
+
+    def band(self, src, dst, k, r0, r1, coef, stream):
+        from . import device
+        device.jacobi2d_band(src, dst, k, r0, r1, coef, stream)
+
+    def band_mirror(self, src, dst, k, r0, r1, mirror, m0, m1, coef, stream):
+        from . import device
+        device.jacobi2d_band_mirror(src, dst, k, r0, r1, mirror.data_ptr(), m0, m1, coef, stream)
+
+    def signal(self, flag, value, stream):
+        from . import device
+        device.flag_signal(flag.data_ptr(), value, stream)
+
+    def wait(self, flag, value, stream):
+        from . import device
+        device.flag_wait(flag.data_ptr(), value, stream)
 
 
 def jacobi_p2p_blocks(slab: "JacobiSlab", peer: PeerJacobi, T, coef=0.2, stream=None):
@@ -480,7 +515,7 @@ def jacobi_p2p_blocks(slab: "JacobiSlab", peer: PeerJacobi, T, coef=0.2, stream=
       5. signal the neighbours: block b finished.
     Ghost rows of both planes must hold the initial state (one exchange
     before the first block, as jacobi() does)."""
-    from . import device
+    ops = peer.ops
     A = slab.A
     top, rows, bot = slab.top, slab.rows, slab.bot
     lo, hi = top, top + rows
@@ -499,28 +534,26 @@ def jacobi_p2p_blocks(slab: "JacobiSlab", peer: PeerJacobi, T, coef=0.2, stream=
         n = peer.base + b  # blocks before this one
         if b > 0:
             if up is not None:
-                device.flag_wait(fl.data_ptr(), n, stream)
-                device.flag_wait(fl.data_ptr() + 8, n, stream)
+                ops.wait(fl[0:1], n, stream)
+                ops.wait(fl[2:3], n, stream)
             if down is not None:
-                device.flag_wait(fl.data_ptr() + 4, n, stream)
-                device.flag_wait(fl.data_ptr() + 12, n, stream)
+                ops.wait(fl[1:2], n, stream)
+                ops.wait(fl[3:4], n, stream)
         plane = (t + 1) % 2
         if up is not None:  # my rows [lo, lo + GHOST) -> the rank above's bottom ghost rows
-            ua = up["A"][plane]
-            dst_ptr = ua.data_ptr() + (up["top"] + up["rows"]) * ua.shape[-1] * ua.element_size()
-            device.jacobi2d_band_mirror(src, dst, k, lo, e0, dst_ptr, lo, lo + GHOST, coef, stream)
+            g = up["top"] + up["rows"]
+            ops.band_mirror(src, dst, k, lo, e0, up["A"][plane][g:g + GHOST], lo, lo + GHOST, coef, stream)
         if down is not None:  # my rows [hi - GHOST, hi) -> the rank below's top ghost rows
-            da = down["A"][plane]
-            device.jacobi2d_band_mirror(src, dst, k, e1, hi, da.data_ptr(), hi - GHOST, hi, coef, stream)
+            ops.band_mirror(src, dst, k, e1, hi, down["A"][plane][0:GHOST], hi - GHOST, hi, coef, stream)
         if up is not None:
-            device.flag_signal(up["flags"].data_ptr() + 4, n + 1, stream)   # its [1]: from below
+            ops.signal(up["flags"][1:2], n + 1, stream)    # its [1]: delivered from below
         if down is not None:
-            device.flag_signal(down["flags"].data_ptr(), n + 1, stream)     # its [0]: from above
-        device.jacobi2d_band(src, dst, k, e0, e1, coef, stream)
+            ops.signal(down["flags"][0:1], n + 1, stream)  # its [0]: delivered from above
+        ops.band(src, dst, k, e0, e1, coef, stream)
         if up is not None:
-            device.flag_signal(up["flags"].data_ptr() + 12, n + 1, stream)  # its [3]: below finished
+            ops.signal(up["flags"][3:4], n + 1, stream)    # its [3]: below finished
         if down is not None:
-            device.flag_signal(down["flags"].data_ptr() + 8, n + 1, stream)  # its [2]: above finished
+            ops.signal(down["flags"][2:3], n + 1, stream)  # its [2]: above finished
         t += k
         b += 1
         yield b

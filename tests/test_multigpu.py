@@ -82,7 +82,8 @@ def _free_port():
     return p
 
 
-CASES = ["histogram", "query", "spmv", "jacobi", "jacobi_overlap", "gemm", "gemm_uneven", "strong_shares"]
+CASES = ["histogram", "query", "spmv", "jacobi", "jacobi_overlap", "jacobi_p2p", "gemm", "gemm_uneven",
+         "strong_shares"]
 
 
 def _worker(rank, world, port, names, q):
@@ -239,6 +240,61 @@ def _case_jacobi_overlap(rank, world):
     MG.jacobi(dist, slab, T, be)
     got = slab.A[:, slab.top:slab.top + (hi - lo)].numpy()
     return bool(calls) and bool(np.array_equal(got, ref[:, lo:hi]))
+
+
+class HostP2POps:
+    """The fused exchange's four device operations on shared CPU tensors
+    (test only): the band through the oracle backend, the mirror as a row
+    copy into the neighbour's (shared-memory) plane, the flags as words of
+    a shared tensor that the waiting rank polls."""
+
+    def band(self, src, dst, k, r0, r1, coef, stream):
+        OracleBackend().jacobi_band(src, dst, k, r0, r1, coef)
+
+    def band_mirror(self, src, dst, k, r0, r1, mirror, m0, m1, coef, stream):
+        self.band(src, dst, k, r0, r1, coef, stream)
+        a, b = max(r0, m0, 1), min(r1, m1, dst.shape[0] - 1)
+        if b > a:
+            mirror[a - m0:b - m0] = dst[a:b]
+
+    def signal(self, flag, value, stream):
+        flag.fill_(value)
+
+    def wait(self, flag, value, stream):
+        import time
+        t0 = time.time()
+        while int(flag.item()) < value:
+            if time.time() - t0 > 60:
+                raise TimeoutError(f"flag stuck at {int(flag.item())} < {value}")
+            time.sleep(1e-4)
+
+
+def _case_jacobi_p2p(rank, world):
+    """The fused ghost exchange (multigpu.PeerJacobi: mirrored edge bands and
+    flag words, no collective) across processes, its planes and flags in
+    shared memory mapped through pg like the CUDA IPC handles: equals the
+    restatement, with every neighbour's waits really waiting."""
+    rng = np.random.default_rng(8)
+    Ng, N, T = 61 * world + 5, 20, 23
+    A = rng.random((2, Ng, N), dtype=np.float32)
+    ref = A.copy()
+    for t in range(T):
+        s_, d_ = ref[t % 2], ref[(t + 1) % 2]
+        acc = s_[1:-1, 1:-1] + s_[0:-2, 1:-1]
+        acc = acc + s_[2:, 1:-1]
+        acc = acc + s_[1:-1, 0:-2]
+        acc = acc + s_[1:-1, 2:]
+        d_[1:-1, 1:-1] = np.float32(0.2) * acc
+    # CPU storages cross processes by shared-memory file name here (the
+    # handles travel through pg's pickles, as CUDA IPC handles do)
+    torch.multiprocessing.set_sharing_strategy("file_system")
+    lo, hi = MG.share(Ng, rank, world)
+    slab = MG.jacobi_slab(torch.from_numpy(A[:, lo:hi].copy()), lo, Ng)
+    peer = MG.PeerJacobi(dist, slab, ops=HostP2POps())
+    MG.jacobi(dist, slab, T, OracleBackend(), p2p=peer)
+    got = slab.A[:, slab.top:slab.top + (hi - lo)].numpy()
+    # a second call continues the flag counts (peer.base)
+    return bool(np.array_equal(got, ref[:, lo:hi])) and peer.base > 0
 
 
 def _case_gemm_uneven(rank, world):
