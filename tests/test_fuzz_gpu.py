@@ -52,6 +52,30 @@ def test_query_fuzz(seed, cuda_ok):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(4 * SCALE))
+def test_query_ordered_multi_piece_fuzz(seed, cuda_ok):
+    """FIFO order across several of the piece kernel's 16 MB pieces: random
+    sizes (1-7 pieces, ragged tails), offsets, operators and thresholds"""
+    import torch
+    from paper_1902_10345_b200 import device
+    rng = np.random.default_rng(5000 + seed)
+    dtype = np.float32 if rng.random() < 0.7 else np.float64
+    n = int(rng.integers(1, 7 * (16 << 20) // np.dtype(dtype).itemsize))
+    off = int(rng.integers(0, 4)) * (16 // np.dtype(dtype).itemsize)  # 16 B-aligned views: the piece kernel
+    base = (rng.random(n + off) * 4 - 2).astype(dtype)
+    col = base[off:]
+    op = OPS[int(rng.integers(0, 6))]
+    thr = float(rng.choice([0.25, 0.0, -1.5, 1.9, -2.5]))
+    dcol = t(base)[off:]
+    out = torch.zeros(n, dtype=dcol.dtype, device=DEV)
+    cnt = torch.full((1,), 5, dtype=torch.int64, device=DEV)
+    device.query(dcol, thr, out, cnt, device.query_workspace(n, col.itemsize, DEV), op, ordered=True)
+    exp, ecnt = oracle.query(col, thr, np.zeros(n, dtype), np.array([5], np.int64), op)
+    assert int(cnt.item()) == int(ecnt[0]), (n, op, thr)
+    np.testing.assert_array_equal(out.cpu().numpy(), exp)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("seed", range(12 * SCALE))
 def test_histogram_fuzz(seed, cuda_ok):
     import torch
