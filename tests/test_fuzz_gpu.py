@@ -208,3 +208,45 @@ def test_jacobi_strip_fuzz(seed, cuda_ok):
             device.jacobi2d_band(banded[0], banded[1], k, r0, r1)
         np.testing.assert_array_equal(banded.cpu().numpy(), whole.cpu().numpy(),
                                       err_msg=f"bands M={M} N={N} k={k} cuts={e0},{e1}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(3 * SCALE))
+def test_jacobi_fused_p2p_slabs_fuzz(seed, cuda_ok):
+    """the fused ghost exchange (multigpu.PeerJacobi) on 2-4 slabs of one
+    device, blocks queued in turn on one stream: random grid shapes and step
+    counts, bit-exact against the one-plane numpy restatement"""
+    import torch
+    from paper_1902_10345_b200 import multigpu as MG
+    rng = np.random.default_rng(7000 + seed)
+    nslabs = int(rng.integers(2, 5))
+    Ng = int(rng.integers(50 * nslabs, 160 * nslabs))
+    N = 4 * int(rng.integers(33, 150))
+    T = int(rng.integers(1, 40))
+    A = np.zeros((2, Ng, N), dtype=np.float32)
+    A[:, 1:-1, 1:-1] = rng.random((Ng - 2, N - 2), dtype=np.float32)
+    ref = A.copy()
+    for s_ in range(T):
+        src, dst = ref[s_ % 2], ref[(s_ + 1) % 2]
+        acc = src[1:-1, 1:-1] + src[:-2, 1:-1]
+        acc = acc + src[2:, 1:-1]
+        acc = acc + src[1:-1, :-2]
+        acc = acc + src[1:-1, 2:]
+        dst[1:-1, 1:-1] = np.float32(0.2) * acc
+    cuts = [round(i * Ng / nslabs) for i in range(nslabs + 1)]
+    At = t(A)
+    slabs = [MG.jacobi_slab(At[:, a:b], a, Ng) for a, b in zip(cuts, cuts[1:])]
+    for up, lo in zip(slabs, slabs[1:]):
+        up.A[:, up.top + up.rows:] = lo.A[:, lo.top:lo.top + up.bot]
+        lo.A[:, :lo.top] = up.A[:, up.top + up.rows - lo.top:up.top + up.rows]
+    peers = MG.PeerJacobi.chain(slabs)
+    live = [MG.jacobi_p2p_blocks(s_, p, T) for s_, p in zip(slabs, peers)]
+    while live:
+        for g in list(live):
+            try:
+                next(g)
+            except StopIteration:
+                live.remove(g)
+    torch.cuda.synchronize()
+    got = np.concatenate([s_.A[:, s_.top:s_.top + s_.rows].cpu().numpy() for s_ in slabs], axis=1)
+    np.testing.assert_array_equal(got[T % 2], ref[T % 2], err_msg=f"{Ng}x{N} T={T} slabs={nslabs}")
