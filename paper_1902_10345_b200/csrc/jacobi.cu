@@ -547,6 +547,9 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* dst_in,
 #ifndef SDFGB_JSP_F32X2
 #define SDFGB_JSP_F32X2 0
 #endif
+#ifndef SDFGB_JSP_MINB
+#define SDFGB_JSP_MINB 4  // resident CTAs per SM the strip kernel is compiled for (128 registers)
+#endif
 #ifndef SDFGB_JSP_L0REG
 #define SDFGB_JSP_L0REG 1  // level 0 kept in the register window (1 LDS per row instead of 3; 19.43 -> 19.2 ms per J1 loop)
 #endif
@@ -630,7 +633,7 @@ std::atomic<int> g_sp_launches{0};
 // into a neighbour rank's ghost rows over NVLink (peer memory), so a slab's
 // edge band and its ghost-row transfer are one kernel (multigpu.jacobi, p2p)
 template <int F, bool MIRROR = false>
-__global__ void __launch_bounds__(kSpWarps * 32, 4)
+__global__ void __launch_bounds__(kSpWarps * 32, SDFGB_JSP_MINB)
 jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* src, const float* dst_in,
                     float* dst, int M, int N, StripPlan plan, int nwarps, int sched_slot, float coef,
                     int64_t moff, int mr0, int mr1) {
@@ -996,7 +999,7 @@ int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra,
                  cudaStream_t s, int64_t moff = 0, int mr0 = 0, int mr1 = 0) {
     const int64_t nstrips = (N + kSpX - 1) / kSpX;
     // persistent: one co-resident wave of warps (4 CTAs x 4 warps per SM)
-    const int64_t resident = (int64_t)num_sms() * 4 * kSpWarps;
+    const int64_t resident = (int64_t)num_sms() * SDFGB_JSP_MINB * kSpWarps;
     const StripPlan plan = strip_plan(ra, rb, nstrips, resident);
     const size_t smem = sp_smem(plan.hmax + 2 * F);
     static size_t attr = 0;
