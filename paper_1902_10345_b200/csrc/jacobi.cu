@@ -547,6 +547,9 @@ jacobi_tb_kernel(const __grid_constant__ CUtensorMap src, const float* dst_in,
 #ifndef SDFGB_JSP_F32X2
 #define SDFGB_JSP_F32X2 0
 #endif
+#ifndef SDFGB_JSP_PDL
+#define SDFGB_JSP_PDL 1  // programmatic dependent launch between consecutive strip launches
+#endif
 #ifndef SDFGB_JSP_MINB
 #define SDFGB_JSP_MINB 4  // resident CTAs per SM the strip kernel is compiled for (128 registers)
 #endif
@@ -645,6 +648,11 @@ jacobi_strip_kernel(const __grid_constant__ CUtensorMap src_map, const float* sr
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = blockIdx.x * kSpWarps + warp;
     if (g >= nwarps) return;  // warp-uniform; warps never synchronise with each other
+#if SDFGB_JSP_PDL
+    // programmatic dependent launch: the CTA launch overlaps the previous
+    // kernel's end; nothing is read or written before it has completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     int* sched = g_sp_sched + 2 * sched_slot;
     const int nstrips = plan.nstrips;
     const int RP = sp_rows(plan.hmax + 2 * F);  // border-column rows per plane, as sized on the host
@@ -1022,8 +1030,22 @@ int launch_strip(const float* src, float* dst, int64_t M, int64_t N, int64_t ra,
     const int64_t nwarps = std::min<int64_t>(plan.total(), (int64_t)num_sms() * per_sm * kSpWarps);
     const unsigned blocks = (unsigned)((nwarps + kSpWarps - 1) / kSpWarps);
     const int slot = g_sp_launches.fetch_add(1) & (kSpSchedSlots - 1);
-    jacobi_strip_kernel<F, MIRROR><<<blocks, kSpWarps * 32, smem, s>>>(map, src, dst, dst, (int)M, (int)N, plan,
-                                                                       (int)nwarps, slot, coef, moff, mr0, mr1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kSpWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = SDFGB_JSP_PDL;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    const float* dsrc = src;
+    float* ddst = dst;
+    const float* din = dst;
+    int Mi = (int)M, Ni = (int)N, nw = (int)nwarps;
+    SDFGB_CUDA(cudaLaunchKernelEx(&cfg, jacobi_strip_kernel<F, MIRROR>, map, dsrc, din, ddst, Mi, Ni, plan, nw, slot,
+                                  coef, moff, mr0, mr1));
     SDFGB_LAUNCHED("jacobi_strip_kernel");
     return SDFGB_OK;
 }
