@@ -202,6 +202,23 @@ static int gen_blocks(int64_t total) {
     if (b > 148 * 16) b = 148 * 16;
     return (int)b;
 }
+// A map kernel launched with programmatic dependent launch: its CTAs are
+// scheduled while the previous kernel of the stream drains; every generated
+// kernel starts with griddepcontrol.wait, so nothing is read or written
+// before that kernel has completed.
+template <typename... P, typename... A>
+static cudaError_t gen_launch(void (*k)(P...), int grid, int block, cudaStream_t st, A... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.stream = st;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
 // Keep stream-ordered allocations cached between runs: with the default
 // release threshold (0) every synchronize hands the pool back to the driver
 // and the next cudaMallocAsync pays a real allocation (ms-scale, variable).
@@ -1188,8 +1205,9 @@ class Lowering:
     def new_kernel(self, body: list, tag: str) -> str:
         name = f"{self.prefix}_k{self.kcount}_{_ident(tag)}"
         self.kcount += 1
+        wait = '    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the previous kernel is done'
         self.kernels.append(f"__global__ void __launch_bounds__(256) {name}({self.kparams()}) {{\n"
-                            + "\n".join(body) + "\n}\n")
+                            + "\n".join([wait] + body) + "\n}\n")
         return name
 
     def top_map(self, st: State, parent: dict, n, host_env: Env, out: list) -> None:
@@ -1276,7 +1294,8 @@ class Lowering:
         out.append(f"    {{ const int64_t tot = {tot};")
         out.append("      if (tot > 0) {")
         grow("(int64_t)gen_blocks(tot) * 256")
-        out.append(f"      {k}<<<gen_blocks(tot), 256, 0, st>>>({self.kargs()}); GEN_CHECK(); }} }}")
+        args = self.kargs()
+        out.append(f"      gen_launch({k}, gen_blocks(tot), 256, st{', ' + args if args else ''}); GEN_CHECK(); }} }}")
 
     def _corner_checks(self, n, denv: Env, track) -> Optional[str]:
         """The in-bounds condition of every recorded access at every corner
