@@ -402,6 +402,9 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on th
         : "memory");
 }
 
+#ifndef SDFGB_GEMM_PDL
+#define SDFGB_GEMM_PDL 1  // programmatic dependent launch of the pair kernel after the split pre-pass
+#endif
 #ifndef SDFGB_GEMM_AREUSE
 #define SDFGB_GEMM_AREUSE 1  // A-collector reuse between the two A-hi MMAs of a K = 8 step
 #endif
@@ -487,6 +490,12 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_c
     tc_fence_before();
     __syncthreads();
     pair_sync();  // the peer's barriers are initialised before any load signals them
+#if SDFGB_GEMM_PDL
+    // programmatic dependent launch: the set-up above (barriers, TMEM,
+    // descriptor prefetch) overlapped the split pre-pass; its output is read
+    // only from here on
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     tc_fence_after();
     const uint32_t tmem_d = *tmem_slot;
 
@@ -896,6 +905,25 @@ int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, c
 }
 
 // C = A x B with B already split (gemm_split_b); Ahi / Alo hold M x K each
+// The pair kernel with programmatic dependent launch (SDFGB_GEMM_PDL): its
+// CTAs start while the split pre-pass drains (the kernel waits on it with
+// griddepcontrol.wait before its first load).
+template <typename K>
+int launch_pair(K kern, unsigned grid, cudaStream_t s, const CUtensorMap& a, const CUtensorMap& b,
+                const CUtensorMap& c, const CUtensorMap& d, float* C, int M, int N, int Kd) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = GEMM2_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = SDFGB_GEMM_PDL;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    return check_cuda(cudaLaunchKernelEx(&cfg, kern, a, b, c, d, C, M, N, Kd), "gemm pair launch");
+}
+
 int gemm_f32_presplit(const float* A, const GemmB& b, float* C, int64_t M, int64_t N, int64_t K, float* Ahi,
                       float* Alo, cudaStream_t s) {
     const float* Bhi = b.hi;
@@ -931,13 +959,13 @@ int gemm_f32_presplit(const float* A, const GemmB& b, float* C, int64_t M, int64
                                                                      : CU_TENSOR_MAP_SWIZZLE_128B;
             SDFGB_TRY(encode_tiled_2d(&mBhi, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Bhi, K, N, 32, BK, sw));
             SDFGB_TRY(encode_tiled_2d(&mBlo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Blo, K, N, 32, BK, sw));
-            gemm_3xtf32_pair_kernel<true><<<(unsigned)(2 * pairs), GEMM_THREADS, GEMM2_SMEM, s>>>(
-                mAhi, mAlo, mBhi, mBlo, C, (int)M, (int)N, (int)K);
+            SDFGB_TRY(launch_pair(gemm_3xtf32_pair_kernel<true>, (unsigned)(2 * pairs), s, mAhi, mAlo, mBhi, mBlo, C,
+                                  (int)M, (int)N, (int)K));
         } else {
             SDFGB_TRY(make_kmajor_map(&mBhi, Bhi, N, K, BHALF));
             SDFGB_TRY(make_kmajor_map(&mBlo, Blo, N, K, BHALF));
-            gemm_3xtf32_pair_kernel<false><<<(unsigned)(2 * pairs), GEMM_THREADS, GEMM2_SMEM, s>>>(
-                mAhi, mAlo, mBhi, mBlo, C, (int)M, (int)N, (int)K);
+            SDFGB_TRY(launch_pair(gemm_3xtf32_pair_kernel<false>, (unsigned)(2 * pairs), s, mAhi, mAlo, mBhi, mBlo, C,
+                                  (int)M, (int)N, (int)K));
         }
         SDFGB_LAUNCHED("gemm_3xtf32_pair_kernel");
         return SDFGB_OK;
