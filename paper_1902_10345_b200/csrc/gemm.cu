@@ -67,17 +67,37 @@ __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float(r);
 }
 
+#ifndef SDFGB_GEMM_PDL
+#define SDFGB_GEMM_PDL 1  // programmatic dependent launch: split pre-pass and pair kernel
+#endif
 #ifndef SDFGB_GEMM_RAW_AHI
 #define SDFGB_GEMM_RAW_AHI 1  // 4096^3: 0.592 -> 0.584 ms, same error class (profiles/r2_gemm_variants.txt)
 #endif
 // A's hi part read straight from A (the tensor core keeps the top 19 bits of
 // a kind::tf32 operand, i.e. truncates): only lo = a - trunc_tf32(a) is written
 __global__ void split_lo_kernel(const float4* __restrict__ A, float4* __restrict__ lo, int64_t n4) {
+#if SDFGB_GEMM_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the previous kernel (a GEMM reading lo) is done
+#endif
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         const float4 a = A[i];
         auto l = [](float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); };
         lo[i] = make_float4(l(a.x), l(a.y), l(a.z), l(a.w));
     }
+}
+
+// the lo pre-pass with programmatic dependent launch (SDFGB_GEMM_PDL)
+int launch_split(const float4* a, float4* lo, int64_t n4, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(num_sms() * 8));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = SDFGB_GEMM_PDL;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    return check_cuda(cudaLaunchKernelEx(&cfg, split_lo_kernel, a, lo, n4), "split_lo launch");
 }
 
 __global__ void split_rows_kernel(const float* __restrict__ A, float* __restrict__ hi,
@@ -402,9 +422,6 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on th
         : "memory");
 }
 
-#ifndef SDFGB_GEMM_PDL
-#define SDFGB_GEMM_PDL 1  // programmatic dependent launch of the pair kernel after the split pre-pass
-#endif
 #ifndef SDFGB_GEMM_AREUSE
 #define SDFGB_GEMM_AREUSE 1  // A-collector reuse between the two A-hi MMAs of a K = 8 step
 #endif
@@ -885,8 +902,7 @@ GemmB gemm_b_operands(const float* B, float* Bhi, float* Blo, int64_t K, int64_t
 int gemm_split_b(const float* B, float* Bhi, float* Blo, int64_t K, int64_t N, cudaStream_t s, GemmB* out) {
     if (gemm_b_mn(B, Blo, K, N)) {
         // MN-major: B's hi is B itself (tensor-core truncation), only lo is written, untransposed
-        split_lo_kernel<<<num_sms() * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(B), reinterpret_cast<float4*>(Blo),
-                                                      K * N / 4);
+        SDFGB_TRY(launch_split(reinterpret_cast<const float4*>(B), reinterpret_cast<float4*>(Blo), K * N / 4, s));
         SDFGB_LAUNCHED("split_lo_kernel");
         *out = {B, Blo, true};
         return SDFGB_OK;
@@ -930,8 +946,7 @@ int gemm_f32_presplit(const float* A, const GemmB& b, float* C, int64_t M, int64
     const float* Blo = b.lo;
     CUtensorMap mAhi, mAlo, mBhi, mBlo;
     if (SDFGB_GEMM_RAW_AHI && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Alo)) & 15) == 0) {
-        split_lo_kernel<<<num_sms() * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(A), reinterpret_cast<float4*>(Alo),
-                                                      M * K / 4);
+        SDFGB_TRY(launch_split(reinterpret_cast<const float4*>(A), reinterpret_cast<float4*>(Alo), M * K / 4, s));
         SDFGB_LAUNCHED("split_lo_kernel");
         SDFGB_TRY(make_kmajor_map(&mAhi, A, M, K));
     } else {
